@@ -1,0 +1,178 @@
+/*
+ * dictmerge.h -- C ABI of libdictmerge, a B200-native (sm_100a) implementation
+ * of the online merge for dictionary-encoded column stores of Krueger et al.,
+ * "Fast Updates on Read-Optimized Databases Using Multi-Core CPUs"
+ * (arXiv 1109.6885, PVLDB 5(1)).  "P:n" = line n of the paper text.
+ *
+ * What one merge computes (Sec 5).  Per column, inputs are the main
+ * partition -- a sorted dictionary U_M and the bit-packed code
+ * vector M whose codes are positions in U_M -- and the delta partition D, raw
+ * values in insertion order.  Outputs are the merged dictionary
+ * U' = sorted distinct (U_M u D) (Eq 3) and the merged code vector M' of
+ * N' = N_M + N_D rows (Eq 2): main rows first, then delta rows in
+ * insertion order, each the position of its value in U', packed at
+ * the new width b' = ceil(log2 |U'|) (Eq 4).  The path is the paper's
+ * optimized merge:
+ *   Step 1(a)  sorted distinct delta values U_D and per-tuple ranks
+ *   Step 1(b)  merge U_M with U_D, dropping duplicates, emitting the
+ *              translation tables X_M (old main code -> new code) and X_D
+ *              (delta-dictionary rank -> new code)
+ *   Step 2(a)  b' = ceil(log2 |U'|)                            (Eq 4)
+ *   Step 2(b)  M'[i] = X_M[M[i]] for main rows (Eq 11), and the delta
+ *              rows appended through X_D.
+ *
+ * Conventions (DESIGN.md "Readings" A1-A5):
+ *   - width(n) = max(1, ceil(log2 n)); width(0) = width(1) = 1.
+ *   - codes are 0-based dictionary positions.
+ *   - a packed code vector of n codes at b bits (1 <= b <= 32) is an LSB-first
+ *     bitstream held in little-endian u64 words: code i occupies stream bits
+ *     [i*b, (i+1)*b), stream bit s is bit s%64 of word s/64.  Exactly
+ *     dm_words(n, b) words are significant and their pad bits are zero.
+ *   - DM_KEY_U64 keys are little-endian u64 compared as unsigned integers.
+ *     DM_KEY_B16 keys are 16 raw bytes compared bytewise (memcmp) over all 16
+ *     bytes; zero padding takes part in the order.
+ *
+ * Memory and ownership.  Every pointer in dm_column_in / dm_column_out is a
+ * DEVICE pointer (current CUDA device) unless the function says "host".  The
+ * caller allocates every buffer (PyTorch in the Python binding) and owns it;
+ * the library never frees caller memory and never writes its inputs.  All
+ * device buffers must be 16-byte aligned.  One workspace (dm_workspace_bytes)
+ * per concurrent call.  Calls are stream-ordered on the given cudaStream_t
+ * (NULL = legacy default stream).
+ *
+ * Errors.  Host-detectable argument errors return before any launch.
+ * Data-dependent errors (a main code >= |U_M|, an unsorted main dictionary,
+ * |U'| > 2^32) are detected on the device, recorded in dm_header.status and
+ * returned by the synchronous entry points; outputs are then unspecified but
+ * the inputs are untouched (outputs always go to separate buffers, so a
+ * failed merge leaves the table as it was).
+ */
+#ifndef DICTMERGE_H
+#define DICTMERGE_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  DM_OK = 0,
+  DM_E_INVALID = -1,     /* bad argument: NULL, misaligned, width out of range, ... */
+  DM_E_CAPACITY = -2,    /* an output or workspace capacity is too small          */
+  DM_E_TOO_WIDE = -3,    /* |U'| > 2^32: b' would exceed 32 bits                   */
+  DM_E_UNSORTED = -4,    /* main dictionary not strictly increasing               */
+  DM_E_CODE_RANGE = -5,  /* some main code >= |U_M|                               */
+  DM_E_CUDA = -6,        /* a CUDA runtime call failed (dm_last_cuda_error)       */
+  DM_E_NCCL = -7         /* reserved for the sharded variant                      */
+} dm_status;
+
+typedef enum { DM_KEY_U64 = 0, DM_KEY_B16 = 1 } dm_key;
+
+/* One column's merge inputs.  All device pointers, read-only. */
+typedef struct {
+  int32_t key;                  /* dm_key                                            */
+  const void* main_dict;        /* U_M: dict_len keys, strictly increasing           */
+  uint64_t dict_len;            /* |U_M|  (< 2^32)                                   */
+  const uint64_t* main_codes;   /* M: dm_words(n_main, main_bits) words              */
+  uint64_t n_main;              /* N_M                                               */
+  uint32_t main_bits;           /* b: width(dict_len) <= b <= 32 (reading A15)       */
+  const void* delta;            /* D: n_delta keys, insertion order                  */
+  uint64_t n_delta;             /* N_D  (< 2^30)                                     */
+} dm_column_in;
+
+/* One column's merge outputs: caller-allocated device buffers. */
+typedef struct {
+  void* merged_dict;               /* U': capacity merged_dict_cap keys               */
+  uint64_t merged_dict_cap;        /* >= dict_len + n_delta                           */
+  uint64_t* merged_codes;          /* M': capacity merged_codes_cap_words u64 words   */
+  uint64_t merged_codes_cap_words; /* >= dm_merged_codes_cap_words(in)                */
+  uint32_t* x_main;                /* optional (NULL = workspace): X_M, dict_len u32  */
+  uint32_t* x_delta;               /* optional: X_D, capacity n_delta u32 (|U_D| used) */
+  void* delta_dict;                /* optional: U_D, capacity n_delta keys            */
+  uint32_t* delta_rank;            /* optional: r[k] = rank of D[k] in U_D, n_delta   */
+  /* results, written (host side) by the synchronous entry points */
+  uint64_t merged_dict_len;        /* |U'|                                            */
+  uint64_t delta_dict_len;         /* |U_D|                                           */
+  uint32_t merged_bits;            /* b'                                              */
+} dm_column_out;
+
+/* Result header, written on the device by dm_merge_column_async. */
+typedef struct {
+  uint64_t merged_dict_len;  /* |U'|                       */
+  uint64_t delta_dict_len;   /* |U_D|                      */
+  uint32_t merged_bits;      /* b'                         */
+  int32_t status;            /* 0 or a negative dm_status  */
+} dm_header;
+
+/* width(n) = max(1, ceil(log2 n)) (Eq 4; reading A1).  Host, pure. */
+uint32_t dm_width(uint64_t n);
+/* ceil(n*bits/64): significant u64 words of a packed vector.  Host, pure. */
+uint64_t dm_words(uint64_t n, uint32_t bits);
+/* dm_words(n_main + n_delta, width(dict_len + n_delta)): an M' capacity that
+ * fits every possible merge result of `in`.  Host, pure. */
+uint64_t dm_merged_codes_cap_words(const dm_column_in* in);
+/* Workspace bytes needed by dm_merge_column[_async] for `in`.  Host, pure. */
+size_t dm_workspace_bytes(const dm_column_in* in);
+
+/* Merge one column, stream-ordered, without any host synchronisation
+ * (capturable in a CUDA graph).  Results land in *d_header (device memory,
+ * 16-byte aligned) when the stream reaches that point.  Returns DM_OK or a
+ * host-detectable error; data-dependent errors appear in d_header->status. */
+dm_status dm_merge_column_async(const dm_column_in* in, const dm_column_out* out, void* ws, size_t ws_bytes,
+                                dm_header* d_header, void* cuda_stream);
+
+/* As dm_merge_column_async, and additionally records four caller-created
+ * cudaEvent_t on the stream: events[0] before Step 1(a) (workspace reset
+ * included), events[1] before Step 1(b), events[2] before Step 2(b),
+ * events[3] after Step 2(b).  Used to time each step on the launching stream. */
+dm_status dm_merge_column_async_ev(const dm_column_in* in, const dm_column_out* out, void* ws, size_t ws_bytes,
+                                   dm_header* d_header, void* cuda_stream, void* const* events);
+
+/* As above, then waits for the stream and fills out->merged_dict_len,
+ * out->delta_dict_len, out->merged_bits; returns the device status. */
+dm_status dm_merge_column(const dm_column_in* in, dm_column_out* out, void* ws, size_t ws_bytes, void* cuda_stream);
+
+/* Merge `ncols` independent columns (a wide table) on one device
+ * and stream.  ws[c] / ws_bytes[c] is column c's workspace.  Synchronous. */
+dm_status dm_merge_table(int ncols, const dm_column_in* in, dm_column_out* out, void* const* ws,
+                         const size_t* ws_bytes, void* cuda_stream);
+
+/* Step 2(b) alone (Eq 11): given translation tables, write
+ * M'[i] = x_main[M[i]] for i < n_main and M'[n_main + k] = x_delta[delta_rank[k]]
+ * for k < n_delta, packed at new_bits (1..32) into dm_words(n_main + n_delta,
+ * new_bits) words of out_codes (capacity out_cap_words).  Every table value must
+ * be < 2^new_bits.  main_codes at main_bits (1..32), codes < dict_len (else
+ * DM_E_CODE_RANGE, reported after a stream synchronisation).  Device pointers,
+ * 16-byte aligned.  Synchronous. */
+dm_status dm_recompress(const uint64_t* main_codes, uint64_t n_main, uint32_t main_bits, uint64_t dict_len,
+                        const uint32_t* x_main, const uint32_t* x_delta, const uint32_t* delta_rank,
+                        uint64_t n_delta, uint32_t new_bits, uint64_t* out_codes, uint64_t out_cap_words,
+                        void* cuda_stream);
+
+/* Pack n u32 codes (each < 2^bits) into dm_words(n, bits) words at `bits`
+ * (device pointers; words need not be zeroed).  Stream-ordered. */
+dm_status dm_pack_codes(const uint32_t* codes, uint64_t n, uint32_t bits, uint64_t* words, void* cuda_stream);
+/* Unpack n codes at `bits` into u32.  Stream-ordered. */
+dm_status dm_unpack_codes(const uint64_t* words, uint64_t n, uint32_t bits, uint32_t* codes, void* cuda_stream);
+
+/* Host-buffer entry point (end-to-end use).  `in` and `out` hold HOST pointers
+ * (pinned memory gives full PCIe bandwidth); the context owns device staging
+ * buffers, grows them on demand and reuses them across calls.  Copies the
+ * inputs to the device, merges, copies U', M' (and any requested X_M / X_D /
+ * U_D / r) back, synchronises and fills the result fields. */
+typedef struct dm_ctx dm_ctx;
+dm_ctx* dm_ctx_create(int device);
+void dm_ctx_destroy(dm_ctx* ctx);
+dm_status dm_merge_column_host(dm_ctx* ctx, const dm_column_in* in, dm_column_out* out);
+
+/* Number of library kernels launched by this process so far (monotone). */
+uint64_t dm_launch_count(void);
+/* Last CUDA error code seen by the library (cudaError_t as int). */
+int dm_last_cuda_error(void);
+const char* dm_status_str(int status);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,312 @@
+"""paper_1109_6885_b200 -- B200-native online merge for dictionary-encoded column stores.
+
+Thin Python binding over ``libdictmerge.so`` (C ABI: ``include/dictmerge.h``).
+This module only marshals arguments: PyTorch allocates device memory and
+supplies the CUDA stream; every step of the merge (Krueger et al., arXiv
+1109.6885, Sec 5: Step 1(a) delta dictionary, Step 1(b) dictionary merge with
+translation tables X_M / X_D, Step 2(a) width, Step 2(b) recompression) runs in
+the library's sm_100a kernels.  There is no CPU fallback: importing this
+package without the built library raises.
+
+Key tensors: ``"u64"`` keys are 1-D ``torch.int64`` tensors holding the u64 bit
+patterns (compared unsigned); ``"b16"`` keys are ``torch.uint8`` tensors of
+shape (n, 16) (compared bytewise).  Packed code vectors are 1-D ``torch.int64``
+tensors of little-endian u64 words (LSB-first bitstream).
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import os
+from typing import Optional, Sequence
+
+import torch
+
+from . import build as _build
+
+__all__ = [
+    "KEY_U64", "KEY_B16", "Status", "DictMergeError", "width", "words", "merged_codes_cap_words",
+    "workspace_bytes", "merge_column", "merge_column_async", "merge_table", "pack_codes", "unpack_codes",
+    "ColumnMerger", "HostContext", "launch_count", "lib_path",
+]
+
+KEY_U64, KEY_B16 = 0, 1
+_KEY = {"u64": KEY_U64, "b16": KEY_B16}
+
+
+class Status:
+    OK, E_INVALID, E_CAPACITY, E_TOO_WIDE, E_UNSORTED, E_CODE_RANGE, E_CUDA, E_NCCL = 0, -1, -2, -3, -4, -5, -6, -7
+
+
+class DictMergeError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        msg = _lib().dm_status_str(status).decode()
+        if status == Status.E_CUDA:
+            msg += f" (cudaError {int(_lib().dm_last_cuda_error())})"
+        super().__init__(f"{where}: {msg} [{status}]")
+        self.status = status
+
+
+class _In(ctypes.Structure):
+    _fields_ = [("key", ctypes.c_int32), ("main_dict", ctypes.c_void_p), ("dict_len", ctypes.c_uint64),
+                ("main_codes", ctypes.c_void_p), ("n_main", ctypes.c_uint64), ("main_bits", ctypes.c_uint32),
+                ("delta", ctypes.c_void_p), ("n_delta", ctypes.c_uint64)]
+
+
+class _Out(ctypes.Structure):
+    _fields_ = [("merged_dict", ctypes.c_void_p), ("merged_dict_cap", ctypes.c_uint64),
+                ("merged_codes", ctypes.c_void_p), ("merged_codes_cap_words", ctypes.c_uint64),
+                ("x_main", ctypes.c_void_p), ("x_delta", ctypes.c_void_p), ("delta_dict", ctypes.c_void_p),
+                ("delta_rank", ctypes.c_void_p), ("merged_dict_len", ctypes.c_uint64),
+                ("delta_dict_len", ctypes.c_uint64), ("merged_bits", ctypes.c_uint32)]
+
+
+class _Hdr(ctypes.Structure):
+    _fields_ = [("merged_dict_len", ctypes.c_uint64), ("delta_dict_len", ctypes.c_uint64),
+                ("merged_bits", ctypes.c_uint32), ("status", ctypes.c_int32)]
+
+
+_L = None
+
+
+def lib_path() -> str:
+    return _build.LIB
+
+
+def _lib():
+    global _L
+    if _L is None:
+        if not os.path.exists(_build.LIB):
+            raise ImportError(f"libdictmerge.so is not built ({_build.LIB}); run "
+                              "`python -m paper_1109_6885_b200.build` or __graft_entry__.build(). "
+                              "There is no CPU fallback.")
+        L = ctypes.CDLL(_build.LIB)
+        u64, u32, vp, i32 = ctypes.c_uint64, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_int
+        P = ctypes.POINTER
+        sig = {
+            "dm_width": (u32, [u64]),
+            "dm_words": (u64, [u64, u32]),
+            "dm_merged_codes_cap_words": (u64, [P(_In)]),
+            "dm_workspace_bytes": (ctypes.c_size_t, [P(_In)]),
+            "dm_merge_column_async": (i32, [P(_In), P(_Out), vp, ctypes.c_size_t, vp, vp]),
+            "dm_merge_column_async_ev": (i32, [P(_In), P(_Out), vp, ctypes.c_size_t, vp, vp, P(vp)]),
+            "dm_merge_column": (i32, [P(_In), P(_Out), vp, ctypes.c_size_t, vp]),
+            "dm_recompress": (i32, [vp, u64, u32, u64, vp, vp, vp, u64, u32, vp, u64, vp]),
+            "dm_merge_table": (i32, [i32, P(_In), P(_Out), P(vp), P(ctypes.c_size_t), vp]),
+            "dm_pack_codes": (i32, [vp, u64, u32, vp, vp]),
+            "dm_unpack_codes": (i32, [vp, u64, u32, vp, vp]),
+            "dm_ctx_create": (vp, [i32]),
+            "dm_ctx_destroy": (None, [vp]),
+            "dm_merge_column_host": (i32, [vp, P(_In), P(_Out)]),
+            "dm_launch_count": (u64, []),
+            "dm_last_cuda_error": (i32, []),
+            "dm_status_str": (ctypes.c_char_p, [i32]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _L = L
+    return _L
+
+
+# ------------------------------------------------------------------ pure helpers
+def width(n: int) -> int:
+    """max(1, ceil(log2 n)) -- Eq 4, reading A1."""
+    return int(_lib().dm_width(n))
+
+
+def words(n: int, bits: int) -> int:
+    return int(_lib().dm_words(n, bits))
+
+
+def launch_count() -> int:
+    return int(_lib().dm_launch_count())
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    return None if t is None or t.numel() == 0 else t.data_ptr()
+
+
+def _key_of(t: torch.Tensor) -> int:
+    return KEY_B16 if (t.dtype == torch.uint8 and t.dim() == 2) else KEY_U64
+
+
+def _make_in(main_dict, main_codes, n_main, main_bits, delta) -> _In:
+    key = _key_of(main_dict) if main_dict.numel() else _key_of(delta)
+    return _In(key, _ptr(main_dict), main_dict.shape[0], _ptr(main_codes), n_main, main_bits, _ptr(delta),
+               delta.shape[0])
+
+
+def merged_codes_cap_words(cin: _In) -> int:
+    return int(_lib().dm_merged_codes_cap_words(ctypes.byref(cin)))
+
+
+def workspace_bytes(cin: _In) -> int:
+    return int(_lib().dm_workspace_bytes(ctypes.byref(cin)))
+
+
+def _stream_handle(stream) -> Optional[int]:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _empty_keys(key: int, n: int, device) -> torch.Tensor:
+    if key == KEY_U64:
+        return torch.empty(max(n, 2), dtype=torch.int64, device=device)
+    return torch.empty((max(n, 1), 16), dtype=torch.uint8, device=device)
+
+
+@dataclasses.dataclass
+class MergeResult:
+    merged_dict: torch.Tensor            # U' (|U'| keys)
+    merged_codes: torch.Tensor           # M' (exactly words(N', b') u64 words, as int64)
+    merged_bits: int                     # b'
+    delta_dict_len: int                  # |U_D|
+    x_main: Optional[torch.Tensor] = None
+    x_delta: Optional[torch.Tensor] = None
+    delta_dict: Optional[torch.Tensor] = None
+    delta_rank: Optional[torch.Tensor] = None
+
+    @property
+    def merged_len(self) -> int:
+        return int(self.merged_dict.shape[0])
+
+
+class ColumnMerger:
+    """Pre-allocated merge of one column shape: outputs, workspace and a device
+    result header live as long as the object, so ``run_async`` launches the
+    whole path with no allocation and no host synchronisation (graph-capturable)."""
+
+    def __init__(self, main_dict: torch.Tensor, main_codes: torch.Tensor, n_main: int, main_bits: int,
+                 delta: torch.Tensor, *, x_tables: bool = False, delta_dict: bool = False):
+        dev = main_dict.device if main_dict.numel() else delta.device
+        if dev.type != "cuda":
+            raise ValueError("merge_column needs CUDA tensors (there is no CPU path)")
+        self.inputs = (main_dict, main_codes, delta)
+        self.cin = _make_in(main_dict, main_codes, n_main, main_bits, delta)
+        key = self.cin.key
+        nU = main_dict.shape[0] + delta.shape[0]
+        self.n_total = n_main + delta.shape[0]
+        self.U = _empty_keys(key, nU, dev)
+        cap = merged_codes_cap_words(self.cin)
+        self.M = torch.empty(max(cap, 2), dtype=torch.int64, device=dev)
+        self.XM = torch.empty(max(main_dict.shape[0], 1), dtype=torch.int32, device=dev) if x_tables else None
+        self.XD = torch.empty(max(delta.shape[0], 1), dtype=torch.int32, device=dev) if x_tables else None
+        self.UD = _empty_keys(key, delta.shape[0], dev) if delta_dict else None
+        self.R = torch.empty(max(delta.shape[0], 1), dtype=torch.int32, device=dev) if delta_dict else None
+        self.cout = _Out(_ptr(self.U), nU, _ptr(self.M), cap, _ptr(self.XM), _ptr(self.XD), _ptr(self.UD),
+                         _ptr(self.R), 0, 0, 0)
+        self.ws_bytes = workspace_bytes(self.cin)
+        self.ws = torch.empty(max(self.ws_bytes, 256), dtype=torch.uint8, device=dev)
+        self.hdr = torch.zeros(4, dtype=torch.int64, device=dev)  # dm_header (24 B, 16-B aligned)
+
+    def run_async(self, stream=None) -> None:
+        st = _lib().dm_merge_column_async(ctypes.byref(self.cin), ctypes.byref(self.cout), self.ws.data_ptr(),
+                                          self.ws_bytes, self.hdr.data_ptr(), _stream_handle(stream))
+        if st != Status.OK:
+            raise DictMergeError(st, "dm_merge_column_async")
+
+    def run_async_timed(self, events, stream=None) -> None:
+        """As run_async, recording 4 torch.cuda.Events at the step boundaries
+        (before 1(a), before 1(b), before 2(b), after 2(b))."""
+        evs = (ctypes.c_void_p * 4)(*[e.cuda_event for e in events])
+        st = _lib().dm_merge_column_async_ev(ctypes.byref(self.cin), ctypes.byref(self.cout), self.ws.data_ptr(),
+                                             self.ws_bytes, self.hdr.data_ptr(), _stream_handle(stream), evs)
+        if st != Status.OK:
+            raise DictMergeError(st, "dm_merge_column_async_ev")
+
+    def header(self) -> _Hdr:
+        raw = self.hdr.cpu().numpy().tobytes()
+        return _Hdr.from_buffer_copy(raw[: ctypes.sizeof(_Hdr)])
+
+    def result(self) -> MergeResult:
+        h = self.header()
+        if h.status != Status.OK:
+            raise DictMergeError(h.status, "dm_merge_column")
+        nw = words(self.n_total, h.merged_bits)
+        return MergeResult(
+            self.U[: h.merged_dict_len], self.M[:nw], int(h.merged_bits), int(h.delta_dict_len),
+            None if self.XM is None else self.XM[: self.cin.dict_len],
+            None if self.XD is None else self.XD[: h.delta_dict_len],
+            None if self.UD is None else self.UD[: h.delta_dict_len],
+            None if self.R is None else self.R[: self.cin.n_delta])
+
+
+def merge_column(main_dict: torch.Tensor, main_codes: torch.Tensor, n_main: int, main_bits: int,
+                 delta: torch.Tensor, *, x_tables: bool = False, delta_dict: bool = False,
+                 stream=None) -> MergeResult:
+    """Merge one column (synchronous): returns U', M', b' (+ X_M / X_D / U_D / r on request)."""
+    m = ColumnMerger(main_dict, main_codes, n_main, main_bits, delta, x_tables=x_tables, delta_dict=delta_dict)
+    m.run_async(stream)
+    return m.result()
+
+
+def merge_column_async(merger: ColumnMerger, stream=None) -> None:
+    merger.run_async(stream)
+
+
+def merge_table(columns: Sequence[tuple], *, stream=None) -> list:
+    """Merge independent columns of a wide table through dm_merge_table.
+
+    ``columns``: sequence of (main_dict, main_codes, n_main, main_bits, delta) on one device."""
+    n = len(columns)
+    ms = [ColumnMerger(*c) for c in columns]
+    ins = (_In * n)(*[m.cin for m in ms])
+    outs = (_Out * n)(*[m.cout for m in ms])
+    wss = (ctypes.c_void_p * n)(*[m.ws.data_ptr() for m in ms])
+    wsb = (ctypes.c_size_t * n)(*[m.ws_bytes for m in ms])
+    st = _lib().dm_merge_table(n, ins, outs, wss, wsb, _stream_handle(stream))
+    if st != Status.OK:
+        raise DictMergeError(st, "dm_merge_table")
+    res = []
+    for m, o in zip(ms, outs):
+        nw = words(m.n_total, o.merged_bits)
+        res.append(MergeResult(m.U[: o.merged_dict_len], m.M[:nw], int(o.merged_bits), int(o.delta_dict_len)))
+    return res
+
+
+def pack_codes(codes: torch.Tensor, bits: int, stream=None) -> torch.Tensor:
+    """Pack u32 codes (int32 tensor) at ``bits`` into words(n, bits) u64 words (library kernel)."""
+    n = codes.numel()
+    out = torch.empty(max(words(n, bits), 2), dtype=torch.int64, device=codes.device)
+    st = _lib().dm_pack_codes(_ptr(codes), n, bits, out.data_ptr(), _stream_handle(stream))
+    if st != Status.OK:
+        raise DictMergeError(st, "dm_pack_codes")
+    return out[: words(n, bits)]
+
+
+def unpack_codes(w: torch.Tensor, n: int, bits: int, stream=None) -> torch.Tensor:
+    out = torch.empty(max(n, 1), dtype=torch.int32, device=w.device)
+    st = _lib().dm_unpack_codes(_ptr(w), n, bits, out.data_ptr(), _stream_handle(stream))
+    if st != Status.OK:
+        raise DictMergeError(st, "dm_unpack_codes")
+    return out[:n]
+
+
+class HostContext:
+    """dm_ctx: merges columns held in HOST memory (inputs copied in, results copied
+    back inside the call).  Buffers should be pinned for full PCIe bandwidth."""
+
+    def __init__(self, device: int = 0):
+        self.h = _lib().dm_ctx_create(device)
+        if not self.h:
+            raise DictMergeError(Status.E_CUDA, "dm_ctx_create")
+
+    def close(self):
+        if self.h:
+            _lib().dm_ctx_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def merge(self, main_dict: torch.Tensor, main_codes: torch.Tensor, n_main: int, main_bits: int,
+              delta: torch.Tensor, out_dict: torch.Tensor, out_codes: torch.Tensor) -> tuple:
+        """All tensors on the CPU.  Returns (|U'|, b', |U_D|); U' and M' land in out_dict / out_codes."""
+        cin = _make_in(main_dict, main_codes, n_main, main_bits, delta)
+        cout = _Out(_ptr(out_dict), out_dict.shape[0], _ptr(out_codes), out_codes.numel(), None, None, None,
+                    None, 0, 0, 0)
+        st = _lib().dm_merge_column_host(self.h, ctypes.byref(cin), ctypes.byref(cout))
+        if st != Status.OK:
+            raise DictMergeError(st, "dm_merge_column_host")
+        return int(cout.merged_dict_len), int(cout.merged_bits), int(cout.delta_dict_len)

@@ -1,0 +1,373 @@
+// dictmerge.cu -- host side of libdictmerge: the C ABI (include/dictmerge.h),
+// argument validation, workspace layout, stream-ordered orchestration of the
+// three kernel families, the wide-table entry point and the host-buffer
+// context.  Every step of the merge runs in the kernels of delta_dict.cu,
+// dict_merge.cu and recompress.cu; this file only plans and launches.
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "dm_internal.h"
+
+namespace dm {
+
+static std::atomic<uint64_t> g_launches{0};
+static std::atomic<int> g_last_cuda{0};
+
+void note_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+uint32_t host_width(uint64_t n) {
+  // Eq 4: ceil(log2 n), with a 1-bit minimum (reading A1).
+  uint32_t w = 1;
+  while (w < 64 && (1ull << w) < n) ++w;
+  return w;
+}
+uint64_t host_words(uint64_t n, uint32_t bits) { return (n * (uint64_t)bits + 63) / 64; }
+
+static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+WsLayout ws_layout(const dm_column_in* in) {
+  WsLayout L{};
+  const size_t E = in->key == DM_KEY_U64 ? 8 : 16;
+  const uint64_t nD = in->n_delta;
+  L.npass = in->key == DM_KEY_U64 ? 8 : 16;
+  const uint64_t sort_tile = (uint64_t)kSortThreads * (in->key == DM_KEY_U64 ? kSortItemsU64 : kSortItemsB16);
+  L.ntiles_sort = (nD + sort_tile - 1) / sort_tile;
+  L.ntiles_unique = (nD + kUniqThreads * kUniqItems - 1) / (kUniqThreads * kUniqItems);
+  L.ntiles_merge = std::max<uint64_t>(1, (in->dict_len + nD + kMergeTile - 1) / kMergeTile);
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = o;
+    o = align_up(o + bytes, 256);
+    return at;
+  };
+  L.hdr = take(sizeof(dm_header));
+  L.counters = take(64 * sizeof(uint32_t));
+  L.hist = take(16 * 256 * sizeof(uint32_t));
+  L.status_sort = take((size_t)L.npass * L.ntiles_sort * 256 * sizeof(uint32_t));
+  L.status_unique = take(L.ntiles_unique * sizeof(uint64_t));
+  L.status_merge = take(L.ntiles_merge * sizeof(uint64_t));
+  L.zero_bytes = o;
+  L.plan = take(sizeof(SortPlan));
+  L.keys0 = take(nD * E);
+  L.keys1 = take(nD * E);
+  L.vals0 = take(nD * 4);
+  L.vals1 = take(nD * 4);
+  L.udict = take(nD * E);
+  L.rank = take(nD * 4);
+  L.part = take((L.ntiles_merge + 1) * sizeof(uint64_t));
+  L.xm = take(in->dict_len * 4);
+  L.xd = take(nD * 4);
+  L.total = o;
+  return L;
+}
+
+cudaError_t last_error_check() { return cudaGetLastError(); }
+
+static dm_status cuda_fail(cudaError_t e) {
+  g_last_cuda.store((int)e);
+  return DM_E_CUDA;
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+static dm_status validate(const dm_column_in* in, const dm_column_out* out) {
+  if (!in || !out) return DM_E_INVALID;
+  if (in->key != DM_KEY_U64 && in->key != DM_KEY_B16) return DM_E_INVALID;
+  if (in->main_bits < 1 || in->main_bits > 32) return DM_E_INVALID;
+  if (in->dict_len >= (1ull << 32)) return DM_E_INVALID;
+  if (in->n_delta >= (1ull << 30)) return DM_E_INVALID;
+  if (in->n_main > 0 && in->dict_len == 0) return DM_E_INVALID;
+  if (in->dict_len > 0 && in->main_bits < host_width(in->dict_len)) return DM_E_INVALID;
+  if (in->dict_len && (!in->main_dict || !aligned16(in->main_dict))) return DM_E_INVALID;
+  if (in->n_main && (!in->main_codes || !aligned16(in->main_codes))) return DM_E_INVALID;
+  if (in->n_delta && (!in->delta || !aligned16(in->delta))) return DM_E_INVALID;
+  const uint64_t dict_cap = in->dict_len + in->n_delta;
+  if (dict_cap > (1ull << 32)) return DM_E_TOO_WIDE;  // |U'| <= |U_M| + N_D must stay <= 2^32
+  if (dict_cap && (!out->merged_dict || !aligned16(out->merged_dict))) return DM_E_INVALID;
+  if (out->merged_dict_cap < dict_cap) return DM_E_CAPACITY;
+  const uint64_t need_words = dm_merged_codes_cap_words(in);
+  if (need_words && (!out->merged_codes || !aligned16(out->merged_codes))) return DM_E_INVALID;
+  if (out->merged_codes_cap_words < need_words) return DM_E_CAPACITY;
+  if (out->delta_dict && !aligned16(out->delta_dict)) return DM_E_INVALID;
+  return DM_OK;
+}
+
+static dm_status merge_async(const dm_column_in* in, const dm_column_out* out, void* ws, size_t ws_bytes,
+                             dm_header* d_header, cudaStream_t st, bool zero_header,
+                             void* const* events = nullptr) {
+  dm_status v = validate(in, out);
+  if (v != DM_OK) return v;
+  const WsLayout L = ws_layout(in);
+  if (!ws || ws_bytes < L.total) return DM_E_CAPACITY;
+  if (!d_header || !aligned16(d_header)) return DM_E_INVALID;
+  char* w = static_cast<char*>(ws);
+  auto mark = [&](int i) {
+    if (events && events[i]) cudaEventRecord(static_cast<cudaEvent_t>(events[i]), st);
+  };
+  mark(0);
+  cudaError_t e = cudaMemsetAsync(w, 0, L.zero_bytes, st);
+  if (e == cudaSuccess && zero_header) e = cudaMemsetAsync(d_header, 0, sizeof(dm_header), st);
+  if (e != cudaSuccess) return cuda_fail(e);
+  void* udict = out->delta_dict ? out->delta_dict : (void*)(w + L.udict);
+  uint32_t* rank = out->delta_rank ? out->delta_rank : reinterpret_cast<uint32_t*>(w + L.rank);
+  uint32_t* xm = out->x_main ? out->x_main : reinterpret_cast<uint32_t*>(w + L.xm);
+  uint32_t* xd = out->x_delta ? out->x_delta : reinterpret_cast<uint32_t*>(w + L.xd);
+  // Step 1(a): delta dictionary U_D and ranks r.
+  if ((e = launch_delta_dictionary(in, w, L, udict, rank, d_header, st)) != cudaSuccess) return cuda_fail(e);
+  mark(1);
+  // Step 1(b) + 2(a): U', X_M, X_D, b' (Eq 4).
+  if ((e = launch_dictionary_merge(in, out, w, L, udict, xm, xd, d_header, st)) != cudaSuccess) return cuda_fail(e);
+  mark(2);
+  // Step 2(b): M' (Eq 11).
+  if ((e = launch_recompress(in, out, xm, xd, rank, d_header, st)) != cudaSuccess) return cuda_fail(e);
+  mark(3);
+  return DM_OK;
+}
+
+struct dm_ctx_impl {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::vector<std::pair<void*, size_t>> bufs;  // device buffers, grown on demand
+  dm_header* host_hdr = nullptr;                // pinned
+  void* get(int slot, size_t bytes) {
+    if ((int)bufs.size() <= slot) bufs.resize(slot + 1, {nullptr, 0});
+    auto& b = bufs[slot];
+    if (b.second < bytes) {
+      if (b.first) cudaFree(b.first);
+      b.first = nullptr;
+      b.second = 0;
+      if (cudaMalloc(&b.first, std::max<size_t>(bytes, 256)) != cudaSuccess) return nullptr;
+      b.second = std::max<size_t>(bytes, 256);
+    }
+    return b.first;
+  }
+};
+
+}  // namespace dm
+
+using namespace dm;
+
+struct dm_ctx {
+  dm_ctx_impl impl;
+};
+
+extern "C" {
+
+uint32_t dm_width(uint64_t n) { return host_width(n); }
+uint64_t dm_words(uint64_t n, uint32_t bits) { return host_words(n, bits); }
+
+uint64_t dm_merged_codes_cap_words(const dm_column_in* in) {
+  if (!in) return 0;
+  return host_words(in->n_main + in->n_delta, std::min<uint32_t>(32, host_width(in->dict_len + in->n_delta)));
+}
+
+size_t dm_workspace_bytes(const dm_column_in* in) { return in ? ws_layout(in).total : 0; }
+
+dm_status dm_merge_column_async(const dm_column_in* in, const dm_column_out* out, void* ws, size_t ws_bytes,
+                                dm_header* d_header, void* cuda_stream) {
+  return merge_async(in, out, ws, ws_bytes, d_header, static_cast<cudaStream_t>(cuda_stream), true);
+}
+
+dm_status dm_merge_column_async_ev(const dm_column_in* in, const dm_column_out* out, void* ws, size_t ws_bytes,
+                                   dm_header* d_header, void* cuda_stream, void* const* events) {
+  return merge_async(in, out, ws, ws_bytes, d_header, static_cast<cudaStream_t>(cuda_stream), true, events);
+}
+
+dm_status dm_merge_column(const dm_column_in* in, dm_column_out* out, void* ws, size_t ws_bytes, void* cuda_stream) {
+  if (!in) return DM_E_INVALID;
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  const WsLayout L = ws_layout(in);
+  if (!ws || ws_bytes < L.total) return DM_E_CAPACITY;
+  dm_header* d_hdr = reinterpret_cast<dm_header*>(static_cast<char*>(ws) + L.hdr);
+  dm_status s = merge_async(in, out, ws, ws_bytes, d_hdr, st, false);  // header lives in the zeroed zone
+  if (s != DM_OK) return s;
+  dm_header h{};
+  cudaError_t e = cudaMemcpyAsync(&h, d_hdr, sizeof(h), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e);
+  out->merged_dict_len = h.merged_dict_len;
+  out->delta_dict_len = h.delta_dict_len;
+  out->merged_bits = h.merged_bits;
+  return (dm_status)h.status;
+}
+
+dm_status dm_merge_table(int ncols, const dm_column_in* in, dm_column_out* out, void* const* ws,
+                         const size_t* ws_bytes, void* cuda_stream) {
+  if (ncols < 0 || (ncols > 0 && (!in || !out || !ws || !ws_bytes))) return DM_E_INVALID;
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  // Each column is merged separately; the columns are independent
+  // tasks issued back to back on one stream.
+  std::vector<dm_header*> hdrs(ncols);
+  for (int c = 0; c < ncols; ++c) {
+    const WsLayout L = ws_layout(&in[c]);
+    if (!ws[c] || ws_bytes[c] < L.total) return DM_E_CAPACITY;
+    hdrs[c] = reinterpret_cast<dm_header*>(static_cast<char*>(ws[c]) + L.hdr);
+    dm_status s = merge_async(&in[c], &out[c], ws[c], ws_bytes[c], hdrs[c], st, false);
+    if (s != DM_OK) return s;
+  }
+  std::vector<dm_header> h(ncols);
+  cudaError_t e = cudaSuccess;
+  for (int c = 0; c < ncols && e == cudaSuccess; ++c)
+    e = cudaMemcpyAsync(&h[c], hdrs[c], sizeof(dm_header), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e);
+  int status = DM_OK;
+  for (int c = 0; c < ncols; ++c) {
+    out[c].merged_dict_len = h[c].merged_dict_len;
+    out[c].delta_dict_len = h[c].delta_dict_len;
+    out[c].merged_bits = h[c].merged_bits;
+    status = std::min(status, (int)h[c].status);
+  }
+  return (dm_status)status;
+}
+
+dm_status dm_recompress(const uint64_t* main_codes, uint64_t n_main, uint32_t main_bits, uint64_t dict_len,
+                        const uint32_t* x_main, const uint32_t* x_delta, const uint32_t* delta_rank,
+                        uint64_t n_delta, uint32_t new_bits, uint64_t* out_codes, uint64_t out_cap_words,
+                        void* cuda_stream) {
+  if (main_bits < 1 || main_bits > 32 || new_bits < 1 || new_bits > 32) return DM_E_INVALID;
+  if (n_main && (!main_codes || !x_main || !aligned16(main_codes))) return DM_E_INVALID;
+  if (n_delta && (!x_delta || !delta_rank)) return DM_E_INVALID;
+  const uint64_t need = host_words(n_main + n_delta, new_bits);
+  if (need && (!out_codes || !aligned16(out_codes))) return DM_E_INVALID;
+  if (out_cap_words < need) return DM_E_CAPACITY;
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  dm_header* d_hdr = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&d_hdr), sizeof(dm_header), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(d_hdr, 0, sizeof(dm_header), st);
+  if (e != cudaSuccess) return cuda_fail(e);
+  dm_column_in in{};
+  in.key = DM_KEY_U64;
+  in.dict_len = dict_len;
+  in.main_codes = main_codes;
+  in.n_main = n_main;
+  in.main_bits = main_bits;
+  in.n_delta = n_delta;
+  dm_column_out out{};
+  out.merged_codes = out_codes;
+  out.merged_codes_cap_words = out_cap_words;
+  e = launch_recompress(&in, &out, x_main, x_delta, delta_rank, d_hdr, st, new_bits);
+  dm_header h{};
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&h, d_hdr, sizeof(h), cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(d_hdr, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e);
+  return (dm_status)h.status;
+}
+
+dm_status dm_pack_codes(const uint32_t* codes, uint64_t n, uint32_t bits, uint64_t* words, void* cuda_stream) {
+  if (bits < 1 || bits > 32) return DM_E_INVALID;
+  if (n && (!codes || !words)) return DM_E_INVALID;
+  cudaError_t e = launch_pack(codes, n, bits, words, static_cast<cudaStream_t>(cuda_stream));
+  return e == cudaSuccess ? DM_OK : cuda_fail(e);
+}
+
+dm_status dm_unpack_codes(const uint64_t* words, uint64_t n, uint32_t bits, uint32_t* codes, void* cuda_stream) {
+  if (bits < 1 || bits > 32) return DM_E_INVALID;
+  if (n && (!codes || !words)) return DM_E_INVALID;
+  cudaError_t e = launch_unpack(words, n, bits, codes, static_cast<cudaStream_t>(cuda_stream));
+  return e == cudaSuccess ? DM_OK : cuda_fail(e);
+}
+
+dm_ctx* dm_ctx_create(int device) {
+  if (cudaSetDevice(device) != cudaSuccess) return nullptr;
+  dm_ctx* c = new dm_ctx();
+  c->impl.device = device;
+  if (cudaStreamCreateWithFlags(&c->impl.stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaMallocHost(&c->impl.host_hdr, sizeof(dm_header)) != cudaSuccess) {
+    delete c;
+    return nullptr;
+  }
+  return c;
+}
+
+void dm_ctx_destroy(dm_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->impl.device);
+  for (auto& b : c->impl.bufs)
+    if (b.first) cudaFree(b.first);
+  if (c->impl.host_hdr) cudaFreeHost(c->impl.host_hdr);
+  if (c->impl.stream) cudaStreamDestroy(c->impl.stream);
+  delete c;
+}
+
+dm_status dm_merge_column_host(dm_ctx* c, const dm_column_in* hin, dm_column_out* hout) {
+  if (!c || !hin || !hout) return DM_E_INVALID;
+  cudaSetDevice(c->impl.device);
+  auto& I = c->impl;
+  cudaStream_t st = I.stream;
+  const size_t E = hin->key == DM_KEY_U64 ? 8 : 16;
+  dm_column_in din = *hin;
+  dm_column_out dout = *hout;
+  const uint64_t in_words = host_words(hin->n_main, hin->main_bits);
+  const uint64_t cap_words = dm_merged_codes_cap_words(hin);
+  enum { B_DICT, B_CODES, B_DELTA, B_UOUT, B_MOUT, B_XM, B_XD, B_UD, B_R, B_WS };
+  din.main_dict = hin->dict_len ? I.get(B_DICT, hin->dict_len * E) : nullptr;
+  din.main_codes = in_words ? static_cast<const uint64_t*>(I.get(B_CODES, in_words * 8)) : nullptr;
+  din.delta = hin->n_delta ? I.get(B_DELTA, hin->n_delta * E) : nullptr;
+  dout.merged_dict = I.get(B_UOUT, (hin->dict_len + hin->n_delta) * E);
+  dout.merged_dict_cap = hin->dict_len + hin->n_delta;
+  dout.merged_codes = static_cast<uint64_t*>(I.get(B_MOUT, cap_words * 8));
+  dout.merged_codes_cap_words = cap_words;
+  dout.x_main = hout->x_main ? static_cast<uint32_t*>(I.get(B_XM, hin->dict_len * 4)) : nullptr;
+  dout.x_delta = hout->x_delta ? static_cast<uint32_t*>(I.get(B_XD, hin->n_delta * 4)) : nullptr;
+  dout.delta_dict = hout->delta_dict ? I.get(B_UD, hin->n_delta * E) : nullptr;
+  dout.delta_rank = hout->delta_rank ? static_cast<uint32_t*>(I.get(B_R, hin->n_delta * 4)) : nullptr;
+  const size_t wsb = dm_workspace_bytes(hin);
+  void* ws = I.get(B_WS, wsb);
+  if (!ws || !dout.merged_dict || !dout.merged_codes) return cuda_fail(cudaErrorMemoryAllocation);
+  cudaError_t e = cudaSuccess;
+  auto h2d = [&](const void* d, const void* h, size_t n) {
+    if (n && e == cudaSuccess) e = cudaMemcpyAsync(const_cast<void*>(d), h, n, cudaMemcpyHostToDevice, st);
+  };
+  h2d(din.main_dict, hin->main_dict, hin->dict_len * E);
+  h2d(din.main_codes, hin->main_codes, in_words * 8);
+  h2d(din.delta, hin->delta, hin->n_delta * E);
+  if (e != cudaSuccess) return cuda_fail(e);
+  const WsLayout L = ws_layout(hin);
+  dm_header* d_hdr = reinterpret_cast<dm_header*>(static_cast<char*>(ws) + L.hdr);
+  dm_status s = merge_async(&din, &dout, ws, wsb, d_hdr, st, false);
+  if (s != DM_OK) return s;
+  e = cudaMemcpyAsync(I.host_hdr, d_hdr, sizeof(dm_header), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e);
+  const dm_header h = *I.host_hdr;
+  if (h.status != DM_OK) return (dm_status)h.status;
+  auto d2h = [&](void* hp, const void* dp, size_t n) {
+    if (hp && n && e == cudaSuccess) e = cudaMemcpyAsync(hp, dp, n, cudaMemcpyDeviceToHost, st);
+  };
+  d2h(hout->merged_dict, dout.merged_dict, h.merged_dict_len * E);
+  d2h(hout->merged_codes, dout.merged_codes, host_words(hin->n_main + hin->n_delta, h.merged_bits) * 8);
+  d2h(hout->x_main, dout.x_main, hin->dict_len * 4);
+  d2h(hout->x_delta, dout.x_delta, h.delta_dict_len * 4);
+  d2h(hout->delta_dict, dout.delta_dict, h.delta_dict_len * E);
+  d2h(hout->delta_rank, dout.delta_rank, hin->n_delta * 4);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e);
+  hout->merged_dict_len = h.merged_dict_len;
+  hout->delta_dict_len = h.delta_dict_len;
+  hout->merged_bits = h.merged_bits;
+  return DM_OK;
+}
+
+uint64_t dm_launch_count(void) { return g_launches.load(); }
+int dm_last_cuda_error(void) { return g_last_cuda.load(); }
+
+const char* dm_status_str(int s) {
+  switch (s) {
+    case DM_OK: return "ok";
+    case DM_E_INVALID: return "invalid argument";
+    case DM_E_CAPACITY: return "capacity too small";
+    case DM_E_TOO_WIDE: return "merged dictionary exceeds 2^32 entries";
+    case DM_E_UNSORTED: return "main dictionary not strictly increasing";
+    case DM_E_CODE_RANGE: return "main code out of dictionary range";
+    case DM_E_CUDA: return "CUDA error";
+    case DM_E_NCCL: return "NCCL error";
+    default: return "unknown status";
+  }
+}
+
+}  // extern "C"

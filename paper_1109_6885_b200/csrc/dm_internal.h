@@ -1,0 +1,88 @@
+// dm_internal.h -- host/device shared internals of libdictmerge (not part of the ABI).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/dictmerge.h"
+
+namespace dm {
+
+// ---- tiling constants
+constexpr int kSortThreads = 256;
+constexpr int kSortItemsU64 = 16;                        // 4096 keys per onesweep tile
+constexpr int kSortItemsB16 = 8;                         // 2048 keys per tile (16-byte keys)
+constexpr int kUniqThreads = 256;
+constexpr int kUniqItems = 8;                            // 2048 per tile
+constexpr int kMergeThreads = 256;
+constexpr int kMergeItems = 8;                           // 2048 merged-diagonal elements per tile
+constexpr int kMergeTile = kMergeThreads * kMergeItems;
+constexpr int kRecThreads = 256;                         // recompress CTA
+constexpr int kRecGroups = 128;                          // 32-row groups per chunk (4096 rows)
+constexpr int kRecStages = 4;                            // TMA input ring depth
+
+constexpr uint32_t kRadixFlagAgg = 1u << 30;
+constexpr uint32_t kRadixFlagPre = 2u << 30;
+constexpr uint32_t kRadixValMask = (1u << 30) - 1;
+
+// Device-computed radix plan (pass skipping: a pass whose digit is constant
+// over all keys is skipped; src/dst select the ping-pong buffers).
+enum { SEL_INPUT = 0, SEL_BUF0 = 1, SEL_BUF1 = 2 };
+struct SortPlan {
+  int32_t active[16];
+  int32_t src[16];
+  int32_t dst[16];
+  int32_t final_sel;
+  int32_t n_active;
+  int32_t pad[2];
+  uint32_t digit_base[16][256];
+};
+
+// Workspace layout (byte offsets).  [0, zero_bytes) is memset to 0 per call.
+struct WsLayout {
+  size_t hdr;            // dm_header used by the synchronous entry points
+  size_t counters;       // u32[64]: tile counters (16 sort passes, unique, merge, ...)
+  size_t hist;           // u32[16][256] global digit histograms
+  size_t status_sort;    // u32[npass][ntiles_sort][256]
+  size_t status_unique;  // u64[ntiles_unique]
+  size_t status_merge;   // u64[ntiles_merge]
+  size_t zero_bytes;
+  size_t plan;           // SortPlan
+  size_t keys0, keys1;   // numeric keys, n_delta each
+  size_t vals0, vals1;   // u32, n_delta each
+  size_t udict;          // U_D raw keys, n_delta
+  size_t rank;           // r: u32 n_delta
+  size_t part;           // u64[ntiles_merge + 1] merge-path co-ranks
+  size_t xm;             // X_M u32[dict_len]
+  size_t xd;             // X_D u32[n_delta]
+  size_t total;
+  uint64_t ntiles_sort, ntiles_unique, ntiles_merge;
+  int npass;
+};
+
+enum { CNT_SORT = 0, CNT_UNIQUE = 16, CNT_MERGE = 17 };
+
+WsLayout ws_layout(const dm_column_in* in);
+uint32_t host_width(uint64_t n);
+uint64_t host_words(uint64_t n, uint32_t bits);
+
+// ---- launch bookkeeping
+void note_launch(int n = 1);
+cudaError_t last_error_check();
+
+// ---- kernel launchers (each .cu file)
+// Step 1(a): sort + unique of D -> U_D (udict), r (rank), hdr->delta_dict_len.
+cudaError_t launch_delta_dictionary(const dm_column_in* in, char* ws, const WsLayout& L, void* udict, uint32_t* rank,
+                                    dm_header* hdr, cudaStream_t st);
+// Step 1(b) + 2(a): merge-path merge -> U', X_M, X_D, hdr->merged_dict_len / merged_bits.
+cudaError_t launch_dictionary_merge(const dm_column_in* in, const dm_column_out* out, char* ws, const WsLayout& L,
+                                    const void* udict, uint32_t* xm, uint32_t* xd, dm_header* hdr, cudaStream_t st);
+// Step 2(b): recompress main through X_M and append delta through X_D.
+// fixed_bits != 0: b' given by the caller (dm_recompress); else read from hdr->merged_bits.
+cudaError_t launch_recompress(const dm_column_in* in, const dm_column_out* out, const uint32_t* xm,
+                              const uint32_t* xd, const uint32_t* rank, dm_header* hdr, cudaStream_t st,
+                              uint32_t fixed_bits = 0);
+cudaError_t launch_pack(const uint32_t* codes, uint64_t n, uint32_t bits, uint64_t* words, cudaStream_t st);
+cudaError_t launch_unpack(const uint64_t* words, uint64_t n, uint32_t bits, uint32_t* codes, cudaStream_t st);
+
+}  // namespace dm

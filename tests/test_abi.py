@@ -1,0 +1,92 @@
+"""The C-ABI library: it builds, loads without a GPU, and exports every symbol
+include/*.h declares; host-only helpers agree with the closed forms.  Also the
+separation rules: the product path never imports the oracle and vice versa."""
+import ctypes
+import glob
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    syms = set()
+    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+        txt = open(h).read()
+        txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+        for m in re.finditer(r"^[A-Za-z_][\w \*]*?\b(dm_\w+)\s*\(", txt, flags=re.M):
+            syms.add(m.group(1))
+    return syms
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_1109_6885_b200 import build
+    path = build.build()
+    return ctypes.CDLL(path)
+
+
+def test_header_declares_the_boundary():
+    s = declared_symbols()
+    for need in ("dm_merge_column", "dm_merge_column_async", "dm_merge_table", "dm_recompress", "dm_width",
+                 "dm_words", "dm_workspace_bytes", "dm_pack_codes", "dm_unpack_codes", "dm_merge_column_host"):
+        assert need in s
+
+
+def test_every_declared_symbol_is_exported(lib):
+    missing = [s for s in declared_symbols() if not hasattr(lib, s)]
+    assert not missing, missing
+
+
+def test_sm100a_only(lib):
+    from paper_1109_6885_b200 import build
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", build.LIB], capture_output=True, text=True)
+    assert "sm_100a" in out.stdout
+
+
+def test_host_helpers_match_closed_forms(lib, oracle_lib):
+    lib.dm_width.restype = ctypes.c_uint32
+    lib.dm_width.argtypes = [ctypes.c_uint64]
+    lib.dm_words.restype = ctypes.c_uint64
+    lib.dm_words.argtypes = [ctypes.c_uint64, ctypes.c_uint32]
+    for n in list(range(0, 3000)) + [2**k + d for k in range(12, 33) for d in (-1, 0, 1)]:
+        w = lib.dm_width(n)
+        assert w == (1 if n <= 1 else (n - 1).bit_length())
+    for n in (0, 1, 63, 64, 65, 10**9):
+        for b in (1, 13, 31, 32):
+            assert lib.dm_words(n, b) == -(-n * b // 64)
+
+
+def test_invalid_arguments_rejected_before_launch():
+    import paper_1109_6885_b200 as dm
+    L = dm._lib()
+    assert L.dm_merge_column(None, None, None, 0, None) == dm.Status.E_INVALID
+    cin = dm._In(7, None, 0, None, 0, 3, None, 0)  # bad key
+    cout = dm._Out()
+    assert L.dm_merge_column_async(ctypes.byref(cin), ctypes.byref(cout), None, 0, None, None) == dm.Status.E_INVALID
+    cin = dm._In(0, 16, 10, 32, 100, 2, None, 0)  # main_bits < width(10)
+    assert L.dm_merge_column_async(ctypes.byref(cin), ctypes.byref(cout), None, 0, None, None) == dm.Status.E_INVALID
+    assert L.dm_pack_codes(None, 0, 33, None, None) == dm.Status.E_INVALID
+
+
+def test_workspace_grows_with_delta():
+    import paper_1109_6885_b200 as dm
+    a = dm.workspace_bytes(dm._In(0, 16, 1000, 16, 5000, 10, 16, 100))
+    b = dm.workspace_bytes(dm._In(0, 16, 1000, 16, 5000, 10, 16, 100000))
+    c = dm.workspace_bytes(dm._In(1, 16, 1000, 16, 5000, 10, 16, 100000))
+    assert 0 < a < b < c
+
+
+def test_product_and_oracle_are_separate():
+    prod = glob.glob(os.path.join(ROOT, "paper_1109_6885_b200", "**", "*.*"), recursive=True)
+    for p in prod:
+        if p.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+            txt = open(p).read()
+            assert not re.search(r"\bimport oracle\b|from oracle\b|dm_oracle", txt), p
+    for p in glob.glob(os.path.join(ROOT, "oracle", "*.*")):
+        if p.endswith((".py", ".cpp", ".h")):
+            txt = open(p).read()
+            assert not re.search(r"import paper_1109_6885_b200|from paper_1109_6885_b200|#include.*dictmerge\.h", txt), p
