@@ -194,6 +194,9 @@ def main():
 
     # ---- timed region: K steps, L2 flushed before each, events on the launching stream
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    for row in ev:  # torch creates the CUDA event lazily on first record
+        for e in row:
+            e.record()
     if pg:
         pg.barrier()
     torch.cuda.synchronize()

@@ -188,7 +188,8 @@ __global__ void __launch_bounds__(256) k_pack(const uint32_t* __restrict__ codes
     const uint32_t v = row < n ? (codes[row] & mask) : 0u;
     const uint32_t word = warp_pack<0>(v, bits, pr0, pop);
     const uint64_t widx = g * bits + lane;
-    if (lane < bits && widx < nw32) words32[widx] = word;
+    // lanes >= bits of the last group zero the pad half-word of the final u64
+    if ((lane < bits || g + 1 == ngroups) && widx < nw32) words32[widx] = lane < bits ? word : 0u;
   }
 }
 

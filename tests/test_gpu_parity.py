@@ -66,8 +66,9 @@ def _recompress_case(b, nb, n_main, n_delta, seed):
     cap = max(dm.words(n_main + n_delta, nb), 2)
     out = torch.full((cap,), -1, dtype=torch.int64, device="cuda")
     T = lambda a: torch.from_numpy(a.view(np.int32).copy()).cuda()
-    st = dm._lib().dm_recompress(M.data_ptr(), n_main, b, dict_len, T(xm).data_ptr(), T(xd).data_ptr(),
-                                 T(r).data_ptr(), n_delta, nb, out.data_ptr(), cap, torch.cuda.current_stream().cuda_stream)
+    txm, txd, tr = T(xm), T(xd), T(r)  # keep the tensors alive across the call
+    st = dm._lib().dm_recompress(M.data_ptr(), n_main, b, dict_len, txm.data_ptr(), txd.data_ptr(),
+                                 tr.data_ptr(), n_delta, nb, out.data_ptr(), cap, torch.cuda.current_stream().cuda_stream)
     assert st == 0
     got = out.cpu().numpy().view(np.uint64)[: want.size]
     assert np.array_equal(got, want), (b, nb)
@@ -187,8 +188,8 @@ def test_determinism_and_async_reuse():
         m.run_async()
         r = m.result()
         outs.append((r.merged_dict.clone(), r.merged_codes.clone()))
-    for a, b in outs[1:]:
-        assert torch.equal(a[0], outs[0][0]) and torch.equal(a[1], outs[0][1])
+    for d, c in outs[1:]:
+        assert torch.equal(d, outs[0][0]) and torch.equal(c, outs[0][1])
 
 
 def test_host_entry_point():
