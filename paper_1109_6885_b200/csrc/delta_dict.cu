@@ -156,13 +156,23 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const void* __restric
     st_volatile_u32(my, kRadixFlagPre | tile_cnt);
   } else {
     st_volatile_u32(my, kRadixFlagAgg | tile_cnt);
-    for (int64_t t = (int64_t)tile - 1; t >= 0; --t) {
-      uint32_t s;
-      do {
-        s = ld_volatile_u32(status + (uint64_t)t * 256 + d);
-      } while ((s >> 30) == 0);
-      excl += s & kRadixValMask;
-      if ((s >> 30) == 2) break;
+    // Look back LB predecessors per round trip (independent loads in flight),
+    // so a first wave of T tiles resolves in ~T/LB round trips, not T.
+    constexpr int LB = 32;
+    bool done = false;
+    for (int64_t t0 = (int64_t)tile - 1; !done; t0 -= LB) {
+      uint32_t s[LB];
+#pragma unroll
+      for (int j = 0; j < LB; ++j)
+        s[j] = t0 - j >= 0 ? ld_volatile_u32(status + (uint64_t)(t0 - j) * 256 + d) : kRadixFlagPre;
+#pragma unroll
+      for (int j = 0; j < LB; ++j) {
+        if (!done) {
+          while ((s[j] >> 30) == 0) s[j] = ld_volatile_u32(status + (uint64_t)(t0 - j) * 256 + d);
+          excl += s[j] & kRadixValMask;
+          done = (s[j] >> 30) == 2;
+        }
+      }
     }
     st_volatile_u32(my, kRadixFlagPre | (excl + tile_cnt));
   }

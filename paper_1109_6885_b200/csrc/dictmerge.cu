@@ -48,7 +48,7 @@ WsLayout ws_layout(const dm_column_in* in) {
   L.hist = take(16 * 256 * sizeof(uint32_t));
   L.status_sort = take((size_t)L.npass * L.ntiles_sort * 256 * sizeof(uint32_t));
   L.status_unique = take(L.ntiles_unique * sizeof(uint64_t));
-  L.status_merge = take(L.ntiles_merge * sizeof(uint64_t));
+  L.status_merge = take(((L.ntiles_merge + 2047) / 2048 + 1) * sizeof(uint64_t));
   L.zero_bytes = o;
   L.plan = take(sizeof(SortPlan));
   L.keys0 = take(nD * E);
@@ -58,6 +58,8 @@ WsLayout ws_layout(const dm_column_in* in) {
   L.udict = take(nD * E);
   L.rank = take(nD * 4);
   L.part = take((L.ntiles_merge + 1) * sizeof(uint64_t));
+  L.mcount = take(L.ntiles_merge * sizeof(uint32_t));
+  L.mexcl = take(L.ntiles_merge * sizeof(uint64_t));
   L.xm = take(in->dict_len * 4);
   L.xd = take(nD * 4);
   L.total = o;

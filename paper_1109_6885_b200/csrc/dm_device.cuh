@@ -225,6 +225,9 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity)
   while (!mbar_try_wait_parity(bar, parity)) {
   }
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));

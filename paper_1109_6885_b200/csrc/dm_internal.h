@@ -17,9 +17,11 @@ constexpr int kUniqItems = 8;                            // 2048 per tile
 constexpr int kMergeThreads = 256;
 constexpr int kMergeItems = 8;                           // 2048 merged-diagonal elements per tile
 constexpr int kMergeTile = kMergeThreads * kMergeItems;
-constexpr int kRecThreads = 256;                         // recompress CTA
+constexpr int kRecConsumerWarps = 16;                    // recompress: consumer warps per CTA
+constexpr int kRecThreads = 32 * (kRecConsumerWarps + 1);  // + one TMA producer warp
 constexpr int kRecGroups = 128;                          // 32-row groups per chunk (4096 rows)
 constexpr int kRecStages = 4;                            // TMA input ring depth
+constexpr uint32_t kRecSmemXBytes = 96 * 1024;           // X_M staged in shared memory up to this size
 
 constexpr uint32_t kRadixFlagAgg = 1u << 30;
 constexpr uint32_t kRadixFlagPre = 2u << 30;
@@ -53,6 +55,8 @@ struct WsLayout {
   size_t udict;          // U_D raw keys, n_delta
   size_t rank;           // r: u32 n_delta
   size_t part;           // u64[ntiles_merge + 1] merge-path co-ranks
+  size_t mcount;         // u32[ntiles_merge] duplicates dropped per merge tile
+  size_t mexcl;          // u64[ntiles_merge] exclusive prefix of mcount
   size_t xm;             // X_M u32[dict_len]
   size_t xd;             // X_D u32[n_delta]
   size_t total;

@@ -50,129 +50,120 @@ __device__ __forceinline__ uint32_t warp_pack(uint32_t v, uint32_t nb, uint32_t 
   return word;
 }
 
-template <int NB>
+// Warp-specialised: warp kRecConsumerWarps is the TMA producer, warps
+// 0..kRecConsumerWarps-1 consume.  full[s] completes when stage s holds its
+// chunk's main words; empty[s] completes when every consumer warp is done with
+// stage s.  No CTA-wide barrier after the prologue.  XS: X_M staged in shared
+// memory (tables up to kRecSmemXBytes), else gathered through L2.
+template <int NB, bool XS>
 __global__ void __launch_bounds__(kRecThreads) k_recompress(const uint64_t* __restrict__ M, uint64_t n_main, uint32_t b,
                                                             uint64_t dict_len, const uint32_t* __restrict__ XM,
                                                             const uint32_t* __restrict__ XD,
                                                             const uint32_t* __restrict__ rank, uint64_t n_delta,
                                                             uint64_t* __restrict__ Mout, dm_header* hdr,
-                                                            uint32_t in_stage_bytes, uint32_t out_stage_bytes,
-                                                            uint32_t fixed_bits) {
+                                                            uint32_t in_stage_bytes, uint32_t fixed_bits) {
   constexpr int G = kRecGroups;
   constexpr int S = kRecStages;
-  constexpr int W = kRecThreads / 32;
-  constexpr int U = 4;  // groups in flight per warp
+  constexpr int CW = kRecConsumerWarps;
+  constexpr int U = G / CW;  // groups per consumer warp per chunk, all in flight together
+  static_assert(G % CW == 0, "groups must split evenly over consumer warps");
   const uint32_t hb = fixed_bits ? fixed_bits : hdr->merged_bits;
   if (NB && hb != (uint32_t)NB) return;
   const uint32_t nb = NB ? (uint32_t)NB : hb;
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* empty = full + S;
   unsigned char* in_ring = smem_raw + 128;
-  unsigned char* out_stage = in_ring + (size_t)S * in_stage_bytes;
-  __shared__ int s_bad;
+  uint32_t* sx = reinterpret_cast<uint32_t*>(in_ring + (size_t)S * in_stage_bytes);  // XS only
 
   const uint64_t n_total = n_main + n_delta;
   const uint64_t R = 32ull * G;
   const uint64_t nchunks = (n_total + R - 1) / R;
   const uint64_t main_bytes = dwords(n_main, b) * 8;
-  const uint64_t out_bytes = dwords(n_total, nb) * 8;
+  const uint64_t nw32 = 2 * dwords(n_total, nb);
   const uint32_t chunk_in = G * b * 4;
-  const uint32_t chunk_out = G * nb * 4;
-  const unsigned lane = lane_id(), w = threadIdx.x >> 5;
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
 
-  const uint64_t pol_stream = policy_evict_first();
   if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CW);
+    }
     fence_mbar_init();
-    s_bad = 0;
+  }
+  if (XS) {
+    for (uint32_t i = threadIdx.x; i < dict_len; i += blockDim.x) sx[i] = __ldg(XM + i);
   }
   __syncthreads();
+
+  if (warp == CW) {  // ---------------------------------------------------- producer
+    if (lane == 0) {
+      const uint64_t pol_stream = policy_evict_first();
+      for (uint64_t k = 0;; ++k) {
+        const uint64_t c = blockIdx.x + k * gridDim.x;
+        if (c >= nchunks) break;
+        const int s = (int)(k % S);
+        if (k >= S) mbar_wait_parity(&empty[s], (uint32_t)(((k / S) - 1) & 1));
+        unsigned char* dst = in_ring + (size_t)s * in_stage_bytes;
+        const uint64_t start = c * (uint64_t)chunk_in;
+        const uint32_t len = start < main_bytes ? (uint32_t)umin64(chunk_in, main_bytes - start) : 0u;
+        const uint32_t tl = len & ~15u;
+        if (len > tl)  // 8-byte tail the bulk copy cannot take; published by the arrive (release)
+          *reinterpret_cast<uint64_t*>(dst + tl) =
+              *reinterpret_cast<const uint64_t*>(reinterpret_cast<const unsigned char*>(M) + start + tl);
+        mbar_arrive_expect_tx(&full[s], tl);
+        if (tl) tma_load_1d(dst, reinterpret_cast<const unsigned char*>(M) + start, tl, &full[s], pol_stream);
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------------ consumers
   const uint64_t pol_x = policy_evict_last();
-
-  auto issue = [=](uint64_t k) {
-    const uint64_t c = blockIdx.x + k * gridDim.x;
-    if (c >= nchunks) return;
-    const int s = (int)(k % S);
-    unsigned char* dst = in_ring + (size_t)s * in_stage_bytes;
-    const uint64_t start = c * (uint64_t)chunk_in;
-    const uint32_t len = start < main_bytes ? (uint32_t)umin64(chunk_in, main_bytes - start) : 0u;
-    const uint32_t tl = len & ~15u;
-    if (len > tl)  // an 8-byte tail the bulk copy cannot take; made visible by the arrive (release)
-      *reinterpret_cast<uint64_t*>(dst + tl) = *reinterpret_cast<const uint64_t*>(
-          reinterpret_cast<const unsigned char*>(M) + start + tl);
-    mbar_arrive_expect_tx(&bar[s], tl);
-    if (tl) tma_load_1d(dst, reinterpret_cast<const unsigned char*>(M) + start, tl, &bar[s], pol_stream);
-  };
-  if (threadIdx.x == 0)
-    for (int k = 0; k < S; ++k) issue(k);
-
-  // lane constants: unpack (row `lane` of a group) and pack (output word `lane`)
   const uint32_t us = lane * b, uw0 = us >> 5, uo = us & 31;
   const uint32_t umask = b == 32 ? 0xffffffffu : ((1u << b) - 1);
   const uint32_t pr0 = (32 * lane) / nb, pop = 32 * lane - pr0 * nb;
+  uint32_t* out32 = reinterpret_cast<uint32_t*>(Mout);
   bool bad = false;
 
   for (uint64_t k = 0;; ++k) {
     const uint64_t c = blockIdx.x + k * gridDim.x;
     if (c >= nchunks) break;
     const int s = (int)(k % S);
-    mbar_wait_parity(&bar[s], (uint32_t)((k / S) & 1));
+    mbar_wait_parity(&full[s], (uint32_t)((k / S) & 1));
     const uint32_t* sin = reinterpret_cast<const uint32_t*>(in_ring + (size_t)s * in_stage_bytes);
-    uint32_t* sout = reinterpret_cast<uint32_t*>(out_stage + (size_t)(k & 1) * out_stage_bytes);
     const uint64_t row_base = c * R;
-#pragma unroll 1
-    for (int g0 = w; g0 < G; g0 += W * U) {
-      uint32_t v[U];
+    uint32_t v[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int g = g0 + W * u;
-        const uint64_t row = row_base + (uint64_t)g * 32 + lane;
-        if (row < n_main) {
-          const uint32_t lo = sin[g * b + uw0], hi = sin[g * b + uw0 + 1];
-          uint32_t code = __funnelshift_r(lo, hi, uo) & umask;
-          if (code >= dict_len) {
-            bad = true;
-            code = 0;
-          }
-          v[u] = ld_gather_u32(XM + code, pol_x);
-        } else if (row < n_total) {
-          v[u] = __ldg(XD + __ldg(rank + (row - n_main)));
-        } else {
-          v[u] = 0;
+    for (int u = 0; u < U; ++u) {
+      const int g = warp + CW * u;
+      const uint64_t row = row_base + (uint64_t)g * 32 + lane;
+      if (row < n_main) {
+        const uint32_t lo = sin[g * b + uw0], hi = sin[g * b + uw0 + 1];
+        uint32_t code = __funnelshift_r(lo, hi, uo) & umask;
+        if (code >= dict_len) {
+          bad = true;
+          code = 0;
         }
+        v[u] = XS ? sx[code] : ld_gather_u32(XM + code, pol_x);
+      } else if (row < n_total) {
+        v[u] = __ldg(XD + __ldg(rank + (row - n_main)));
+      } else {
+        v[u] = 0;
       }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);  // stage s fully read by this warp
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int g = g0 + W * u;
-        const uint32_t word = warp_pack<NB>(v[u], nb, pr0, pop);
-        if (lane < nb) sout[g * nb + lane] = word;
-      }
-    }
-    fence_proxy_async_smem();
-    if (threadIdx.x == 0) tma_store_wait_read<0>();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const uint64_t ostart = c * (uint64_t)chunk_out;
-      const uint32_t olen = (uint32_t)umin64(chunk_out, out_bytes - ostart);
-      const uint32_t otl = olen & ~15u;
-      unsigned char* gdst = reinterpret_cast<unsigned char*>(Mout) + ostart;
-      if (otl) {
-        tma_store_1d(gdst, sout, otl, pol_stream);
-        tma_store_commit();
-      }
-      if (olen > otl)
-        *reinterpret_cast<uint64_t*>(gdst + otl) =
-            *reinterpret_cast<const uint64_t*>(reinterpret_cast<const unsigned char*>(sout) + otl);
-      issue(k + S);
+    for (int u = 0; u < U; ++u) {
+      const int g = warp + CW * u;
+      const uint32_t word = warp_pack<NB>(v[u], nb, pr0, pop);
+      const uint64_t ow = (c * G + g) * nb + lane;
+      if (lane < nb && ow < nw32) __stcs(out32 + ow, word);
     }
   }
-  if (bad) s_bad = 1;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    tma_store_wait_all<0>();
-    if (s_bad) atomicMin(&hdr->status, (int)DM_E_CODE_RANGE);
-  }
+  if (__any_sync(FULL, bad) && lane == 0) atomicMin(&hdr->status, (int)DM_E_CODE_RANGE);
 }
 
 __global__ void __launch_bounds__(256) k_pack(const uint32_t* __restrict__ codes, uint64_t n, uint32_t bits,
@@ -206,23 +197,28 @@ __global__ void __launch_bounds__(256) k_unpack(const uint32_t* __restrict__ wor
 
 template <int NB>
 cudaError_t launch_nb(const dm_column_in* in, const dm_column_out* out, const uint32_t* xm, const uint32_t* xd,
-                      const uint32_t* rank, dm_header* hdr, cudaStream_t st, uint32_t nb_cap,
-                      uint32_t fixed_bits) {
+                      const uint32_t* rank, dm_header* hdr, cudaStream_t st, uint32_t nb_cap, uint32_t fixed_bits) {
+  (void)nb_cap;
   const uint32_t in_stage = kRecGroups * in->main_bits * 4 + 16;
-  const uint32_t out_stage = kRecGroups * nb_cap * 4;
-  const size_t smem = 128 + (size_t)kRecStages * in_stage + 2 * (size_t)out_stage;
-  cudaFuncSetAttribute(k_recompress<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const bool xs = in->dict_len * 4 <= kRecSmemXBytes;
+  const size_t smem = 128 + (size_t)kRecStages * in_stage + (xs ? in->dict_len * 4 : 0);
   int dev = 0, sms = 148, occ = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_recompress<NB>, kRecThreads, smem);
-  if (occ < 1) occ = 1;
   const uint64_t n_total = in->n_main + in->n_delta;
   const uint64_t nchunks = (n_total + 32ull * kRecGroups - 1) / (32ull * kRecGroups);
-  const unsigned grid = (unsigned)std::min<uint64_t>(nchunks, (uint64_t)sms * occ);
-  k_recompress<NB><<<grid, kRecThreads, smem, st>>>(in->main_codes, in->n_main, in->main_bits, in->dict_len, xm, xd,
-                                                    rank, in->n_delta, out->merged_codes, hdr, in_stage, out_stage,
-                                                    fixed_bits);
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kRecThreads, smem);
+    if (occ < 1) occ = 1;
+    const unsigned grid = (unsigned)std::min<uint64_t>(nchunks, (uint64_t)sms * occ);
+    kern<<<grid, kRecThreads, smem, st>>>(in->main_codes, in->n_main, in->main_bits, in->dict_len, xm, xd, rank,
+                                          in->n_delta, out->merged_codes, hdr, in_stage, fixed_bits);
+  };
+  if (xs)
+    go(k_recompress<NB, true>);
+  else
+    go(k_recompress<NB, false>);
   note_launch();
   return cudaGetLastError();
 }
