@@ -192,27 +192,44 @@ def main():
     torch.cuda.synchronize()
     r0 = merger.result()
 
-    # ---- timed region: K steps, L2 flushed before each, events on the launching stream
+    # ---- per-step breakdown (eager launches, events at the step boundaries)
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     for row in ev:  # torch creates the CUDA event lazily on first record
         for e in row:
             e.record()
-    if pg:
-        pg.barrier()
     torch.cuda.synchronize()
     launches0 = dm.launch_count()
-    with ClockSampler(local) as clk:
-        for k in range(args.steps):
-            flush.zero_()
-            merger.run_async_timed(ev[k])
-        torch.cuda.synchronize()
-    launches = dm.launch_count() - launches0
-    if pg:
-        pg.barrier()
-    step_ms = [ev[k][0].elapsed_time(ev[k][3]) for k in range(args.steps)]
+    for k in range(args.steps):
+        flush.zero_()
+        merger.run_async_timed(ev[k])
+    torch.cuda.synchronize()
+    launches_per_merge = (dm.launch_count() - launches0) / max(args.steps, 1)
     s1a = [ev[k][0].elapsed_time(ev[k][1]) for k in range(args.steps)]
     s1b = [ev[k][1].elapsed_time(ev[k][2]) for k in range(args.steps)]
     s2 = [ev[k][2].elapsed_time(ev[k][3]) for k in range(args.steps)]
+    eager_ms = [ev[k][0].elapsed_time(ev[k][3]) for k in range(args.steps)]
+
+    # ---- timed region: K whole merges replayed from a CUDA graph (one driver call
+    # each), L2 flushed before each, CUDA events around each merge on its stream
+    merger.capture_graph()
+    gev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for a, b in gev:
+        a.record()
+        b.record()
+    if pg:
+        pg.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.zero_()
+            gev[k][0].record()
+            merger.replay_graph()
+            gev[k][1].record()
+        torch.cuda.synchronize()
+    launches = int(round(launches_per_merge * args.steps))
+    if pg:
+        pg.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in gev]
     total_ms = sum(step_ms)
     if pg:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
@@ -282,7 +299,10 @@ def main():
                        "parallelism": f"column-sharded x{world} (independent columns, no collective)",
                        "l2": "flushed (512 MB write) before every timed step"},
             "steps_ms": {"s1a_delta_dict": statistics.mean(s1a), "s1b_dict_merge": statistics.mean(s1b),
-                         "s2b_recompress": s2_ms, "total": statistics.mean(step_ms)},
+                         "s2b_recompress": s2_ms, "eager_total": statistics.mean(eager_ms),
+                         "graph_total": statistics.mean(step_ms),
+                         "note": "s1a/s1b/s2b from eager launches with events between steps; "
+                                 "value/ms_per_step from CUDA-graph replays"},
             "hbm_fraction_strict": strict_bytes / (statistics.mean(step_ms) / 1e3) / 1e9 / peak_hbm,
             "roofline": {"kernel": "k_recompress (Step 2(b))", "bound": "hbm", "achieved": achieved,
                          "peak": peak_hbm, "unit": "GB/s", "frac": achieved / peak_hbm, "traffic": traffic,

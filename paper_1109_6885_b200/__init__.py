@@ -80,7 +80,7 @@ def _lib():
             raise ImportError(f"libdictmerge.so is not built ({_build.LIB}); run "
                               "`python -m paper_1109_6885_b200.build` or __graft_entry__.build(). "
                               "There is no CPU fallback.")
-        L = ctypes.CDLL(_build.LIB)
+        L = ctypes.CDLL(os.environ.get("DM_LIB_PATH", _build.LIB))
         u64, u32, vp, i32 = ctypes.c_uint64, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_int
         P = ctypes.POINTER
         sig = {
@@ -206,6 +206,22 @@ class ColumnMerger:
                                           self.ws_bytes, self.hdr.data_ptr(), _stream_handle(stream))
         if st != Status.OK:
             raise DictMergeError(st, "dm_merge_column_async")
+
+    def capture_graph(self) -> "torch.cuda.CUDAGraph":
+        """Capture one whole merge (memset + all kernels, no host sync) into a CUDA
+        graph; ``replay_graph`` then relaunches it with one driver call."""
+        self.run_async()  # warm the library's per-device launch caches outside capture
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        with torch.cuda.graph(g, stream=side):
+            self.run_async()
+        torch.cuda.synchronize()
+        self.graph = g
+        return g
+
+    def replay_graph(self) -> None:
+        self.graph.replay()
 
     def run_async_timed(self, events, stream=None) -> None:
         """As run_async, recording 4 torch.cuda.Events at the step boundaries

@@ -27,6 +27,13 @@ def up_to_date() -> bool:
     return os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(p) for p in _inputs())
 
 
+def build_trace() -> str:
+    """Diagnostic variant with %globaltimer phase stamps (-DDM_TRACE); not used by the product path."""
+    out = os.path.join(HERE, "libdictmerge_trace.so")
+    subprocess.check_call([NVCC, *FLAGS, "-DDM_TRACE", *sources(), "-o", out])
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return LIB

@@ -8,43 +8,44 @@
 // raw insertion-order array (BASELINE.json north_star), so the sort happens at
 // merge time:
 //
-//   k_hist       one read of D: all digit histograms (8 or 16 passes) at once
-//   k_plan       exclusive digit offsets per pass; passes whose digit is constant
-//                over every key are skipped (device-decided, no host sync)
-//   k_onesweep   one LSD pass: stable warp-multisplit ranking in shared memory,
-//                per-digit decoupled look-back across tiles, coalesced scatter
-//   k_unique     head flags over the sorted keys, single-pass scan (look-back) ->
-//                U_D[rank] and r[original index] = rank
+//   k_hist       one read of D: all digit histograms (8 or 16 byte passes) at
+//                once; the last block to finish turns them into the pass plan:
+//                exclusive digit offsets, and passes whose byte is constant over
+//                every key are skipped (device-decided, no host sync)
+//   k_onesweep   one stable LSD pass: warp-multisplit ranking (match.any) in
+//                shared memory, local reorder, per-digit decoupled look-back
+//                across tiles (32 predecessors per round trip), scatter
+//   k_unique     head flags over the sorted keys (warp ballots), single-pass
+//                scan with look-back -> U_D[rank] and r[original index] = rank
 #include "dm_device.cuh"
+
+#ifdef DM_TRACE
+__device__ unsigned long long dm_trace_buf[8 * 32];
+extern "C" int dm_debug_trace(unsigned long long* host) {
+  return (int)cudaMemcpyFromSymbol(host, dm_trace_buf, sizeof(dm_trace_buf));
+}
+__device__ __forceinline__ void dm_trace(int slot) {
+  if (threadIdx.x == 0 && blockIdx.x < 8) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    dm_trace_buf[blockIdx.x * 32 + slot] = t;
+  }
+}
+#define DM_T(slot) dm_trace(slot)
+#else
+#define DM_T(slot)
+#endif
 
 namespace dm {
 namespace {
 
-template <class KT>
-__global__ void __launch_bounds__(256) k_hist(const void* __restrict__ D, uint64_t n, uint32_t* __restrict__ hist) {
-  constexpr int P = KT::kPasses;
-  __shared__ uint32_t s_h[P][256];
-  for (int i = threadIdx.x; i < P * 256; i += blockDim.x) (&s_h[0][0])[i] = 0;
-  __syncthreads();
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    const typename KT::K k = KT::load(D, i);
-#pragma unroll
-    for (int p = 0; p < P; ++p) atomicAdd(&s_h[p][KT::digit(k, p)], 1u);
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < P * 256; i += blockDim.x) {
-    const uint32_t c = (&s_h[0][0])[i];
-    if (c) atomicAdd(&hist[i], c);
-  }
-}
-
-__global__ void __launch_bounds__(256) k_plan(const uint32_t* __restrict__ hist, uint64_t n, int npass,
-                                              SortPlan* __restrict__ plan) {
+__device__ void build_plan(const uint32_t* hist, uint64_t n, int npass, SortPlan* plan) {
+  // Called by one block of 256 threads (the last k_hist block).
   __shared__ uint32_t s_warp[9];
   __shared__ int s_active[16];
   const int t = threadIdx.x;
   for (int p = 0; p < npass; ++p) {
-    const uint32_t c = hist[p * 256 + t];
+    const uint32_t c = t < 256 ? __ldcg(hist + p * 256 + t) : 0u;
     const int full = __syncthreads_or(c == (uint32_t)n);
     uint32_t total;
     const uint32_t ex = block_exclusive_scan<256>(c, s_warp, total);
@@ -72,29 +73,63 @@ __global__ void __launch_bounds__(256) k_plan(const uint32_t* __restrict__ hist,
   }
 }
 
-// One stable LSD radix pass over (key, original-index) pairs.
+template <class KT>
+__global__ void __launch_bounds__(256) k_hist(const void* __restrict__ D, uint64_t n, uint32_t* __restrict__ hist,
+                                              uint32_t* done, SortPlan* __restrict__ plan) {
+  constexpr int P = KT::kPasses;
+  __shared__ uint32_t s_h[P][256];
+  __shared__ bool s_last;
+  for (int i = threadIdx.x; i < P * 256; i += blockDim.x) (&s_h[0][0])[i] = 0;
+  __syncthreads();
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const typename KT::K k = KT::load(D, i);
+#pragma unroll
+    for (int p = 0; p < P; ++p) atomicAdd(&s_h[p][KT::digit(k, p)], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < P * 256; i += blockDim.x) {
+    const uint32_t c = (&s_h[0][0])[i];
+    if (c) atomicAdd(&hist[i], c);
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    build_plan(hist, n, P, plan);
+  }
+}
+
+// One stable LSD radix pass over (key, original-index) pairs.  NT threads,
+// ITEMS keys per thread, tile = NT * ITEMS keys in (warp, item, lane) order.
 template <class KT, int ITEMS>
 __global__ void __launch_bounds__(kSortThreads) k_onesweep(const void* __restrict__ D, void* kbuf0, void* kbuf1,
                                                           uint32_t* vbuf0, uint32_t* vbuf1, uint64_t n, int pass,
                                                           const SortPlan* __restrict__ plan, uint32_t* status,
                                                           uint32_t* counter) {
   using K = typename KT::K;
-  constexpr int W = kSortThreads / 32;
-  constexpr int TILE = kSortThreads * ITEMS;
+  constexpr int NT = kSortThreads;
+  constexpr int W = NT / 32;
+  constexpr int TILE = NT * ITEMS;
+  DM_T(0);
   if (!plan->active[pass]) return;
+  DM_T(1);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   K* s_keys = reinterpret_cast<K*>(smem_raw);
   uint32_t* s_vals = reinterpret_cast<uint32_t*>(smem_raw + sizeof(K) * TILE);
   __shared__ uint32_t s_whist[W][257];
   __shared__ uint32_t s_bstart[256];
   __shared__ uint32_t s_gofs[256];
+  __shared__ uint32_t s_tcnt[256];
   __shared__ uint32_t s_warp[W + 1];
   __shared__ uint32_t s_tile;
 
   const unsigned lane = lane_id(), w = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < W * 257; i += kSortThreads) (&s_whist[0][0])[i] = 0;
+  for (int i = threadIdx.x; i < W * 257; i += NT) (&s_whist[0][0])[i] = 0;
   if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
   __syncthreads();
+  DM_T(2);
   const uint64_t tile = s_tile;
   const uint64_t base = tile * TILE;
   const int src = plan->src[pass];
@@ -107,24 +142,23 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const void* __restric
   uint32_t val[ITEMS];
   uint32_t dig[ITEMS];
   uint32_t rnk[ITEMS];
+  // All loads first, branch-free (clamped index), so they are in flight together.
+  const bool from_input = src == SEL_INPUT;
+  const void* kp = from_input ? D : ksrc;
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     const uint64_t idx = base + (uint64_t)w * 32 * ITEMS + (uint64_t)i * 32 + lane;
-    if (idx < n) {
-      if (src == SEL_INPUT) {
-        key[i] = KT::load(D, idx);
-        val[i] = (uint32_t)idx;
-      } else {
-        key[i] = NumStore<KT>::ld(ksrc, idx);
-        val[i] = vsrc[idx];
-      }
-      dig[i] = KT::digit(key[i], pass);
-    } else {
-      dig[i] = 256;  // out of range: private bucket, never published
-    }
+    const uint64_t ic = idx < n ? idx : n - 1;
+    key[i] = KT::ld_any(kp, ic, from_input);
+    val[i] = from_input ? (uint32_t)idx : vsrc[ic];
   }
-  // Stable warp-level multisplit: keys are ranked in (warp, item, lane) order,
-  // which is their input order.
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const uint64_t idx = base + (uint64_t)w * 32 * ITEMS + (uint64_t)i * 32 + lane;
+    dig[i] = idx < n ? KT::digit(key[i], pass) : 256u;  // 256: private bucket, never published
+  }
+  DM_T(3);
+  // Stable warp-level multisplit: ranks in (warp, item, lane) order = input order.
   const unsigned lt = lanemask_lt();
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
@@ -140,48 +174,30 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const void* __restric
     __syncwarp();
   }
   __syncthreads();
-  // Per digit: exclusive offsets across warps, the tile's count, the look-back.
-  const int d = threadIdx.x;  // kSortThreads == 256 digits
-  uint32_t run = 0;
+  DM_T(4);
+  // Per digit: exclusive offsets across warps and the tile's count; publish the
+  // aggregate right away so successors can start their look-back.
+  const int d = threadIdx.x;
+  uint32_t tile_cnt = 0;
+  if (d < 256) {
+    uint32_t run = 0;
 #pragma unroll
-  for (int ww = 0; ww < W; ++ww) {
-    const uint32_t c = s_whist[ww][d];
-    s_whist[ww][d] = run;
-    run += c;
-  }
-  const uint32_t tile_cnt = run;
-  uint32_t* my = status + tile * 256 + d;
-  uint32_t excl = 0;
-  if (tile == 0) {
-    st_volatile_u32(my, kRadixFlagPre | tile_cnt);
-  } else {
-    st_volatile_u32(my, kRadixFlagAgg | tile_cnt);
-    // Look back LB predecessors per round trip (independent loads in flight),
-    // so a first wave of T tiles resolves in ~T/LB round trips, not T.
-    constexpr int LB = 32;
-    bool done = false;
-    for (int64_t t0 = (int64_t)tile - 1; !done; t0 -= LB) {
-      uint32_t s[LB];
-#pragma unroll
-      for (int j = 0; j < LB; ++j)
-        s[j] = t0 - j >= 0 ? ld_volatile_u32(status + (uint64_t)(t0 - j) * 256 + d) : kRadixFlagPre;
-#pragma unroll
-      for (int j = 0; j < LB; ++j) {
-        if (!done) {
-          while ((s[j] >> 30) == 0) s[j] = ld_volatile_u32(status + (uint64_t)(t0 - j) * 256 + d);
-          excl += s[j] & kRadixValMask;
-          done = (s[j] >> 30) == 2;
-        }
-      }
+    for (int ww = 0; ww < W; ++ww) {
+      const uint32_t c = s_whist[ww][d];
+      s_whist[ww][d] = run;
+      run += c;
     }
-    st_volatile_u32(my, kRadixFlagPre | (excl + tile_cnt));
+    tile_cnt = run;
+    s_tcnt[d] = run;
+    st_volatile_u32(status + tile * 256 + d, (tile == 0 ? kRadixFlagPre : kRadixFlagAgg) | tile_cnt);
   }
   uint32_t tot;
-  const uint32_t bstart = block_exclusive_scan<kSortThreads>(tile_cnt, s_warp, tot);
-  s_bstart[d] = bstart;
-  s_gofs[d] = plan->digit_base[pass][d] + excl - bstart;
+  const uint32_t bstart = block_exclusive_scan<NT>(d < 256 ? tile_cnt : 0u, s_warp, tot);
+  if (d < 256) s_bstart[d] = bstart;
   __syncthreads();
-  // Local reorder into shared memory (block-sorted by digit), then coalesced-ish writes.
+  DM_T(5);
+  // Local reorder into shared memory (block-sorted by digit): frees the registers
+  // before the look-back.
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     if (dig[i] < 256) {
@@ -190,17 +206,46 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const void* __restric
       s_vals[pos] = val[i];
     }
   }
+  DM_T(6);
+  if (d < 256) {
+    uint32_t excl = 0;
+    if (tile > 0) {
+      // LB predecessors per round trip: a first wave of T tiles resolves in ~T/LB trips.
+      constexpr int LB = 32;
+      bool done = false;
+      for (int64_t t0 = (int64_t)tile - 1; !done; t0 -= LB) {
+        uint32_t s[LB];
+#pragma unroll
+        for (int j = 0; j < LB; ++j)
+          s[j] = t0 - j >= 0 ? ld_volatile_u32(status + (uint64_t)(t0 - j) * 256 + d) : kRadixFlagPre;
+#pragma unroll
+        for (int j = 0; j < LB; ++j) {
+          if (!done) {
+            while ((s[j] >> 30) == 0) s[j] = ld_volatile_u32(status + (uint64_t)(t0 - j) * 256 + d);
+            excl += s[j] & kRadixValMask;
+            done = (s[j] >> 30) == 2;
+          }
+        }
+      }
+      st_volatile_u32(status + tile * 256 + d, kRadixFlagPre | (excl + s_tcnt[d]));
+    }
+    s_gofs[d] = plan->digit_base[pass][d] + excl - s_bstart[d];
+  }
   __syncthreads();
+  DM_T(7);
   const uint32_t valid = (uint32_t)umin64(TILE, n - base);
-  for (uint32_t j = threadIdx.x; j < valid; j += kSortThreads) {
+#pragma unroll 4
+  for (uint32_t j = threadIdx.x; j < valid; j += NT) {
     const K k = s_keys[j];
     const uint32_t dst = s_gofs[KT::digit(k, pass)] + j;
     NumStore<KT>::st(kdst, dst, k);
     vdst[dst] = s_vals[j];
   }
+  DM_T(8);
 }
 
 // Head flags + single-pass scan over the sorted keys -> U_D and r.
+// Warp-striped layout: element (w, i, l) is position base + w*32*ITEMS + i*32 + l.
 template <class KT>
 __global__ void __launch_bounds__(kUniqThreads) k_unique(const void* __restrict__ D, const void* kbuf0,
                                                         const void* kbuf1, const uint32_t* vbuf0,
@@ -209,8 +254,9 @@ __global__ void __launch_bounds__(kUniqThreads) k_unique(const void* __restrict_
                                                         uint32_t* counter, void* __restrict__ udict,
                                                         uint32_t* __restrict__ rank, dm_header* hdr) {
   using K = typename KT::K;
-  constexpr int TILE = kUniqThreads * kUniqItems;
-  __shared__ uint32_t s_warp[kUniqThreads / 32 + 1];
+  constexpr int NT = kUniqThreads, ITEMS = kUniqItems, W = NT / 32;
+  constexpr int TILE = NT * ITEMS;
+  __shared__ uint32_t s_warp[W + 1];
   __shared__ uint64_t s_excl;
   __shared__ uint32_t s_tile;
   if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
@@ -219,45 +265,68 @@ __global__ void __launch_bounds__(kUniqThreads) k_unique(const void* __restrict_
   const int sel = plan->final_sel;
   const void* ks = sel == SEL_BUF0 ? kbuf0 : kbuf1;
   const uint32_t* vs = sel == SEL_BUF0 ? vbuf0 : vbuf1;
-  auto key_at = [&](uint64_t p) -> K { return sel == SEL_INPUT ? KT::load(D, p) : NumStore<KT>::ld(ks, p); };
-  auto val_at = [&](uint64_t p) -> uint32_t { return sel == SEL_INPUT ? (uint32_t)p : vs[p]; };
+  const bool from_input = sel == SEL_INPUT;
+  const void* kp = from_input ? D : ks;
+  auto val_at = [&](uint64_t p) -> uint32_t { return from_input ? (uint32_t)p : vs[p]; };
 
-  const uint64_t p0 = tile * TILE + (uint64_t)threadIdx.x * kUniqItems;
-  K key[kUniqItems];
-  uint32_t head = 0;  // bitmask over items
-  uint32_t cnt = 0;
-  K prev;
-  if (p0 < n && p0 > 0) prev = key_at(p0 - 1);
+  const unsigned lane = lane_id(), w = threadIdx.x >> 5;
+  const uint64_t wbase = tile * TILE + (uint64_t)w * 32 * ITEMS;
+  K key[ITEMS];
+  uint32_t hb[ITEMS];  // head ballots per item
+  uint32_t wcount = 0;
+  // the element just before this warp's first element (branch-free, clamped)
+  K before = KT::ld_any(kp, wbase > 0 ? umin64(wbase - 1, n - 1) : 0, from_input);
 #pragma unroll
-  for (int i = 0; i < kUniqItems; ++i) {
-    const uint64_t p = p0 + i;
-    if (p < n) {
-      key[i] = key_at(p);
-      const bool h = (p == 0) || !KT::eq(key[i], prev);
-      head |= (uint32_t)h << i;
-      cnt += h;
-      prev = key[i];
-    }
+  for (int i = 0; i < ITEMS; ++i) {
+    const uint64_t p = wbase + (uint64_t)i * 32 + lane;
+    key[i] = KT::ld_any(kp, p < n ? p : n - 1, from_input);
   }
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const uint64_t p = wbase + (uint64_t)i * 32 + lane;
+    // previous element: lane-1 of this item, lane 31 of the previous item, or `before`
+    K prev;
+    if constexpr (sizeof(K) == 8) {
+      uint64_t up = __shfl_up_sync(FULL, (uint64_t)key[i], 1);
+      uint64_t last = i > 0 ? __shfl_sync(FULL, (uint64_t)key[i > 0 ? i - 1 : 0], 31) : (uint64_t)before;
+      if (i == 0) last = __shfl_sync(FULL, (uint64_t)before, 0);
+      prev = (K)(lane == 0 ? last : up);
+    } else {
+      K128 kk = *reinterpret_cast<K128*>(&key[i]);
+      K128 pk = *reinterpret_cast<K128*>(&key[i > 0 ? i - 1 : 0]);
+      K128 bk = *reinterpret_cast<K128*>(&before);
+      uint64_t uh = __shfl_up_sync(FULL, kk.hi, 1), ul = __shfl_up_sync(FULL, kk.lo, 1);
+      uint64_t lh = i > 0 ? __shfl_sync(FULL, pk.hi, 31) : __shfl_sync(FULL, bk.hi, 0);
+      uint64_t ll = i > 0 ? __shfl_sync(FULL, pk.lo, 31) : __shfl_sync(FULL, bk.lo, 0);
+      K128 r = lane == 0 ? K128{lh, ll} : K128{uh, ul};
+      prev = *reinterpret_cast<K*>(&r);
+    }
+    const bool h = p < n && (p == 0 || !KT::eq(key[i], prev));
+    hb[i] = __ballot_sync(FULL, h);
+    wcount += __popc(hb[i]);
+  }
+  // block scan over warp counts (lane 0 of each warp contributes)
   uint32_t tile_cnt;
-  const uint32_t texcl = block_exclusive_scan<kUniqThreads>(cnt, s_warp, tile_cnt);
+  const uint32_t wex = block_exclusive_scan<NT>(lane == 0 ? wcount : 0u, s_warp, tile_cnt);
+  const uint32_t wexcl = __shfl_sync(FULL, wex, 0);
   if (threadIdx.x < 32) {
     const uint64_t e = lookback_exclusive(status, tile, tile_cnt);
     if (threadIdx.x == 0) s_excl = e;
   }
   __syncthreads();
-  uint64_t r = s_excl + texcl;  // number of heads strictly before p0
+  uint64_t run = s_excl + wexcl;  // heads strictly before this warp's first element
+  const unsigned lt = lanemask_lt();
 #pragma unroll
-  for (int i = 0; i < kUniqItems; ++i) {
-    const uint64_t p = p0 + i;
+  for (int i = 0; i < ITEMS; ++i) {
+    const uint64_t p = wbase + (uint64_t)i * 32 + lane;
+    const uint64_t r = run + __popc(hb[i] & lt);  // heads before p
+    const bool h = (hb[i] >> lane) & 1;
     if (p < n) {
-      if ((head >> i) & 1) {
-        KT::store(udict, r, key[i]);
-        ++r;
-      }
-      rank[val_at(p)] = (uint32_t)(r - 1);
-      if (p == n - 1) hdr->delta_dict_len = r;
+      if (h) KT::store(udict, r, key[i]);
+      rank[val_at(p)] = (uint32_t)(r + h - 1);
+      if (p == n - 1) hdr->delta_dict_len = r + h;
     }
+    run += __popc(hb[i]);
   }
 }
 
@@ -269,13 +338,12 @@ cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, void* udict
   uint32_t* hist = reinterpret_cast<uint32_t*>(ws + L.hist);
   SortPlan* plan = reinterpret_cast<SortPlan*>(ws + L.plan);
   const int hist_blocks = (int)std::min<uint64_t>((n + 4095) / 4096, 148 * 4);
-  k_hist<KT><<<hist_blocks, 256, 0, st>>>(in->delta, n, hist);
-  k_plan<<<1, 256, 0, st>>>(hist, n, KT::kPasses, plan);
-  note_launch(2);
+  k_hist<KT><<<hist_blocks, 256, 0, st>>>(in->delta, n, hist, counters + CNT_HIST, plan);
+  note_launch();
   using K = typename KT::K;
   constexpr int TILE = kSortThreads * ITEMS;
   const size_t dsmem = (sizeof(K) + sizeof(uint32_t)) * TILE;
-  cudaFuncSetAttribute(k_onesweep<KT, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem);
+  ensure_smem((const void*)k_onesweep<KT, ITEMS>);
   const uint64_t ntiles = (n + TILE - 1) / TILE;
   for (int p = 0; p < KT::kPasses; ++p) {
     uint32_t* status = reinterpret_cast<uint32_t*>(ws + L.status_sort) + (uint64_t)p * ntiles * 256;

@@ -131,8 +131,22 @@ struct TileRank {
     sq = sc + (T + 2);
     se = sq + (T + 2);
     if (threadIdx.x == 0 && has_prev) sk[0] = KT::load(A, i0 - 1);
-    for (uint32_t k = threadIdx.x; k < na; k += kMergeThreads) sk[1 + k] = KT::load(A, i0 + k);
-    for (uint32_t k = threadIdx.x; k < nb; k += kMergeThreads) sk[1 + na + k] = KT::load(B, j0 + k);
+    {
+      // na + nb <= kMergeTile: at most kMergeItems strided slots per thread; all
+      // loads are issued before the first shared store (branch-free, clamped).
+      K v[kMergeItems];
+#pragma unroll
+      for (int r = 0; r < kMergeItems; ++r) {
+        const uint32_t k = threadIdx.x + r * kMergeThreads;
+        const bool in_a = k < na || nb == 0;  // tile is non-empty, so one side exists
+        v[r] = in_a ? KT::load(A, i0 + umin32(k, na - 1)) : KT::load(B, j0 + umin32(k - na, nb - 1));
+      }
+#pragma unroll
+      for (int r = 0; r < kMergeItems; ++r) {
+        const uint32_t k = threadIdx.x + r * kMergeThreads;
+        if (k < na + nb) sk[1 + k] = v[r];
+      }
+    }
     const uint32_t nc = (small_b ? na : nb) + 1;
     for (uint32_t k = threadIdx.x; k < nc; k += kMergeThreads) sc[k] = 0;
     for (uint32_t k = threadIdx.x; k <= nb; k += kMergeThreads) se[k] = 0;
@@ -266,21 +280,20 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_write(const void* __res
   using K = typename KT::K;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t s_warp[kMergeThreads / 32 + 1];
-  __shared__ int s_unsorted;
-  if (threadIdx.x == 0) s_unsorted = 0;
   TileRank<KT> tr;
   const uint64_t tile = blockIdx.x;
+  const uint64_t D0 = excl[tile];  // issued early; consumed after the ranking
   if (!tr.setup(A, nA, B, hdr->delta_dict_len, part, tile, smem_raw, s_warp)) return;
-  K* s_out = reinterpret_cast<K*>(smem_raw + tile_smem_bytes(sizeof(K)));  // U' staging [kMergeTile]
-  const uint64_t D0 = excl[tile];
   const uint64_t base = tr.d0 - D0;  // first U' index this tile writes
+  // U' is written directly: consecutive U_M elements land at consecutive slots
+  // except at the (few, for U_D-sparse tiles) insertion points.
   bool unsorted = false;
   for (uint32_t a = threadIdx.x; a < tr.na; a += kMergeThreads) {
     uint32_t nbb, dupb;
     tr.a_rank(a, nbb, dupb);
     const uint32_t o = a + nbb - dupb;  // tile-local U' slot
     const K v = tr.A_(a);
-    s_out[o] = v;
+    KT::store(U, base + o, v);
     XM[tr.i0 + a] = (uint32_t)(base + o);
     // strictly increasing U_M over the pairs this tile owns
     if ((a > 0 || tr.has_prev) && !KT::lt(a > 0 ? tr.A_(a - 1) : tr.sk[0], v)) unsorted = true;
@@ -292,15 +305,11 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_write(const void* __res
     if (dup) {
       XD[tr.j0 + j] = (uint32_t)(base + o - 1);  // its U_M twin's index
     } else {
-      s_out[o] = tr.B_(j);
+      KT::store(U, base + o, tr.B_(j));
       XD[tr.j0 + j] = (uint32_t)(base + o);
     }
   }
-  if (unsorted) s_unsorted = 1;
-  __syncthreads();
-  const uint32_t n_out = tr.na + tr.nb - tr.dups();
-  for (uint32_t k = threadIdx.x; k < n_out; k += kMergeThreads) KT::store(U, base + k, s_out[k]);
-  if (threadIdx.x == 0 && s_unsorted) atomicMin(&hdr->status, (int)DM_E_UNSORTED);
+  if (__any_sync(FULL, unsorted) && lane_id() == 0) atomicMin(&hdr->status, (int)DM_E_UNSORTED);
 }
 
 __global__ void k_empty_header(dm_header* hdr) {
@@ -327,14 +336,14 @@ cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, const void*
   k_partition<KT><<<(unsigned)((nt + 1 + 7) / 8), 256, 0, st>>>(in->main_dict, in->dict_len, udict, hdr, nt + 1,
                                                                    part);
   const size_t smem_count = sizeof(K) * (kMergeTile + 1) + 3 * sizeof(uint32_t) * (kMergeTile + 2);
-  cudaFuncSetAttribute(k_merge_count<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_count);
+  ensure_smem((const void*)k_merge_count<KT>);
   k_merge_count<KT><<<(unsigned)nt, kMergeThreads, smem_count, st>>>(in->main_dict, in->dict_len, udict, part, hdr,
                                                                      cnt);
   k_scan_counts<<<(unsigned)((nt + 2047) / 2048), 256, 0, st>>>(
       cnt, nt, excl, reinterpret_cast<uint64_t*>(ws + L.status_merge),
       reinterpret_cast<uint32_t*>(ws + L.counters) + CNT_MERGE, in->dict_len, hdr);
-  const size_t smem_write = smem_count + sizeof(K) * kMergeTile;
-  cudaFuncSetAttribute(k_merge_write<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_write);
+  const size_t smem_write = smem_count;
+  ensure_smem((const void*)k_merge_write<KT>);
   k_merge_write<KT><<<(unsigned)nt, kMergeThreads, smem_write, st>>>(in->main_dict, in->dict_len, udict, part, excl,
                                                                      U, xm, xd, hdr);
   note_launch(4);

@@ -6,7 +6,9 @@
 #include <algorithm>
 #include <atomic>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "dm_internal.h"
@@ -17,6 +19,61 @@ static std::atomic<uint64_t> g_launches{0};
 static std::atomic<int> g_last_cuda{0};
 
 void note_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+namespace {
+std::mutex g_cache_mu;
+struct FuncKey {
+  const void* f;
+  int dev;
+  size_t smem;
+  int threads;
+  bool operator<(const FuncKey& o) const {
+    return std::tie(f, dev, smem, threads) < std::tie(o.f, o.dev, o.smem, o.threads);
+  }
+};
+std::map<FuncKey, int> g_func_cache;
+int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+}  // namespace
+
+void ensure_smem(const void* func) {
+  const FuncKey k{func, current_device(), 0, -1};
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  if (g_func_cache.count(k)) return;
+  int optin = 0;
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, k.dev);
+  cudaFuncAttributes fa{};
+  cudaFuncGetAttributes(&fa, func);
+  cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
+  g_func_cache[k] = 1;
+}
+
+int device_sms() {
+  const FuncKey k{nullptr, current_device(), 0, -2};
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  auto it = g_func_cache.find(k);
+  if (it != g_func_cache.end()) return it->second;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, k.dev);
+  g_func_cache[k] = sms;
+  return sms;
+}
+
+int occupancy(const void* func, int threads, size_t smem) {
+  ensure_smem(func);
+  const FuncKey k{func, current_device(), smem, threads};
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  auto it = g_func_cache.find(k);
+  if (it != g_func_cache.end()) return it->second;
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, func, threads, smem);
+  if (occ < 1) occ = 1;
+  g_func_cache[k] = occ;
+  return occ;
+}
 
 uint32_t host_width(uint64_t n) {
   // Eq 4: ceil(log2 n), with a 1-bit minimum (reading A1).

@@ -36,6 +36,10 @@ struct KeyU64 {
   __device__ __forceinline__ static bool lt(K a, K b) { return a < b; }
   __device__ __forceinline__ static bool eq(K a, K b) { return a == b; }
   __device__ __forceinline__ static bool le(K a, K b) { return a <= b; }
+  // raw input and numeric workspace layouts coincide for u64 keys
+  __device__ __forceinline__ static K ld_any(const void* p, uint64_t i, bool /*raw*/) {
+    return static_cast<const uint64_t*>(p)[i];
+  }
 };
 
 // 16-byte keys: raw bytes compared with memcmp (reading A5).  The numeric form
@@ -64,6 +68,11 @@ struct KeyB16 {
   __device__ __forceinline__ static bool lt(K a, K b) { return a.hi < b.hi || (a.hi == b.hi && a.lo < b.lo); }
   __device__ __forceinline__ static bool eq(K a, K b) { return a.hi == b.hi && a.lo == b.lo; }
   __device__ __forceinline__ static bool le(K a, K b) { return !lt(b, a); }
+  // one 16-byte load; raw (input) layout converted to the numeric (hi, lo) form
+  __device__ __forceinline__ static K ld_any(const void* p, uint64_t i, bool raw) {
+    const ulonglong2 v = static_cast<const ulonglong2*>(p)[i];
+    return raw ? K{bswap(v.x), bswap(v.y)} : K{v.x, v.y};
+  }
 };
 
 // Numeric-form storage used inside the workspace (ping-pong sort buffers).

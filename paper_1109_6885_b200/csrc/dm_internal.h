@@ -9,11 +9,11 @@
 namespace dm {
 
 // ---- tiling constants
-constexpr int kSortThreads = 256;
-constexpr int kSortItemsU64 = 16;                        // 4096 keys per onesweep tile
-constexpr int kSortItemsB16 = 8;                         // 2048 keys per tile (16-byte keys)
-constexpr int kUniqThreads = 256;
-constexpr int kUniqItems = 8;                            // 2048 per tile
+constexpr int kSortThreads = 512;
+constexpr int kSortItemsU64 = 16;                        // 8192 keys per onesweep tile
+constexpr int kSortItemsB16 = 8;                         // 4096 keys per tile (16-byte keys)
+constexpr int kUniqThreads = 512;
+constexpr int kUniqItems = 8;                            // 4096 per tile
 constexpr int kMergeThreads = 256;
 constexpr int kMergeItems = 8;                           // 2048 merged-diagonal elements per tile
 constexpr int kMergeTile = kMergeThreads * kMergeItems;
@@ -64,14 +64,18 @@ struct WsLayout {
   int npass;
 };
 
-enum { CNT_SORT = 0, CNT_UNIQUE = 16, CNT_MERGE = 17 };
+enum { CNT_SORT = 0, CNT_UNIQUE = 16, CNT_MERGE = 17, CNT_HIST = 18 };
 
 WsLayout ws_layout(const dm_column_in* in);
 uint32_t host_width(uint64_t n);
 uint64_t host_words(uint64_t n, uint32_t bits);
 
-// ---- launch bookkeeping
+// ---- launch bookkeeping (host; cached so a merge issues no per-launch driver queries)
 void note_launch(int n = 1);
+// Raise the dynamic shared memory limit of `func` to the device maximum, once per device.
+void ensure_smem(const void* func);
+int device_sms();
+int occupancy(const void* func, int threads, size_t smem);
 cudaError_t last_error_check();
 
 // ---- kernel launchers (each .cu file)

@@ -202,15 +202,11 @@ cudaError_t launch_nb(const dm_column_in* in, const dm_column_out* out, const ui
   const uint32_t in_stage = kRecGroups * in->main_bits * 4 + 16;
   const bool xs = in->dict_len * 4 <= kRecSmemXBytes;
   const size_t smem = 128 + (size_t)kRecStages * in_stage + (xs ? in->dict_len * 4 : 0);
-  int dev = 0, sms = 148, occ = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = device_sms();
   const uint64_t n_total = in->n_main + in->n_delta;
   const uint64_t nchunks = (n_total + 32ull * kRecGroups - 1) / (32ull * kRecGroups);
   auto go = [&](auto kern) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kRecThreads, smem);
-    if (occ < 1) occ = 1;
+    const int occ = occupancy((const void*)kern, kRecThreads, smem);
     const unsigned grid = (unsigned)std::min<uint64_t>(nchunks, (uint64_t)sms * occ);
     kern<<<grid, kRecThreads, smem, st>>>(in->main_codes, in->n_main, in->main_bits, in->dict_len, xm, xd, rank,
                                           in->n_delta, out->merged_codes, hdr, in_stage, fixed_bits);
