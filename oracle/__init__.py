@@ -153,3 +153,23 @@ def merge(col, mode: str = "linear", main_words: Optional[np.ndarray] = None) ->
     return MergeResult(
         st, Uo[:n_u].copy(), nb, Mo[: words(nM + nD, nb)].copy(), XM[:nUM].copy(), XD[:n_ud].copy(),
         UD[:n_ud].copy(), R[:nD].copy(), tuple(cout.seconds))
+
+
+def codes_at(main_dict: np.ndarray, delta: np.ndarray, values: np.ndarray, key_bytes: int = 8):
+    """Definitional codes of `values` in U' = set_union(U_M, sorted distinct D).  Returns (codes, |U'|)."""
+    L = lib()
+    L.dmo_codes_at.restype = ctypes.c_int
+    L.dmo_codes_at.argtypes = [ctypes.c_uint32, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_uint64,
+                               ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint64)]
+    kdt = np.uint64 if key_bytes == 8 else np.uint8
+    UM = np.ascontiguousarray(main_dict, dtype=kdt)
+    D = np.ascontiguousarray(delta, dtype=kdt)
+    V = np.ascontiguousarray(values, dtype=kdt)
+    nv = V.shape[0]
+    out = np.zeros(max(nv, 1), dtype=np.uint32)
+    n = ctypes.c_uint64(0)
+    st = L.dmo_codes_at(key_bytes, _ptr(UM), UM.shape[0], _ptr(D), D.shape[0], _ptr(V), nv, out.ctypes.data,
+                        ctypes.byref(n))
+    if st != OK:
+        raise ValueError(f"dmo_codes_at failed: {st}")
+    return out[:nv], int(n.value)

@@ -7,6 +7,7 @@
 #include "dm_oracle.h"
 
 #include <algorithm>
+#include <iterator>
 #include <chrono>
 #include <cstring>
 #include <utility>
@@ -210,6 +211,26 @@ int merge_definitional(const dmo_in* in, dmo_out* out) {
   return DMO_OK;
 }
 
+template <class K>
+int codes_at(const K* UM, uint64_t nUM, const K* D, uint64_t nD, const K* vals, uint64_t nv, uint32_t* codes,
+             uint64_t* merged_len) {
+  for (uint64_t i = 1; i < nUM; ++i)
+    if (!(UM[i - 1] < UM[i])) return DMO_E_UNSORTED;
+  std::vector<K> UD(D, D + nD);
+  std::sort(UD.begin(), UD.end());
+  UD.erase(std::unique(UD.begin(), UD.end()), UD.end());
+  std::vector<K> U;
+  U.reserve(nUM + UD.size());
+  std::set_union(UM, UM + nUM, UD.begin(), UD.end(), std::back_inserter(U));
+  *merged_len = U.size();
+  for (uint64_t i = 0; i < nv; ++i) {
+    auto it = std::lower_bound(U.begin(), U.end(), vals[i]);
+    if (it == U.end() || !(*it == vals[i])) return DMO_E_CODE_RANGE;
+    codes[i] = (uint32_t)(it - U.begin());
+  }
+  return DMO_OK;
+}
+
 bool args_ok(const dmo_in* in, const dmo_out* out) {
   if (!in || !out) return false;
   if (in->key_bytes != 8 && in->key_bytes != 16) return false;
@@ -252,6 +273,18 @@ int dmo_merge_linear(const dmo_in* in, dmo_out* out) {
 int dmo_merge_definitional(const dmo_in* in, dmo_out* out) {
   if (!args_ok(in, out)) return DMO_E_INVALID;
   return in->key_bytes == 8 ? merge_definitional<uint64_t>(in, out) : merge_definitional<K16>(in, out);
+}
+
+int dmo_codes_at(uint32_t key_bytes, const void* main_dict, uint64_t dict_len, const void* delta, uint64_t n_delta,
+                 const void* values, uint64_t n_values, uint32_t* codes, uint64_t* merged_len) {
+  if (key_bytes == 8)
+    return codes_at<uint64_t>(static_cast<const uint64_t*>(main_dict), dict_len,
+                              static_cast<const uint64_t*>(delta), n_delta, static_cast<const uint64_t*>(values),
+                              n_values, codes, merged_len);
+  if (key_bytes == 16)
+    return codes_at<K16>(static_cast<const K16*>(main_dict), dict_len, static_cast<const K16*>(delta), n_delta,
+                         static_cast<const K16*>(values), n_values, codes, merged_len);
+  return DMO_E_INVALID;
 }
 
 }  // extern "C"

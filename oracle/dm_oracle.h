@@ -79,6 +79,15 @@ int dmo_merge_linear(const dmo_in* in, dmo_out* out);
  * M'[i] = position of V[i] in U' by binary search; X_M / X_D likewise. */
 int dmo_merge_definitional(const dmo_in* in, dmo_out* out);
 
+/* Definitional codes for given values (for sampled-row checks of very large
+ * merges): U' = std::set_union(U_M, sorted distinct D) (Eq 3), then
+ * codes[i] = position of values[i] in U' by binary search.
+ * Every value must occur in U_M or D (DMO_E_CODE_RANGE otherwise).
+ * *merged_len receives |U'|. */
+int dmo_codes_at(uint32_t key_bytes, const void* main_dict, uint64_t dict_len, const void* delta,
+                 uint64_t n_delta, const void* values, uint64_t n_values, uint32_t* codes,
+                 uint64_t* merged_len);
+
 #ifdef __cplusplus
 }
 #endif

@@ -186,6 +186,35 @@ static dm_status merge_async(const dm_column_in* in, const dm_column_out* out, v
   return DM_OK;
 }
 
+// Per-device pool of non-blocking streams used by dm_merge_table.
+struct StreamPool {
+  std::vector<cudaStream_t> streams;
+  std::vector<cudaEvent_t> join;
+  cudaEvent_t fork = nullptr;
+};
+constexpr int kTableStreams = 16;
+
+static StreamPool& stream_pool() {
+  static std::mutex mu;
+  static std::map<int, StreamPool> pools;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  StreamPool& p = pools[dev];
+  if (p.streams.empty()) {
+    cudaEventCreateWithFlags(&p.fork, cudaEventDisableTiming);
+    for (int k = 0; k < kTableStreams; ++k) {
+      cudaStream_t s;
+      cudaEvent_t e;
+      if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) break;
+      cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+      p.streams.push_back(s);
+      p.join.push_back(e);
+    }
+  }
+  return p;
+}
+
 struct dm_ctx_impl {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -258,17 +287,38 @@ dm_status dm_merge_table(int ncols, const dm_column_in* in, dm_column_out* out, 
   if (ncols < 0 || (ncols > 0 && (!in || !out || !ws || !ws_bytes))) return DM_E_INVALID;
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
   // Each column is merged separately; the columns are independent
-  // tasks issued back to back on one stream.
+  // tasks.  The GPU form of the paper's task queue: columns, largest
+  // first, are dealt round-robin onto a pool of streams forked from (and joined
+  // back into) the caller's stream, so one column's latency-bound Step 1
+  // kernels overlap other columns' streaming Step 2.
   std::vector<dm_header*> hdrs(ncols);
   for (int c = 0; c < ncols; ++c) {
     const WsLayout L = ws_layout(&in[c]);
     if (!ws[c] || ws_bytes[c] < L.total) return DM_E_CAPACITY;
     hdrs[c] = reinterpret_cast<dm_header*>(static_cast<char*>(ws[c]) + L.hdr);
-    dm_status s = merge_async(&in[c], &out[c], ws[c], ws_bytes[c], hdrs[c], st, false);
+    dm_status v = validate(&in[c], &out[c]);
+    if (v != DM_OK) return v;
+  }
+  std::vector<int> order(ncols);
+  for (int c = 0; c < ncols; ++c) order[c] = c;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+    return in[a].n_main + in[a].n_delta > in[b].n_main + in[b].n_delta;
+  });
+  StreamPool& pool = stream_pool();
+  const int K = std::max(1, std::min<int>(ncols, (int)pool.streams.size()));
+  cudaError_t e = cudaEventRecord(pool.fork, st);
+  for (int k = 0; k < K && e == cudaSuccess; ++k) e = cudaStreamWaitEvent(pool.streams[k], pool.fork, 0);
+  if (e != cudaSuccess) return cuda_fail(e);
+  for (int t = 0; t < ncols; ++t) {
+    const int c = order[t];
+    dm_status s = merge_async(&in[c], &out[c], ws[c], ws_bytes[c], hdrs[c], pool.streams[t % K], false);
     if (s != DM_OK) return s;
   }
+  for (int k = 0; k < K && e == cudaSuccess; ++k) {
+    e = cudaEventRecord(pool.join[k], pool.streams[k]);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, pool.join[k], 0);
+  }
   std::vector<dm_header> h(ncols);
-  cudaError_t e = cudaSuccess;
   for (int c = 0; c < ncols && e == cudaSuccess; ++c)
     e = cudaMemcpyAsync(&h[c], hdrs[c], sizeof(dm_header), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);

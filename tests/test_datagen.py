@@ -59,3 +59,15 @@ def test_cfg5_small_scale_all_new():
     assert np.array_equal(np.sort(c.main_codes), np.arange(c.dict_len, dtype=np.uint32))
     assert not np.isin(c.delta, c.main_dict).any()
     assert np.unique(c.delta).size == c.n_delta
+
+
+def test_torch_twin_matches_numpy_cfg5():
+    import torch
+    from datagen import torch_gen
+    scale = 2.0 ** -14
+    c = g.make_config(5, scale=scale)
+    md, codes, bits, delta = torch_gen.make_cfg5(scale=scale, device="cpu")
+    assert np.array_equal(md.numpy().view(np.uint64), c.main_dict)
+    assert np.array_equal(codes.numpy().view(np.uint32), c.main_codes)
+    assert np.array_equal(delta.numpy().view(np.uint64), c.delta)
+    assert bits == c.main_bits

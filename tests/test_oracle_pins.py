@@ -292,3 +292,13 @@ def test_b16_order_edges():
     r = oracle.merge(col)
     assert [bytes(x) for x in r.merged_dict] == want
     assert want.index(b"\x7f" + b"\x00" * 15) < want.index(b"\x80" + b"\x00" * 15)
+
+
+@pytest.mark.parametrize("key", ["u64", "b16"])
+def test_codes_at_agrees_with_full_merge(key):
+    col = datagen.make_random_case(77, 3000, 500, 700, 0.4, key=key)
+    r = oracle.merge(col, "definitional")
+    V = np.concatenate([col.main_dict[col.main_codes.astype(np.int64)], col.delta])
+    codes, n = oracle.codes_at(col.main_dict, col.delta, V, key_bytes=col.key_bytes)
+    assert n == r.merged_len
+    assert codes.tolist() == oracle.unpack(r.merged_words, V.shape[0], r.merged_bits).tolist()
