@@ -133,10 +133,23 @@ dm_status dm_merge_column_async_ev(const dm_column_in* in, const dm_column_out* 
  * out->delta_dict_len, out->merged_bits; returns the device status. */
 dm_status dm_merge_column(const dm_column_in* in, dm_column_out* out, void* ws, size_t ws_bytes, void* cuda_stream);
 
-/* Merge `ncols` independent columns (a wide table) on one device
- * and stream.  ws[c] / ws_bytes[c] is column c's workspace.  Synchronous. */
+/* Merge `ncols` independent columns (a wide table) on one device.
+ * ws[c] / ws_bytes[c] is column c's workspace.  Columns run concurrently on an
+ * internal stream pool forked from and joined back into `cuda_stream`.
+ * Synchronous: fills every out[c] result field; returns the worst status. */
 dm_status dm_merge_table(int ncols, const dm_column_in* in, dm_column_out* out, void* const* ws,
                          const size_t* ws_bytes, void* cuda_stream);
+/* As dm_merge_table without the host synchronisation: column c's results land
+ * in d_headers[c] (device memory).  Stream-ordered, graph-capturable. */
+dm_status dm_merge_table_async(int ncols, const dm_column_in* in, const dm_column_out* out, void* const* ws,
+                               const size_t* ws_bytes, dm_header* const* d_headers, void* cuda_stream);
+
+/* Steps 1(a), 1(b) and 2(a) only (no M'): U', X_M, X_D, U_D, r and the header.
+ * out->x_main, out->x_delta and out->delta_rank must be non-NULL;
+ * out->merged_codes is ignored.  Used by the row-sharded Step 2 (each device
+ * then runs dm_recompress on its row range).  Stream-ordered. */
+dm_status dm_dictionary_merge_async(const dm_column_in* in, const dm_column_out* out, void* ws, size_t ws_bytes,
+                                    dm_header* d_header, void* cuda_stream);
 
 /* Step 2(b) alone (Eq 11): given translation tables, write
  * M'[i] = x_main[M[i]] for i < n_main and M'[n_main + k] = x_delta[delta_rank[k]]

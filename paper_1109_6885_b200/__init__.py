@@ -93,6 +93,8 @@ def _lib():
             "dm_merge_column": (i32, [P(_In), P(_Out), vp, ctypes.c_size_t, vp]),
             "dm_recompress": (i32, [vp, u64, u32, u64, vp, vp, vp, u64, u32, vp, u64, vp]),
             "dm_merge_table": (i32, [i32, P(_In), P(_Out), P(vp), P(ctypes.c_size_t), vp]),
+            "dm_merge_table_async": (i32, [i32, P(_In), P(_Out), P(vp), P(ctypes.c_size_t), P(vp), vp]),
+            "dm_dictionary_merge_async": (i32, [P(_In), P(_Out), vp, ctypes.c_size_t, vp, vp]),
             "dm_pack_codes": (i32, [vp, u64, u32, vp, vp]),
             "dm_unpack_codes": (i32, [vp, u64, u32, vp, vp]),
             "dm_ctx_create": (vp, [i32]),
@@ -280,6 +282,99 @@ def merge_table(columns: Sequence[tuple], *, stream=None) -> list:
         nw = words(m.n_total, o.merged_bits)
         res.append(MergeResult(m.U[: o.merged_dict_len], m.M[:nw], int(o.merged_bits), int(o.delta_dict_len)))
     return res
+
+
+class TableMerger:
+    """Pre-allocated merge of a wide table's independent columns
+    through ``dm_merge_table_async``: one call launches every column on the
+    library's stream pool; graph-capturable like ColumnMerger."""
+
+    def __init__(self, columns: Sequence[tuple]):
+        self.ms = [ColumnMerger(*c) for c in columns]
+        n = len(self.ms)
+        self.n = n
+        self.ins = (_In * n)(*[m.cin for m in self.ms])
+        self.outs = (_Out * n)(*[m.cout for m in self.ms])
+        self.wss = (ctypes.c_void_p * n)(*[m.ws.data_ptr() for m in self.ms])
+        self.wsb = (ctypes.c_size_t * n)(*[m.ws_bytes for m in self.ms])
+        self.hdrs = (ctypes.c_void_p * n)(*[m.hdr.data_ptr() for m in self.ms])
+        self.graph = None
+
+    def run_async(self, stream=None) -> None:
+        st = _lib().dm_merge_table_async(self.n, self.ins, self.outs, self.wss, self.wsb, self.hdrs,
+                                         _stream_handle(stream))
+        if st != Status.OK:
+            raise DictMergeError(st, "dm_merge_table_async")
+
+    def capture_graph(self):
+        self.run_async()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        with torch.cuda.graph(g, stream=side):
+            self.run_async()
+        torch.cuda.synchronize()
+        self.graph = g
+        return g
+
+    def replay_graph(self) -> None:
+        self.graph.replay()
+
+    def results(self) -> list:
+        return [m.result() for m in self.ms]
+
+    @property
+    def tuples(self) -> int:
+        return sum(m.n_total for m in self.ms)
+
+
+class DictionaryMerger:
+    """Steps 1(a), 1(b), 2(a) only (``dm_dictionary_merge_async``): U', X_M, X_D,
+    U_D, r and the header -- the root's part of the row-sharded merge."""
+
+    def __init__(self, main_dict: torch.Tensor, n_main: int, main_bits: int, delta: torch.Tensor):
+        dev = main_dict.device if main_dict.numel() else delta.device
+        self.cin = _make_in(main_dict, None, n_main, main_bits, delta)
+        self.cin.main_codes = None
+        key = self.cin.key
+        nU = main_dict.shape[0] + delta.shape[0]
+        self.U = _empty_keys(key, nU, dev)
+        self.XM = torch.empty(max(main_dict.shape[0], 1), dtype=torch.int32, device=dev)
+        self.XD = torch.empty(max(delta.shape[0], 1), dtype=torch.int32, device=dev)
+        self.UD = _empty_keys(key, delta.shape[0], dev)
+        self.R = torch.empty(max(delta.shape[0], 1), dtype=torch.int32, device=dev)
+        self.cout = _Out(_ptr(self.U), nU, None, 0, _ptr(self.XM), _ptr(self.XD), _ptr(self.UD), _ptr(self.R),
+                         0, 0, 0)
+        self.ws_bytes = workspace_bytes(self.cin)
+        self.ws = torch.empty(max(self.ws_bytes, 256), dtype=torch.uint8, device=dev)
+        self.hdr = torch.zeros(4, dtype=torch.int64, device=dev)
+        self.inputs = (main_dict, delta)
+
+    def run_async(self, stream=None) -> None:
+        st = _lib().dm_dictionary_merge_async(ctypes.byref(self.cin), ctypes.byref(self.cout), self.ws.data_ptr(),
+                                              self.ws_bytes, self.hdr.data_ptr(), _stream_handle(stream))
+        if st != Status.OK:
+            raise DictMergeError(st, "dm_dictionary_merge_async")
+
+    def header(self) -> _Hdr:
+        raw = self.hdr.cpu().numpy().tobytes()
+        return _Hdr.from_buffer_copy(raw[: ctypes.sizeof(_Hdr)])
+
+
+def recompress(main_codes: torch.Tensor, n_main: int, main_bits: int, dict_len: int, x_main: torch.Tensor,
+               x_delta: torch.Tensor, delta_rank: torch.Tensor, n_delta: int, new_bits: int,
+               stream=None) -> torch.Tensor:
+    """Step 2(b) alone (``dm_recompress``): returns words(n_main + n_delta, new_bits) u64 words."""
+    dev = x_main.device
+    nw = words(n_main + n_delta, new_bits)
+    out = torch.empty(max(nw, 2), dtype=torch.int64, device=dev)
+    st = _lib().dm_recompress(_ptr(main_codes) if n_main else None, n_main, main_bits, dict_len,
+                              _ptr(x_main), _ptr(x_delta) if n_delta else None,
+                              _ptr(delta_rank) if n_delta else None, n_delta, new_bits, out.data_ptr(), out.numel(),
+                              _stream_handle(stream))
+    if st != Status.OK:
+        raise DictMergeError(st, "dm_recompress")
+    return out[:nw]
 
 
 def pack_codes(codes: torch.Tensor, bits: int, stream=None) -> torch.Tensor:

@@ -132,7 +132,7 @@ static dm_status cuda_fail(cudaError_t e) {
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-static dm_status validate(const dm_column_in* in, const dm_column_out* out) {
+static dm_status validate(const dm_column_in* in, const dm_column_out* out, bool with_step2 = true) {
   if (!in || !out) return DM_E_INVALID;
   if (in->key != DM_KEY_U64 && in->key != DM_KEY_B16) return DM_E_INVALID;
   if (in->main_bits < 1 || in->main_bits > 32) return DM_E_INVALID;
@@ -141,23 +141,28 @@ static dm_status validate(const dm_column_in* in, const dm_column_out* out) {
   if (in->n_main > 0 && in->dict_len == 0) return DM_E_INVALID;
   if (in->dict_len > 0 && in->main_bits < host_width(in->dict_len)) return DM_E_INVALID;
   if (in->dict_len && (!in->main_dict || !aligned16(in->main_dict))) return DM_E_INVALID;
-  if (in->n_main && (!in->main_codes || !aligned16(in->main_codes))) return DM_E_INVALID;
+  if (with_step2 && in->n_main && (!in->main_codes || !aligned16(in->main_codes))) return DM_E_INVALID;
   if (in->n_delta && (!in->delta || !aligned16(in->delta))) return DM_E_INVALID;
   const uint64_t dict_cap = in->dict_len + in->n_delta;
   if (dict_cap > (1ull << 32)) return DM_E_TOO_WIDE;  // |U'| <= |U_M| + N_D must stay <= 2^32
   if (dict_cap && (!out->merged_dict || !aligned16(out->merged_dict))) return DM_E_INVALID;
   if (out->merged_dict_cap < dict_cap) return DM_E_CAPACITY;
-  const uint64_t need_words = dm_merged_codes_cap_words(in);
-  if (need_words && (!out->merged_codes || !aligned16(out->merged_codes))) return DM_E_INVALID;
-  if (out->merged_codes_cap_words < need_words) return DM_E_CAPACITY;
+  if (with_step2) {
+    const uint64_t need_words = dm_merged_codes_cap_words(in);
+    if (need_words && (!out->merged_codes || !aligned16(out->merged_codes))) return DM_E_INVALID;
+    if (out->merged_codes_cap_words < need_words) return DM_E_CAPACITY;
+  } else {
+    if (in->dict_len && !out->x_main) return DM_E_INVALID;
+    if (in->n_delta && (!out->x_delta || !out->delta_rank)) return DM_E_INVALID;
+  }
   if (out->delta_dict && !aligned16(out->delta_dict)) return DM_E_INVALID;
   return DM_OK;
 }
 
 static dm_status merge_async(const dm_column_in* in, const dm_column_out* out, void* ws, size_t ws_bytes,
                              dm_header* d_header, cudaStream_t st, bool zero_header,
-                             void* const* events = nullptr) {
-  dm_status v = validate(in, out);
+                             void* const* events = nullptr, bool with_step2 = true) {
+  dm_status v = validate(in, out, with_step2);
   if (v != DM_OK) return v;
   const WsLayout L = ws_layout(in);
   if (!ws || ws_bytes < L.total) return DM_E_CAPACITY;
@@ -181,7 +186,8 @@ static dm_status merge_async(const dm_column_in* in, const dm_column_out* out, v
   if ((e = launch_dictionary_merge(in, out, w, L, udict, xm, xd, d_header, st)) != cudaSuccess) return cuda_fail(e);
   mark(2);
   // Step 2(b): M' (Eq 11).
-  if ((e = launch_recompress(in, out, xm, xd, rank, d_header, st)) != cudaSuccess) return cuda_fail(e);
+  if (with_step2 && (e = launch_recompress(in, out, xm, xd, rank, d_header, st)) != cudaSuccess)
+    return cuda_fail(e);
   mark(3);
   return DM_OK;
 }
@@ -296,28 +302,10 @@ dm_status dm_merge_table(int ncols, const dm_column_in* in, dm_column_out* out, 
     const WsLayout L = ws_layout(&in[c]);
     if (!ws[c] || ws_bytes[c] < L.total) return DM_E_CAPACITY;
     hdrs[c] = reinterpret_cast<dm_header*>(static_cast<char*>(ws[c]) + L.hdr);
-    dm_status v = validate(&in[c], &out[c]);
-    if (v != DM_OK) return v;
   }
-  std::vector<int> order(ncols);
-  for (int c = 0; c < ncols; ++c) order[c] = c;
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
-    return in[a].n_main + in[a].n_delta > in[b].n_main + in[b].n_delta;
-  });
-  StreamPool& pool = stream_pool();
-  const int K = std::max(1, std::min<int>(ncols, (int)pool.streams.size()));
-  cudaError_t e = cudaEventRecord(pool.fork, st);
-  for (int k = 0; k < K && e == cudaSuccess; ++k) e = cudaStreamWaitEvent(pool.streams[k], pool.fork, 0);
-  if (e != cudaSuccess) return cuda_fail(e);
-  for (int t = 0; t < ncols; ++t) {
-    const int c = order[t];
-    dm_status s = merge_async(&in[c], &out[c], ws[c], ws_bytes[c], hdrs[c], pool.streams[t % K], false);
-    if (s != DM_OK) return s;
-  }
-  for (int k = 0; k < K && e == cudaSuccess; ++k) {
-    e = cudaEventRecord(pool.join[k], pool.streams[k]);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, pool.join[k], 0);
-  }
+  dm_status s0 = dm_merge_table_async(ncols, in, out, ws, ws_bytes, hdrs.data(), cuda_stream);
+  if (s0 != DM_OK) return s0;
+  cudaError_t e = cudaSuccess;
   std::vector<dm_header> h(ncols);
   for (int c = 0; c < ncols && e == cudaSuccess; ++c)
     e = cudaMemcpyAsync(&h[c], hdrs[c], sizeof(dm_header), cudaMemcpyDeviceToHost, st);
@@ -331,6 +319,42 @@ dm_status dm_merge_table(int ncols, const dm_column_in* in, dm_column_out* out, 
     status = std::min(status, (int)h[c].status);
   }
   return (dm_status)status;
+}
+
+dm_status dm_merge_table_async(int ncols, const dm_column_in* in, const dm_column_out* out, void* const* ws,
+                               const size_t* ws_bytes, dm_header* const* hdrs, void* cuda_stream) {
+  if (ncols < 0 || (ncols > 0 && (!in || !out || !ws || !ws_bytes || !hdrs))) return DM_E_INVALID;
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  for (int c = 0; c < ncols; ++c) {
+    dm_status v = validate(&in[c], &out[c]);
+    if (v != DM_OK) return v;
+    if (!ws[c] || ws_bytes[c] < ws_layout(&in[c]).total) return DM_E_CAPACITY;
+  }
+  std::vector<int> order(ncols);
+  for (int c = 0; c < ncols; ++c) order[c] = c;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+    return in[a].n_main + in[a].n_delta > in[b].n_main + in[b].n_delta;
+  });
+  StreamPool& pool = stream_pool();
+  const int K = std::max(1, std::min<int>(ncols, (int)pool.streams.size()));
+  cudaError_t e = cudaEventRecord(pool.fork, st);
+  for (int k = 0; k < K && e == cudaSuccess; ++k) e = cudaStreamWaitEvent(pool.streams[k], pool.fork, 0);
+  if (e != cudaSuccess) return cuda_fail(e);
+  for (int t = 0; t < ncols; ++t) {
+    const int c = order[t];
+    dm_status s = merge_async(&in[c], &out[c], ws[c], ws_bytes[c], hdrs[c], pool.streams[t % K], true);
+    if (s != DM_OK) return s;
+  }
+  for (int k = 0; k < K && e == cudaSuccess; ++k) {
+    e = cudaEventRecord(pool.join[k], pool.streams[k]);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, pool.join[k], 0);
+  }
+  return e == cudaSuccess ? DM_OK : cuda_fail(e);
+}
+
+dm_status dm_dictionary_merge_async(const dm_column_in* in, const dm_column_out* out, void* ws, size_t ws_bytes,
+                                    dm_header* d_header, void* cuda_stream) {
+  return merge_async(in, out, ws, ws_bytes, d_header, static_cast<cudaStream_t>(cuda_stream), true, nullptr, false);
 }
 
 dm_status dm_recompress(const uint64_t* main_codes, uint64_t n_main, uint32_t main_bits, uint64_t dict_len,

@@ -209,6 +209,31 @@ def test_host_entry_point():
     ctx.close()
 
 
+def test_row_sharded_step2_on_one_device():
+    """The row-sharded path with G logical shards on one GPU: root
+    Steps 1(a)/1(b)/2(a) via dm_dictionary_merge_async, then dm_recompress on each
+    4096-row-aligned shard; the shards concatenate to the unsharded M'."""
+    import paper_1109_6885_b200 as dm
+    from paper_1109_6885_b200 import sharding
+    col = datagen.make_random_case(41, 1 << 20, 1 << 16, 50001, 0.7, main_bits=18)
+    UM, M, D = to_device(col)
+    ref = oracle.merge(col)
+    dmg = dm.DictionaryMerger(UM, col.n_main, col.main_bits, D)
+    dmg.run_async()
+    h = dmg.header()
+    assert h.status == 0 and h.merged_bits == ref.merged_bits and h.merged_dict_len == ref.merged_len
+    assert np.array_equal(keys_np(dmg.U[: h.merged_dict_len], "u64"), ref.merged_dict)
+    for g in (1, 2, 3, 8):
+        parts = []
+        for s in sharding.plan_row_shards(col.n_main, col.n_delta, g):
+            mslice = M[s.in_word(col.main_bits):] if s.n_main else M
+            parts.append(dm.recompress(mslice, s.n_main, col.main_bits, col.dict_len, dmg.XM, dmg.XD,
+                                       dmg.R[s.delta_begin:], s.n_delta, h.merged_bits))
+        got = torch.cat(parts).cpu().numpy().view(np.uint64)
+        # each shard's last word is complete except the final shard's
+        assert np.array_equal(got, ref.merged_words), g
+
+
 def test_merge_table_matches_per_column():
     import paper_1109_6885_b200 as dm
     cols = [datagen.make_config(4, scale=0.002, column=j) for j in (0, 7, 100, 239, 240, 299)]
