@@ -1,18 +1,19 @@
 #!/usr/bin/env python
 """bench.py -- merged tuples/s of the online dictionary merge on B200 (arXiv 1109.6885).
 
-One "step" = one whole merge of one column (Steps 1(a), 1(b), 2(a), 2(b)) on the
-BASELINE.json workload configs[1] ("cfg2": N_M = 1e8 rows at 24 bits over a
-1e7-entry u64 dictionary, N_D = 1e6 delta tuples, 10% new), synthetic seeded
-inputs (datagen), resident in HBM when the timed region starts.
+One "step" = one whole merge (Steps 1(a), 1(b), 2(a), 2(b)) of the workload's
+column(s), synthetic seeded inputs (datagen) resident in HBM when the timed
+region starts, L2 flushed (512 MB write) before every timed step.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload cfg2|cfg1|cfg3|cfg4|cfg5]
 
-N > 1 (torchrun, one rank per GPU): each rank merges its own column (whole
-columns are independent units) -- no collective on the data path,
-weak scaling; the step time is the max over ranks.
-
-Prints ONE JSON line (rank 0).  Keys: see DESIGN.md "Measurement".
+Default workload: BASELINE.json configs[1] ("cfg2": N_M = 1e8 rows at 24 bits over
+a 1e7-entry u64 dictionary, N_D = 1e6, 10% new) -- the config the metric is quoted
+on.  N > 1 (torchrun, one rank per GPU): whole columns are independent units
+(P:184), so each rank merges its own column (cfg1/2/3/5) or its LPT share of
+the 300 columns (cfg4): no collective on the data path, weak scaling, step time =
+max over ranks.  Prints ONE JSON line (rank 0).  Keys: DESIGN.md "Measurement".
 """
 from __future__ import annotations
 
@@ -32,8 +33,14 @@ sys.path.insert(0, ROOT)
 
 import datagen  # noqa: E402
 
-CFG = 2
-WORKLOAD = "cfg2: single u64 column, N_M=1e8 @24b over |U_M|=1e7 (uniform in [0,2^48), uniform codes), N_D=1e6 (90% reuse / 10% new)"
+WORKLOADS = {
+    "cfg1": "cfg1: single u64 column, N_M=1e6 @14b over |U_M|=1e4 in [0,2^40), N_D=1e4 (50% new)",
+    "cfg2": "cfg2: single u64 column, N_M=1e8 @24b over |U_M|=1e7 (uniform in [0,2^48), uniform codes), "
+            "N_D=1e6 (90% reuse / 10% new)",
+    "cfg3": "cfg3: single 16-byte string column, N_M=1e8 @20b over |U_M|=1e6 (Zipf(1) codes), N_D=5e6 (20% new)",
+    "cfg4": "cfg4: 300-column table, N_M=1e7 + N_D=1e5 per column, card log-uniform [2,1e7], 240 u64 + 60 strings",
+    "cfg5": "cfg5: single u64 column, N_M=|U_M|=2^30 @30b (all unique), N_D=5e7 all new -> 31 bits (reading A12)",
+}
 METRIC = "merged tuples/sec per column (N_M+N_D)"
 UNIT = "tuples/s"
 
@@ -45,14 +52,16 @@ def peaks():
         return None
 
 
-def algorithmic_bytes(col, merged_len, merged_bits, delta_dict_len):
-    """Per-kernel and whole-merge minimum bytes."""
-    E = col.key_bytes
-    nM, nD, nU = col.n_main, col.n_delta, col.dict_len
-    npr = nM + nD
-    step2 = nM * col.main_bits / 8 + npr * merged_bits / 8 + 4 * nU + 4 * nD + 4 * delta_dict_len
-    strict = nM * col.main_bits / 8 + nD * E + nU * E + merged_len * E + npr * merged_bits / 8
-    return step2, strict
+def strict_bytes(n_main, main_bits, n_delta, key_bytes, dict_len, merged_len, merged_bits):
+    """SURVEY §8d minimum: each input read once, each output written once."""
+    return (n_main * main_bits / 8 + n_delta * key_bytes + dict_len * key_bytes + merged_len * key_bytes
+            + (n_main + n_delta) * merged_bits / 8)
+
+
+def step2_bytes(n_main, main_bits, n_delta, dict_len, merged_bits, delta_dict_len):
+    """Step 2(b) algorithmic bytes per launch."""
+    return (n_main * main_bits / 8 + (n_main + n_delta) * merged_bits / 8 + 4 * dict_len + 4 * n_delta
+            + 4 * delta_dict_len)
 
 
 class ClockSampler:
@@ -111,49 +120,106 @@ def host_info():
     return cpu, os.cpu_count()
 
 
-def run_oracle_steps(col, steps):
-    """The oracle as it stands (linear mode, 1 thread) on the full column."""
+# ------------------------------------------------------------------------ inputs
+def cfg_number(workload: str) -> int:
+    return int(workload[3:])
+
+
+def host_columns(workload: str, rank: int, world: int):
+    """The datagen columns this rank merges (host arrays)."""
+    cfg = cfg_number(workload)
+    if cfg == 4:
+        from paper_1109_6885_b200.sharding import column_cost, lpt_partition
+        costs = []
+        for j in range(300):
+            _, card, key, _ = datagen.cfg4_column_params(j)
+            costs.append(column_cost(10**7, 10**5, card, datagen.width_hint(card), 8 if key == "u64" else 16))
+        mine = lpt_partition(costs, world)[rank]
+        return [datagen.make_config(4, column=j) for j in mine]
+    return [datagen.make_config(cfg, seed=datagen.BASE_SEED + 7 * rank)]
+
+
+def device_inputs(col, dev):
+    import torch
+    import paper_1109_6885_b200 as dm
+    if col.key == "u64":
+        UM = torch.from_numpy(col.main_dict.view(np.int64)).to(dev)
+        D = torch.from_numpy(col.delta.view(np.int64)).to(dev)
+    else:
+        UM = torch.from_numpy(np.ascontiguousarray(col.main_dict)).to(dev)
+        D = torch.from_numpy(np.ascontiguousarray(col.delta)).to(dev)
+    codes = torch.from_numpy(col.main_codes.view(np.int32)).to(dev)
+    M = dm.pack_codes(codes, col.main_bits)
+    return UM, M, col.n_main, col.main_bits, D
+
+
+def cfg5_device_inputs(dev, rank):
+    import paper_1109_6885_b200 as dm
+    from datagen import torch_gen
+    UM, codes, bits, D = torch_gen.make_cfg5(seed=datagen.BASE_SEED + 7 * rank, device=dev)
+    M = dm.pack_codes(codes, bits)
+    del codes
+    return UM, M, UM.numel(), bits, D
+
+
+# ----------------------------------------------------------------- oracle legs
+def oracle_sample(workload: str):
+    """A bounded sample of the workload for the CPU oracle (≈10-30 s of work)."""
+    cfg = cfg_number(workload)
+    if cfg == 4:
+        return [datagen.make_config(4, column=j) for j in (0, 60, 120, 180, 239, 240, 270, 299)], \
+            "8 of the 300 cfg4 columns at full size (0,60,120,180,239 u64; 240,270,299 strings)"
+    if cfg == 5:
+        return [datagen.make_config(5, scale=1 / 16)], "cfg5 at 1/16 scale (2^26 main rows, 3.1e6 delta)"
+    col = datagen.make_config(cfg)
+    return [col], f"the full {workload} column (N'={col.n_main + col.n_delta})"
+
+
+def run_oracle(cols, reps):
     import oracle
     oracle.build()
-    W = oracle.pack(col.main_codes, col.main_bits)
+    packed = [oracle.pack(c.main_codes, c.main_bits) for c in cols]
+    tuples = sum(c.n_main + c.n_delta for c in cols)
     times = []
-    for _ in range(steps):
+    for _ in range(reps):
         t0 = time.perf_counter()
-        r = oracle.merge(col, "linear", main_words=W)
+        for c, W in zip(cols, packed):
+            r = oracle.merge(c, "linear", main_words=W)
+            assert r.status == 0
         times.append(time.perf_counter() - t0)
-        assert r.status == 0
-    return times
+    return tuples, times
 
 
 def reference_arm(args, rank, world):
     if rank != 0:
         return 0
-    col = datagen.make_config(CFG)
-    n = col.n_main + col.n_delta
-    run_oracle_steps(col, args.warmup)
-    times = run_oracle_steps(col, args.steps)
+    cols, sample = oracle_sample(args.workload)
+    tuples, _ = run_oracle(cols, max(args.warmup, 0)) if args.warmup else (None, None)
+    tuples, times = run_oracle(cols, args.steps)
     t = sum(times) / len(times)
     cpu, ncpu = host_info()
-    v = n / t
+    v = tuples / t
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u64", "data": "synthetic (datagen, seeded)",
-        "config": {"workload": WORKLOAD, "seed": datagen.config_seed(CFG)},
+        "vs_baseline": None, "dtype": "u64" if cfg_number(args.workload) != 3 else "u8x16",
+        "data": "synthetic (datagen, seeded)", "config": {"workload": WORKLOADS[args.workload]},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": f"full cfg2 column per step ({n} tuples), oracle linear mode, 1 thread, {cpu}"},
+                         "sample": f"{sample}; oracle linear mode, 1 thread of {ncpu} ({cpu})"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
+# ------------------------------------------------------------------------- main
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -176,38 +242,50 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
         pg = dist
 
-    # ---- inputs (per rank: its own column; rank 0 = the seeded cfg2 column)
-    col = datagen.make_config(CFG, seed=datagen.BASE_SEED + 7 * rank)
-    UM = torch.from_numpy(col.main_dict.view(np.int64)).to(dev)
-    D = torch.from_numpy(col.delta.view(np.int64)).to(dev)
-    codes = torch.from_numpy(col.main_codes.view(np.int32)).to(dev)
-    M = dm.pack_codes(codes, col.main_bits)
-    del codes
-    merger = dm.ColumnMerger(UM, M, col.n_main, col.main_bits, D)
+    cfg = cfg_number(args.workload)
+    table = cfg == 4
+    # ---- inputs, resident in HBM
+    if cfg == 5:
+        cols = None
+        dev_cols = [cfg5_device_inputs(dev, rank)]
+    else:
+        cols = host_columns(args.workload, rank, world)
+        dev_cols = [device_inputs(c, dev) for c in cols]
+    if table:
+        merger = dm.TableMerger(dev_cols)
+        n_tuples = merger.tuples
+    else:
+        merger = dm.ColumnMerger(*dev_cols[0])
+        n_tuples = merger.n_total
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 2x the 126 MB L2
-    stream = torch.cuda.current_stream()
 
     for _ in range(max(args.warmup, 0)):
         merger.run_async()
     torch.cuda.synchronize()
-    r0 = merger.result()
 
-    # ---- per-step breakdown (eager launches, events at the step boundaries)
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
-    for row in ev:  # torch creates the CUDA event lazily on first record
-        for e in row:
-            e.record()
-    torch.cuda.synchronize()
+    # ---- per-step breakdown (single column: eager launches, events at the step boundaries)
+    s1a = s1b = s2 = eager_ms = None
     launches0 = dm.launch_count()
-    for k in range(args.steps):
-        flush.zero_()
-        merger.run_async_timed(ev[k])
-    torch.cuda.synchronize()
+    if not table:
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+        for row in ev:  # torch creates the CUDA event lazily on first record
+            for e in row:
+                e.record()
+        torch.cuda.synchronize()
+        launches0 = dm.launch_count()
+        for k in range(args.steps):
+            flush.zero_()
+            merger.run_async_timed(ev[k])
+        torch.cuda.synchronize()
+        s1a = [ev[k][0].elapsed_time(ev[k][1]) for k in range(args.steps)]
+        s1b = [ev[k][1].elapsed_time(ev[k][2]) for k in range(args.steps)]
+        s2 = [ev[k][2].elapsed_time(ev[k][3]) for k in range(args.steps)]
+        eager_ms = [ev[k][0].elapsed_time(ev[k][3]) for k in range(args.steps)]
+    else:
+        for k in range(args.steps):
+            merger.run_async()
+        torch.cuda.synchronize()
     launches_per_merge = (dm.launch_count() - launches0) / max(args.steps, 1)
-    s1a = [ev[k][0].elapsed_time(ev[k][1]) for k in range(args.steps)]
-    s1b = [ev[k][1].elapsed_time(ev[k][2]) for k in range(args.steps)]
-    s2 = [ev[k][2].elapsed_time(ev[k][3]) for k in range(args.steps)]
-    eager_ms = [ev[k][0].elapsed_time(ev[k][3]) for k in range(args.steps)]
 
     # ---- timed region: K whole merges replayed from a CUDA graph (one driver call
     # each), L2 flushed before each, CUDA events around each merge on its stream
@@ -226,94 +304,117 @@ def main():
             merger.replay_graph()
             gev[k][1].record()
         torch.cuda.synchronize()
-    launches = int(round(launches_per_merge * args.steps))
     if pg:
         pg.barrier()
     step_ms = [a.elapsed_time(b) for a, b in gev]
     total_ms = sum(step_ms)
+    tot = torch.tensor([total_ms, float(n_tuples)], dtype=torch.float64, device=dev)
     if pg:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        t = tot[:1].clone()
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
-        total_ms = float(t.item())
+        n_all = tot[1:].clone()
+        pg.all_reduce(n_all, op=pg.ReduceOp.SUM)
+        total_ms, all_tuples = float(t.item()), float(n_all.item())
+    else:
+        all_tuples = float(n_tuples)
     ms_per_step = total_ms / args.steps
-    n_tuples = col.n_main + col.n_delta
-    value = world * n_tuples / (ms_per_step / 1e3)
+    value = all_tuples / (ms_per_step / 1e3)
 
-    res = merger.result()
-    step2_bytes, strict_bytes = algorithmic_bytes(col, res.merged_len, res.merged_bits, res.delta_dict_len)
+    # ---- roofline of the dominant kernel (Step 2(b), k_recompress)
     pk = peaks()
     peak_hbm = pk["hbm_gbs"] if pk else 6650.0
-    s2_ms = statistics.mean(s2)
-    achieved = step2_bytes / (s2_ms / 1e3) / 1e9
+    results = merger.results() if table else [merger.result()]
+    key_bytes = [(UM.shape[1] if UM.dim() == 2 else 8) for (UM, _, _, _, _) in dev_cols]
+    sb = sum(strict_bytes(n_m, b, D.shape[0], kb, UM.shape[0], r.merged_len, r.merged_bits)
+             for (UM, _, n_m, b, D), kb, r in zip(dev_cols, key_bytes, results))
+    s2b = sum(step2_bytes(n_m, b, D.shape[0], UM.shape[0], r.merged_bits, r.delta_dict_len)
+              for (UM, _, n_m, b, D), r in zip(dev_cols, results))
     traffic = None
     tp = os.path.join(ROOT, "profiles", "recompress_traffic.json")
-    if os.path.exists(tp):
+    if os.path.exists(tp) and not table:
         try:
-            traffic = json.load(open(tp)).get("traffic_bytes_per_launch")
+            traffic = json.load(open(tp)).get(args.workload, {}).get("traffic_bytes_per_launch")
         except Exception:
             traffic = None
+    if not table:
+        s2_ms = statistics.mean(s2)
+        achieved = s2b / (s2_ms / 1e3) / 1e9
+        roofline = {"kernel": "k_recompress (Step 2(b))", "bound": "hbm", "achieved": achieved,
+                    "peak": peak_hbm, "unit": "GB/s", "frac": achieved / peak_hbm, "traffic": traffic,
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if pk else "fallback 6.65 TB/s",
+                    "algorithmic_bytes_per_launch": s2b,
+                    "gather_bound_note": "X_M lookups: measured L2 random-gather ceiling 2.8e11/s "
+                                         "(profiles/r01/microbench_gather.jsonl)"}
+    else:
+        achieved = sb / (ms_per_step / 1e3) / 1e9
+        roofline = {"kernel": "whole table merge (all kernels, 300 columns)", "bound": "hbm", "achieved": achieved,
+                    "peak": peak_hbm, "unit": "GB/s", "frac": achieved / peak_hbm, "traffic": None,
+                    "algorithmic_bytes_per_launch": sb}
 
     # ---- e2e through the public host-buffer API (H2D inputs + D2H results inside)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not table:
+        UM, M, n_m, b, D = dev_cols[0]
         ctx = dm.HostContext(local)
-        hUM = torch.from_numpy(col.main_dict.view(np.int64)).pin_memory()
-        hD = torch.from_numpy(col.delta.view(np.int64)).pin_memory()
-        hM = M.cpu().pin_memory()
-        hU = torch.empty(col.dict_len + col.n_delta, dtype=torch.int64).pin_memory()
+        hUM, hD, hM = UM.cpu().pin_memory(), D.cpu().pin_memory(), M.cpu().pin_memory()
+        kb = key_bytes[0]
+        hU = (torch.empty(UM.shape[0] + D.shape[0], dtype=torch.int64) if kb == 8 else
+              torch.empty((UM.shape[0] + D.shape[0], 16), dtype=torch.uint8)).pin_memory()
         hMo = torch.empty(dm.words(n_tuples, 32), dtype=torch.int64).pin_memory()
-        ctx.merge(hUM, hM, col.n_main, col.main_bits, hD, hU, hMo)  # warm-up (allocations)
+        ctx.merge(hUM, hM, n_m, b, hD, hU, hMo)  # warm-up (allocations)
         if pg:
             pg.barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            nU, nb, _ = ctx.merge(hUM, hM, col.n_main, col.main_bits, hD, hU, hMo)
+            nU, nb, _ = ctx.merge(hUM, hM, n_m, b, hD, hU, hMo)
         e2e_s = (time.perf_counter() - t0) / args.e2e_steps
         if pg:
             t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
             pg.all_reduce(t, op=pg.ReduceOp.MAX)
             e2e_s = float(t.item())
-        h2d = hUM.numel() * 8 + hD.numel() * 8 + hM.numel() * 8
-        d2h = nU * 8 + dm.words(n_tuples, nb) * 8
-        e2e = {"value": world * n_tuples / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_s * 1e3}
+        h2d = hUM.numel() * hUM.element_size() + hD.numel() * hD.element_size() + hM.numel() * 8
+        d2h = nU * kb + dm.words(n_tuples, nb) * 8
+        e2e = {"value": all_tuples / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_s * 1e3,
+               "path": "dm_merge_column_host (pinned host buffers, copies inside the timed call)"}
         ctx.close()
 
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        times = run_oracle_steps(col, 2)
+        ocols, sample = oracle_sample(args.workload)
+        tuples, times = run_oracle(ocols, 1 if cfg in (4, 5) else 2)
         cpu, ncpu = host_info()
-        t = min(times)
-        cpu_baseline = {"value": n_tuples / t, "unit": UNIT, "cores": 1, "kind": "oracle",
-                        "sample": f"the full cfg2 column (N'={n_tuples}), oracle linear mode, best of 2, "
-                                  f"1 thread of {ncpu} ({cpu})"}
+        cpu_baseline = {"value": tuples / min(times), "unit": UNIT, "cores": 1, "kind": "oracle",
+                        "sample": f"{sample}; oracle linear mode, best of {len(times)}, 1 thread of {ncpu} ({cpu})"}
 
     if rank == 0:
+        r0 = results[0]
+        cfgd = {"workload": WORKLOADS[args.workload], "columns_per_rank": len(dev_cols),
+                "parallelism": f"column-sharded x{world} (independent columns, no collective)",
+                "l2": "flushed (512 MB write) before every timed step",
+                "timing": "CUDA-graph replay of the whole merge, CUDA events on the launching stream"}
+        if not table:
+            UM, M, n_m, b, D = dev_cols[0]
+            cfgd.update({"n_main": n_m, "n_delta": int(D.shape[0]), "dict_len": int(UM.shape[0]), "main_bits": b,
+                         "merged_len": r0.merged_len, "merged_bits": r0.merged_bits})
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": METRIC if not table else "merged column-tuples/sec (sum over columns of N_M+N_D)",
+            "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u64", "data": "synthetic (datagen, seeded; BASELINE configs[1])",
-            "config": {"workload": WORKLOAD, "seed": datagen.config_seed(CFG), "n_main": col.n_main,
-                       "n_delta": col.n_delta, "dict_len": col.dict_len, "main_bits": col.main_bits,
-                       "merged_len": res.merged_len, "merged_bits": res.merged_bits,
-                       "parallelism": f"column-sharded x{world} (independent columns, no collective)",
-                       "l2": "flushed (512 MB write) before every timed step"},
-            "steps_ms": {"s1a_delta_dict": statistics.mean(s1a), "s1b_dict_merge": statistics.mean(s1b),
-                         "s2b_recompress": s2_ms, "eager_total": statistics.mean(eager_ms),
-                         "graph_total": statistics.mean(step_ms),
-                         "note": "s1a/s1b/s2b from eager launches with events between steps; "
-                                 "value/ms_per_step from CUDA-graph replays"},
-            "hbm_fraction_strict": strict_bytes / (statistics.mean(step_ms) / 1e3) / 1e9 / peak_hbm,
-            "roofline": {"kernel": "k_recompress (Step 2(b))", "bound": "hbm", "achieved": achieved,
-                         "peak": peak_hbm, "unit": "GB/s", "frac": achieved / peak_hbm, "traffic": traffic,
-                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if pk else "fallback 6.65 TB/s",
-                         "algorithmic_bytes_per_launch": step2_bytes},
-            "cpu_baseline": cpu_baseline,
-            "e2e": e2e,
-            "gpu_launches": launches,
-            "gpu_launches_per_step": launches / max(args.steps, 1),
+            "vs_baseline": None, "dtype": "u64" if cfg != 3 else "u8x16",
+            "data": f"synthetic (datagen, seeded; BASELINE configs[{cfg - 1}])", "config": cfgd,
+            "hbm_fraction_strict": sb / (ms_per_step / 1e3) / 1e9 / peak_hbm,
+            "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e,
+            "gpu_launches": int(round(launches_per_merge * args.steps)),
+            "gpu_launches_per_step": launches_per_merge,
             "clocks": clk.summary(),
         }
+        if not table:
+            line["steps_ms"] = {"s1a_delta_dict": statistics.mean(s1a), "s1b_dict_merge": statistics.mean(s1b),
+                                "s2b_recompress": statistics.mean(s2), "eager_total": statistics.mean(eager_ms),
+                                "graph_total": ms_per_step,
+                                "note": "s1a/s1b/s2b from eager launches with events between steps; "
+                                        "value/ms_per_step from CUDA-graph replays"}
         print(json.dumps(line), flush=True)
     if pg:
         pg.barrier()

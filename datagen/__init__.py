@@ -289,6 +289,16 @@ def _scaled(n: int, scale: float, lo: int = 1) -> int:
     return max(lo, int(round(n * scale)))
 
 
+def cfg4_column_params(j: int, seed: Optional[int] = None):
+    """cfg4 column j: (column seed, cardinality log-uniform on [2, 1e7], key type, new-value
+    fraction: 1% below 2^16 distinct values else 10%, reading A13)."""
+    s = config_seed(4, BASE_SEED if seed is None else seed)
+    sj = int(mix64(np.uint64(s + 4000 + j)))
+    u = float(uniform01(sj, 5, 0))
+    card = max(2, int(round(math.exp(math.log(2) + u * (math.log(10**7) - math.log(2))))))
+    return sj, card, ("u64" if j < 240 else "b16"), (0.01 if card < (1 << 16) else 0.10)
+
+
 def make_config(cfg: int, seed: Optional[int] = None, scale: float = 1.0, column: Optional[int] = None):
     """Inputs for BASELINE.json configs[cfg-1] (cfg in 1..5).
 
@@ -310,11 +320,8 @@ def make_config(cfg: int, seed: Optional[int] = None, scale: float = 1.0, column
         cols = []
         rng_cols = range(300) if column is None else [column]
         for j in rng_cols:
-            sj = int(mix64(np.uint64(s + 4000 + j)))
-            u = float(uniform01(sj, 5, 0))
-            card = max(2, int(round(math.exp(math.log(2) + u * (math.log(10**7) - math.log(2))))))
+            sj, card, key, p_new = cfg4_column_params(j, seed)
             card = _scaled(card, scale, 2) if scale != 1.0 else card
-            p_new = 0.01 if card < (1 << 16) else 0.10
             n_m, n_d = _scaled(10**7, scale), _scaled(10**5, scale)
             if j < 240:
                 c = _u64_column(sj, n_m, card, n_d, p_new, 64, name=f"cfg4.col{j}")

@@ -25,10 +25,12 @@ extern "C" int dm_debug_trace(unsigned long long* host) {
   return (int)cudaMemcpyFromSymbol(host, dm_trace_buf, sizeof(dm_trace_buf));
 }
 __device__ __forceinline__ void dm_trace(int slot) {
-  if (threadIdx.x == 0 && blockIdx.x < 8) {
+  // blocks 0, S, 2S, ... (S = gridDim/8 rounded up): first wave and steady state
+  const unsigned stride = (gridDim.x + 7) / 8;
+  if (threadIdx.x == 0 && blockIdx.x % stride == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    dm_trace_buf[blockIdx.x * 32 + slot] = t;
+    dm_trace_buf[(blockIdx.x / stride) * 32 + slot] = t;
   }
 }
 #define DM_T(slot) dm_trace(slot)
@@ -103,13 +105,12 @@ __global__ void __launch_bounds__(256) k_hist(const void* __restrict__ D, uint64
 
 // One stable LSD radix pass over (key, original-index) pairs.  NT threads,
 // ITEMS keys per thread, tile = NT * ITEMS keys in (warp, item, lane) order.
-template <class KT, int ITEMS>
-__global__ void __launch_bounds__(kSortThreads) k_onesweep(const void* __restrict__ D, void* kbuf0, void* kbuf1,
-                                                          uint32_t* vbuf0, uint32_t* vbuf1, uint64_t n, int pass,
-                                                          const SortPlan* __restrict__ plan, uint32_t* status,
-                                                          uint32_t* counter) {
+template <class KT, int NT, int ITEMS>
+__global__ void __launch_bounds__(NT) k_onesweep(const void* __restrict__ D, void* kbuf0, void* kbuf1,
+                                                uint32_t* vbuf0, uint32_t* vbuf1, uint64_t n, int pass,
+                                                const SortPlan* __restrict__ plan, uint32_t* status,
+                                                uint32_t* counter) {
   using K = typename KT::K;
-  constexpr int NT = kSortThreads;
   constexpr int W = NT / 32;
   constexpr int TILE = NT * ITEMS;
   DM_T(0);
@@ -159,18 +160,29 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const void* __restric
   }
   DM_T(3);
   // Stable warp-level multisplit: ranks in (warp, item, lane) order = input order.
+  // Peers (lanes with the same digit) from 8 bit-plane ballots -- far cheaper
+  // than match.any, which measured as the pass's throughput limiter -- then a
+  // short per-item chain: every lane reads its digit's running count, the
+  // digit's leader adds the item's population.
   const unsigned lt = lanemask_lt();
+  unsigned peers[ITEMS];
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
-    const unsigned peers = __match_any_sync(FULL, dig[i]);
-    const unsigned leader = __ffs(peers) - 1;
-    uint32_t old = 0;
-    if (lane == leader) {
-      old = s_whist[w][dig[i]];
-      s_whist[w][dig[i]] = old + __popc(peers);
+    unsigned p = __ballot_sync(FULL, dig[i] < 256);  // valid lanes only
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      const unsigned bit = (dig[i] >> b) & 1u;
+      const unsigned v = __ballot_sync(FULL, bit);
+      p &= bit ? v : ~v;
     }
-    old = __shfl_sync(FULL, old, leader);
-    rnk[i] = old + __popc(peers & lt);
+    peers[i] = dig[i] < 256 ? p : (1u << lane);  // invalid lanes: private bucket 256
+  }
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const uint32_t old = s_whist[w][dig[i]];
+    const unsigned below = peers[i] & lt;
+    if (below == 0) s_whist[w][dig[i]] = old + __popc(peers[i]);  // the leader (lowest lane)
+    rnk[i] = old + __popc(below);
     __syncwarp();
   }
   __syncthreads();
@@ -330,7 +342,25 @@ __global__ void __launch_bounds__(kUniqThreads) k_unique(const void* __restrict_
   }
 }
 
-template <class KT, int ITEMS>
+template <class KT, int NT, int ITEMS>
+void launch_passes(const dm_column_in* in, char* ws, const WsLayout& L, SortPlan* plan, uint32_t* counters,
+                   cudaStream_t st) {
+  using K = typename KT::K;
+  const uint64_t n = in->n_delta;
+  constexpr int TILE = NT * ITEMS;
+  const size_t dsmem = (sizeof(K) + sizeof(uint32_t)) * TILE;
+  ensure_smem((const void*)k_onesweep<KT, NT, ITEMS>);
+  const uint64_t ntiles = (n + TILE - 1) / TILE;
+  for (int p = 0; p < KT::kPasses; ++p) {
+    uint32_t* status = reinterpret_cast<uint32_t*>(ws + L.status_sort) + (uint64_t)p * ntiles * 256;
+    k_onesweep<KT, NT, ITEMS><<<(unsigned)ntiles, NT, dsmem, st>>>(
+        in->delta, ws + L.keys0, ws + L.keys1, reinterpret_cast<uint32_t*>(ws + L.vals0),
+        reinterpret_cast<uint32_t*>(ws + L.vals1), n, p, plan, status, counters + CNT_SORT + p);
+    note_launch();
+  }
+}
+
+template <class KT>
 cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, void* udict, uint32_t* rank, dm_header* hdr,
                 cudaStream_t st) {
   const uint64_t n = in->n_delta;
@@ -340,17 +370,12 @@ cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, void* udict
   const int hist_blocks = (int)std::min<uint64_t>((n + 4095) / 4096, 148 * 4);
   k_hist<KT><<<hist_blocks, 256, 0, st>>>(in->delta, n, hist, counters + CNT_HIST, plan);
   note_launch();
-  using K = typename KT::K;
-  constexpr int TILE = kSortThreads * ITEMS;
-  const size_t dsmem = (sizeof(K) + sizeof(uint32_t)) * TILE;
-  ensure_smem((const void*)k_onesweep<KT, ITEMS>);
-  const uint64_t ntiles = (n + TILE - 1) / TILE;
-  for (int p = 0; p < KT::kPasses; ++p) {
-    uint32_t* status = reinterpret_cast<uint32_t*>(ws + L.status_sort) + (uint64_t)p * ntiles * 256;
-    k_onesweep<KT, ITEMS><<<(unsigned)ntiles, kSortThreads, dsmem, st>>>(
-        in->delta, ws + L.keys0, ws + L.keys1, reinterpret_cast<uint32_t*>(ws + L.vals0),
-        reinterpret_cast<uint32_t*>(ws + L.vals1), n, p, plan, status, counters + CNT_SORT + p);
-    note_launch();
+  constexpr bool U64 = KT::kBytes == 8;
+  switch (sort_variant()) {  // must match sort_tile_keys() (workspace layout)
+    case 1: launch_passes<KT, 256, U64 ? 16 : 8>(in, ws, L, plan, counters, st); break;
+    case 2: launch_passes<KT, 256, U64 ? 8 : 4>(in, ws, L, plan, counters, st); break;
+    case 3: launch_passes<KT, 1024, U64 ? 8 : 4>(in, ws, L, plan, counters, st); break;
+    default: launch_passes<KT, 512, U64 ? 16 : 8>(in, ws, L, plan, counters, st); break;
   }
   const uint64_t utiles = (n + kUniqThreads * kUniqItems - 1) / (kUniqThreads * kUniqItems);
   k_unique<KT><<<(unsigned)utiles, kUniqThreads, 0, st>>>(
@@ -366,8 +391,8 @@ cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, void* udict
 cudaError_t launch_delta_dictionary(const dm_column_in* in, char* ws, const WsLayout& L, void* udict, uint32_t* rank,
                                     dm_header* hdr, cudaStream_t st) {
   if (in->n_delta == 0) return cudaSuccess;
-  return in->key == DM_KEY_U64 ? run<KeyU64, kSortItemsU64>(in, ws, L, udict, rank, hdr, st)
-                               : run<KeyB16, kSortItemsB16>(in, ws, L, udict, rank, hdr, st);
+  return in->key == DM_KEY_U64 ? run<KeyU64>(in, ws, L, udict, rank, hdr, st)
+                               : run<KeyB16>(in, ws, L, udict, rank, hdr, st);
 }
 
 }  // namespace dm

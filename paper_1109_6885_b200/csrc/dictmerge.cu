@@ -83,6 +83,20 @@ uint32_t host_width(uint64_t n) {
 }
 uint64_t host_words(uint64_t n, uint32_t bits) { return (n * (uint64_t)bits + 63) / 64; }
 
+int sort_variant() {
+  static const int v = [] {
+    const char* s = std::getenv("DM_SORT_CFG");
+    const int x = s ? std::atoi(s) : 0;
+    return (x >= 0 && x < 4) ? x : 0;
+  }();
+  return v;
+}
+
+uint64_t sort_tile_keys(int key) {
+  const SortShape& s = kSortShapes[sort_variant()];
+  return (uint64_t)s.threads * (key == DM_KEY_U64 ? s.items_u64 : s.items_b16);
+}
+
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 WsLayout ws_layout(const dm_column_in* in) {
@@ -90,7 +104,7 @@ WsLayout ws_layout(const dm_column_in* in) {
   const size_t E = in->key == DM_KEY_U64 ? 8 : 16;
   const uint64_t nD = in->n_delta;
   L.npass = in->key == DM_KEY_U64 ? 8 : 16;
-  const uint64_t sort_tile = (uint64_t)kSortThreads * (in->key == DM_KEY_U64 ? kSortItemsU64 : kSortItemsB16);
+  const uint64_t sort_tile = sort_tile_keys(in->key);
   L.ntiles_sort = (nD + sort_tile - 1) / sort_tile;
   L.ntiles_unique = (nD + kUniqThreads * kUniqItems - 1) / (kUniqThreads * kUniqItems);
   L.ntiles_merge = std::max<uint64_t>(1, (in->dict_len + nD + kMergeTile - 1) / kMergeTile);

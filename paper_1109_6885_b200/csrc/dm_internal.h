@@ -9,9 +9,13 @@
 namespace dm {
 
 // ---- tiling constants
-constexpr int kSortThreads = 512;
-constexpr int kSortItemsU64 = 16;                        // 8192 keys per onesweep tile
-constexpr int kSortItemsB16 = 8;                         // 4096 keys per tile (16-byte keys)
+// Onesweep tile shapes (threads x keys per thread); variant chosen by sort_variant().
+struct SortShape {
+  int threads, items_u64, items_b16;
+};
+constexpr SortShape kSortShapes[4] = {{512, 16, 8}, {256, 16, 8}, {256, 8, 4}, {1024, 8, 4}};
+int sort_variant();  // DM_SORT_CFG environment override (experiments), default 0
+uint64_t sort_tile_keys(int key);
 constexpr int kUniqThreads = 512;
 constexpr int kUniqItems = 8;                            // 4096 per tile
 constexpr int kMergeThreads = 256;
