@@ -234,13 +234,21 @@ def main():
     import torch
     import paper_1109_6885_b200 as dm
 
+    # BENCH_PG_BACKEND=gloo exercises the multi-rank path with several ranks on one
+    # GPU (test use only; ranks never wait on each other inside a kernel).
+    backend = os.environ.get("BENCH_PG_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1) if backend != "nccl" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     pg = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
         pg = dist
+    red_dev = dev if backend == "nccl" else torch.device("cpu")
 
     cfg = cfg_number(args.workload)
     table = cfg == 4
@@ -308,7 +316,7 @@ def main():
         pg.barrier()
     step_ms = [a.elapsed_time(b) for a, b in gev]
     total_ms = sum(step_ms)
-    tot = torch.tensor([total_ms, float(n_tuples)], dtype=torch.float64, device=dev)
+    tot = torch.tensor([total_ms, float(n_tuples)], dtype=torch.float64, device=red_dev)
     if pg:
         t = tot[:1].clone()
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
@@ -369,7 +377,7 @@ def main():
             nU, nb, _ = ctx.merge(hUM, hM, n_m, b, hD, hU, hMo)
         e2e_s = (time.perf_counter() - t0) / args.e2e_steps
         if pg:
-            t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+            t = torch.tensor([e2e_s], dtype=torch.float64, device=red_dev)
             pg.all_reduce(t, op=pg.ReduceOp.MAX)
             e2e_s = float(t.item())
         h2d = hUM.numel() * hUM.element_size() + hD.numel() * hD.element_size() + hM.numel() * 8
