@@ -11,16 +11,16 @@
 // place of threads:
 //   k_partition    merge-path co-ranks at every tile diagonal (the quantile
 //                  split, [8][5] in P:302), one warp per boundary, 32-way search
-//   k_merge_count  phase 1: per tile, stage both ranges in shared memory,
-//                  per-thread co-rank + 8-step serial merge; a U_D element equal
-//                  to the U_M element right before it in merged order is the
-//                  duplicate (ties take U_M first -- the GPU form of P:304's
-//                  boundary check); the tile's duplicate count is stored
+//   k_merge_count  phase 1: per tile, stage both ranges in shared memory and
+//                  rank the smaller side inside the larger (TileRank below); a
+//                  U_D value equal to the U_M value right before it in merged
+//                  order is the duplicate (ties take U_M first -- the GPU form of
+//                  P:304's boundary check); the tile's duplicate count is stored
 //   k_scan_counts  phase 2: prefix sum of the counts; writes |U'|, b'
-//   k_merge_write  phase 3: re-merge and write U', X_M, X_D at the offsets,
-//                  staged in shared memory so the writes are coalesced
-// A single-pass variant (decoupled look-back inside the merge) was measured
-// slower: every tile of the first wave waits on a look-back chain.
+//   k_merge_write  phase 3: rank again and write U', X_M, X_D at the offsets
+// Measured alternatives: a per-thread co-rank + serial merge (the CPU pattern)
+// cost ~160 instructions per element; a single pass with decoupled look-back
+// was 1% faster on cfg2 but 11% slower on cfg5 (look-back chains at 5e5 tiles).
 #include "dm_device.cuh"
 
 namespace dm {
