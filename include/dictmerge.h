@@ -179,6 +179,20 @@ dm_ctx* dm_ctx_create(int device);
 void dm_ctx_destroy(dm_ctx* ctx);
 dm_status dm_merge_column_host(dm_ctx* ctx, const dm_column_in* in, dm_column_out* out);
 
+/* Process-wide tuning knobs (they never change results, only which kernels
+ * run).  knob 0 = placement of the main translation table in Step 2(b):
+ *   0 auto (default): plain X_M in shared memory when it fits (<= 96 KB);
+ *     else, when the plain X_M exceeds 64 MB (it would not stay L2-resident),
+ *     the compact table XC (per 2048 codes a 16-byte record,
+ *     per new dictionary value one byte; X_M[c] = c + #{new values inserted at
+ *     or before main position c}, P:224-230 restated) read through L2; else
+ *     the plain X_M through L2;
+ *   1 plain X_M only;  2 XC, staged in shared memory when it fits, else L2;
+ *   3 XC through L2.
+ * Returns DM_OK, or DM_E_INVALID for an unknown knob or value.  Affects calls
+ * made after it returns (a captured CUDA graph keeps the kernels it recorded). */
+int dm_set_tuning(int knob, int value);
+
 /* Number of library kernels launched by this process so far (monotone). */
 uint64_t dm_launch_count(void);
 /* Last CUDA error code seen by the library (cudaError_t as int). */

@@ -27,7 +27,7 @@ from . import build as _build
 __all__ = [
     "KEY_U64", "KEY_B16", "Status", "DictMergeError", "width", "words", "merged_codes_cap_words",
     "workspace_bytes", "merge_column", "merge_column_async", "merge_table", "pack_codes", "unpack_codes",
-    "ColumnMerger", "HostContext", "launch_count", "lib_path",
+    "ColumnMerger", "HostContext", "launch_count", "lib_path", "set_tuning",
 ]
 
 KEY_U64, KEY_B16 = 0, 1
@@ -101,6 +101,7 @@ def _lib():
             "dm_ctx_destroy": (None, [vp]),
             "dm_merge_column_host": (i32, [vp, P(_In), P(_Out)]),
             "dm_launch_count": (u64, []),
+            "dm_set_tuning": (i32, [i32, i32]),
             "dm_last_cuda_error": (i32, []),
             "dm_status_str": (ctypes.c_char_p, [i32]),
         }
@@ -124,6 +125,17 @@ def words(n: int, bits: int) -> int:
 
 def launch_count() -> int:
     return int(_lib().dm_launch_count())
+
+
+XM_AUTO, XM_PLAIN, XM_COMPACT, XM_COMPACT_L2 = 0, 1, 2, 3
+
+
+def set_tuning(knob: int, value: int) -> None:
+    """dm_set_tuning: knob 0 = Step 2(b) translation-table placement (XM_* above).
+    Never changes results; used by tests to force each kernel variant."""
+    st = _lib().dm_set_tuning(knob, value)
+    if st != Status.OK:
+        raise DictMergeError(st, "dm_set_tuning")
 
 
 def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:

@@ -276,7 +276,9 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_write(const void* __res
                                                                const uint64_t* __restrict__ part,
                                                                const uint64_t* __restrict__ excl,
                                                                void* __restrict__ U, uint32_t* __restrict__ XM,
-                                                               uint32_t* __restrict__ XD, dm_header* hdr) {
+                                                               uint32_t* __restrict__ XD, dm_header* hdr,
+                                                               uint32_t* __restrict__ rblk,
+                                                               uint8_t* __restrict__ offs) {
   using K = typename KT::K;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t s_warp[kMergeThreads / 32 + 1];
@@ -293,8 +295,15 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_write(const void* __res
     tr.a_rank(a, nbb, dupb);
     const uint32_t o = a + nbb - dupb;  // tile-local U' slot
     const K v = tr.A_(a);
-    KT::store(U, base + o, v);
-    XM[tr.i0 + a] = (uint32_t)(base + o);
+    const uint64_t i = tr.i0 + a, u = base + o;
+    KT::store(U, u, v);
+    XM[i] = (uint32_t)u;
+    if (rblk) {
+      // XC: R(g) = #{new values with insertion point p <= 256g} = X_M[256g] - 256g,
+      // and after the last main entry (the end of the last list).
+      if ((i & (kXcBlock - 1)) == 0) rblk[i / kXcBlock] = (uint32_t)(u - i);
+      if (i == nA - 1) rblk[(nA + kXcBlock - 1) / kXcBlock] = (uint32_t)(u - i);
+    }
     // strictly increasing U_M over the pairs this tile owns
     if ((a > 0 || tr.has_prev) && !KT::lt(a > 0 ? tr.A_(a - 1) : tr.sk[0], v)) unsorted = true;
   }
@@ -307,9 +316,42 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_write(const void* __res
     } else {
       KT::store(U, base + o, tr.B_(j));
       XD[tr.j0 + j] = (uint32_t)(base + o);
+      if (offs) {
+        // a new value: inserted before U_M[p], p = #U_M below it; it is the
+        // (u - p)-th new value in sorted order.  It raises X_M[c] for c >= p;
+        // stored in the list of the block holding p - 1 (blocks own (256g, 256g+256])
+        const uint64_t p = tr.i0 + tr.b_q(j);
+        offs[base + o - p] = (uint8_t)((p - 1) & (kXcBlock - 1));
+      }
     }
   }
   if (__any_sync(FULL, unsorted) && lane_id() == 0) atomicMin(&hdr->status, (int)DM_E_UNSORTED);
+}
+
+// XC superblock records (NEXT3) from the block samples R(g) = rblk[g]:
+// {R(8s), cum bytes 0..3, cum bytes 4..7, flag}, cum[t] = R(8s+t+1) - R(8s).
+// Flag = the counts do not fit a byte, or one block holds more than
+// kXcMaxBlock insertions (bounds the per-lookup scan); flagged superblocks are
+// looked up in the plain X_M.
+__global__ void __launch_bounds__(256) k_xc_records(const uint32_t* __restrict__ rblk, uint64_t nblk, uint64_t nsb,
+                                                    uint4* __restrict__ rec) {
+  const uint64_t sb = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (sb >= nsb) return;
+  constexpr uint32_t BPS = kXcSuper / kXcBlock;
+  const uint64_t g0 = sb * BPS;
+  const uint32_t R0 = rblk[g0];
+  uint32_t prev = 0, lo = 0, hi = 0, flag = 0;
+#pragma unroll
+  for (uint32_t t = 0; t < BPS; ++t) {
+    const uint32_t c = rblk[umin64(g0 + t + 1, nblk)] - R0;
+    if (c > 255u || c - prev > kXcMaxBlock) flag = 1;
+    if (t < 4)
+      lo |= (c & 255u) << (8 * t);
+    else
+      hi |= (c & 255u) << (8 * (t - 4));
+    prev = c;
+  }
+  rec[sb] = make_uint4(R0, lo, hi, flag);
 }
 
 __global__ void k_empty_header(dm_header* hdr) {
@@ -344,9 +386,18 @@ cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, const void*
       reinterpret_cast<uint32_t*>(ws + L.counters) + CNT_MERGE, in->dict_len, hdr);
   const size_t smem_write = smem_count;
   ensure_smem((const void*)k_merge_write<KT>);
+  const bool xc = xc_wanted(in->dict_len);
+  uint32_t* rblk = xc ? reinterpret_cast<uint32_t*>(ws + L.xc_rblk) : nullptr;
+  uint8_t* offs = xc ? reinterpret_cast<uint8_t*>(ws + L.xc_offs) : nullptr;
   k_merge_write<KT><<<(unsigned)nt, kMergeThreads, smem_write, st>>>(in->main_dict, in->dict_len, udict, part, excl,
-                                                                     U, xm, xd, hdr);
+                                                                     U, xm, xd, hdr, rblk, offs);
   note_launch(4);
+  if (xc) {
+    const uint64_t nsb = xc_nsb(in->dict_len);
+    k_xc_records<<<(unsigned)((nsb + 255) / 256), 256, 0, st>>>(rblk, xc_nblk(in->dict_len), nsb,
+                                                                reinterpret_cast<uint4*>(ws + L.xc_rec));
+    note_launch();
+  }
   return cudaGetLastError();
 }
 

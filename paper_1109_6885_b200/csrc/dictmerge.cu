@@ -83,6 +83,9 @@ uint32_t host_width(uint64_t n) {
 }
 uint64_t host_words(uint64_t n, uint32_t bits) { return (n * (uint64_t)bits + 63) / 64; }
 
+static std::atomic<int> g_tuning[4] = {};
+int tuning(int knob) { return (knob >= 0 && knob < 4) ? g_tuning[knob].load(std::memory_order_relaxed) : 0; }
+
 int sort_variant() {
   static const int v = [] {
     const char* s = std::getenv("DM_SORT_CFG");
@@ -133,6 +136,9 @@ WsLayout ws_layout(const dm_column_in* in) {
   L.mexcl = take(L.ntiles_merge * sizeof(uint64_t));
   L.xm = take(in->dict_len * 4);
   L.xd = take(nD * 4);
+  L.xc_rblk = take((xc_nblk(in->dict_len) + 1) * 4);
+  L.xc_rec = take(xc_nsb(in->dict_len) * 16);
+  L.xc_offs = take(nD + 16);
   L.total = o;
   return L;
 }
@@ -200,7 +206,11 @@ static dm_status merge_async(const dm_column_in* in, const dm_column_out* out, v
   if ((e = launch_dictionary_merge(in, out, w, L, udict, xm, xd, d_header, st)) != cudaSuccess) return cuda_fail(e);
   mark(2);
   // Step 2(b): M' (Eq 11).
-  if (with_step2 && (e = launch_recompress(in, out, xm, xd, rank, d_header, st)) != cudaSuccess)
+  const bool xc = xc_wanted(in->dict_len);
+  if (with_step2 && (e = launch_recompress(in, out, xm, xd, rank, d_header, st, 0,
+                                           xc ? reinterpret_cast<const uint4*>(w + L.xc_rec) : nullptr,
+                                           xc ? reinterpret_cast<const uint8_t*>(w + L.xc_offs) : nullptr)) !=
+                         cudaSuccess)
     return cuda_fail(e);
   mark(3);
   return DM_OK;
@@ -263,6 +273,12 @@ struct dm_ctx {
 };
 
 extern "C" {
+
+int dm_set_tuning(int knob, int value) {
+  if (knob != 0 || value < 0 || value > 3) return DM_E_INVALID;
+  g_tuning[knob].store(value);
+  return DM_OK;
+}
 
 uint32_t dm_width(uint64_t n) { return host_width(n); }
 uint64_t dm_words(uint64_t n, uint32_t bits) { return host_words(n, bits); }

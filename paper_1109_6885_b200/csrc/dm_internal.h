@@ -26,6 +26,33 @@ constexpr int kRecThreads = 32 * (kRecConsumerWarps + 1);  // + one TMA producer
 constexpr int kRecGroups = 128;                          // 32-row groups per chunk (4096 rows)
 constexpr int kRecStages = 4;                            // TMA input ring depth
 constexpr uint32_t kRecSmemXBytes = 96 * 1024;           // X_M staged in shared memory up to this size
+constexpr int kRecStagesXc = 3;                          // ring depth when the compact X_M takes the smem
+
+// Compact translation table "XC": X_M[c] = c + #{new values
+// inserted at or before main position c} (insertion point p of a new value =
+// #U_M below it; it raises X_M[c] for c >= p).  Per 2048-code superblock s one
+// 16-byte record {R, cum[0..3], cum[4..7], flag}: R = #{p <= 2048s}, cum[t] =
+// #{2048s < p <= 2048s + 256(t+1)}; per new value (sorted order) one byte,
+// (p - 1) mod 256.  A
+// superblock whose counts do not fit (> 255, or > kXcMaxBlock in one block) is
+// flagged and its lookups read the plain X_M.
+constexpr uint32_t kXcBlock = 256;
+constexpr uint32_t kXcSuper = 2048;
+constexpr uint32_t kXcMaxBlock = 32;
+constexpr uint64_t kXcGlobalMinBytes = 64ull << 20;     // plain X_M above this: use XC from L2
+enum XMode { XM_RAW_GLOBAL = 0, XM_RAW_SMEM = 1, XM_XC_SMEM = 2, XM_XC_GLOBAL = 3 };
+// Tuning knobs (dm_set_tuning): index 0 = X_M placement (0 auto, 1 plain only,
+// 2 compact (smem if it fits, else L2), 3 compact from L2).
+int tuning(int knob);
+inline uint64_t xc_nblk(uint64_t dict_len) { return (dict_len + kXcBlock - 1) / kXcBlock; }
+inline uint64_t xc_nsb(uint64_t dict_len) { return (dict_len + kXcSuper - 1) / kXcSuper; }
+// Whether a merge builds XC at all: only when the plain X_M is too big for smem.
+inline bool xc_enabled(uint64_t dict_len) { return dict_len * 4 > kRecSmemXBytes; }
+// Whether this merge builds XC: auto only when the plain X_M exceeds kXcGlobalMinBytes.
+inline bool xc_wanted(uint64_t dict_len) {
+  const int k = tuning(0);
+  return k == 1 ? false : k == 0 ? dict_len * 4 > kXcGlobalMinBytes : xc_enabled(dict_len);
+}
 
 constexpr uint32_t kRadixFlagAgg = 1u << 30;
 constexpr uint32_t kRadixFlagPre = 2u << 30;
@@ -63,6 +90,9 @@ struct WsLayout {
   size_t mexcl;          // u64[ntiles_merge] exclusive prefix of mcount
   size_t xm;             // X_M u32[dict_len]
   size_t xd;             // X_D u32[n_delta]
+  size_t xc_rblk;        // XC: u32[nblk + 1], new values inserted before each 256-block
+  size_t xc_rec;         // XC: uint4[nsb] superblock records
+  size_t xc_offs;        // XC: u8[n_delta] insertion position mod 256 per new value
   size_t total;
   uint64_t ntiles_sort, ntiles_unique, ntiles_merge;
   int npass;
@@ -87,13 +117,16 @@ cudaError_t last_error_check();
 cudaError_t launch_delta_dictionary(const dm_column_in* in, char* ws, const WsLayout& L, void* udict, uint32_t* rank,
                                     dm_header* hdr, cudaStream_t st);
 // Step 1(b) + 2(a): merge-path merge -> U', X_M, X_D, hdr->merged_dict_len / merged_bits.
+// When xc_enabled(dict_len), also builds the compact table XC in the workspace.
 cudaError_t launch_dictionary_merge(const dm_column_in* in, const dm_column_out* out, char* ws, const WsLayout& L,
                                     const void* udict, uint32_t* xm, uint32_t* xd, dm_header* hdr, cudaStream_t st);
 // Step 2(b): recompress main through X_M and append delta through X_D.
 // fixed_bits != 0: b' given by the caller (dm_recompress); else read from hdr->merged_bits.
+// xc_rec / xc_offs: the compact table (NULL: plain X_M only).
 cudaError_t launch_recompress(const dm_column_in* in, const dm_column_out* out, const uint32_t* xm,
                               const uint32_t* xd, const uint32_t* rank, dm_header* hdr, cudaStream_t st,
-                              uint32_t fixed_bits = 0);
+                              uint32_t fixed_bits = 0, const uint4* xc_rec = nullptr,
+                              const uint8_t* xc_offs = nullptr);
 cudaError_t launch_pack(const uint32_t* codes, uint64_t n, uint32_t bits, uint64_t* words, cudaStream_t st);
 cudaError_t launch_unpack(const uint64_t* words, uint64_t n, uint32_t bits, uint32_t* codes, cudaStream_t st);
 

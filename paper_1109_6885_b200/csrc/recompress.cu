@@ -50,26 +50,77 @@ __device__ __forceinline__ uint32_t warp_pack(uint32_t v, uint32_t nb, uint32_t 
   return word;
 }
 
+// Compact X_M lookup (XC, NEXT3; layout in dm_internal.h):
+//   X_M[c] = c + start + #{entries of c's 256-block with offset < c mod 256}
+// where start = R + cum[t-1] = #{new values with insertion point p <= 256g}
+// (g = c's block) and the block's entries are the new values with p in
+// (256g, 256g + 256], stored as (p - 1) mod 256: consecutive bytes
+// [start, end), scanned a word at a time with a SIMD byte compare.  SM: tables in shared memory; else
+// read through L2 (evict-last).  Flagged superblocks use the plain X_M.
+__device__ __forceinline__ uint4 ld_gather_v4(const uint4* p, uint64_t policy) {
+  uint4 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p), "l"(policy));
+  return v;
+}
+template <bool SM>
+__device__ __forceinline__ uint32_t xc_lookup(uint32_t code, const uint4* __restrict__ rec,
+                                              const uint32_t* __restrict__ offs32, const uint32_t* __restrict__ XM,
+                                              uint64_t pol) {
+  const uint32_t sb = code / kXcSuper, t = (code / kXcBlock) % (kXcSuper / kXcBlock), o = code % kXcBlock;
+  const uint4 r = SM ? rec[sb] : ld_gather_v4(rec + sb, pol);
+  if (r.w) return ld_gather_u32(XM + code, pol);
+  const uint64_t cum = ((uint64_t)r.z << 32) | r.y;
+  const uint32_t start = r.x + (t ? (uint32_t)(cum >> (8 * t - 8)) & 255u : 0u);
+  const uint32_t end = r.x + ((uint32_t)(cum >> (8 * t)) & 255u);
+  const uint32_t ob = o * 0x01010101u;
+  uint32_t cnt = 0;
+  for (uint32_t w = start & ~3u; w < end; w += 4) {
+    const uint32_t v = SM ? offs32[w >> 2] : ld_gather_u32(offs32 + (w >> 2), pol);
+    const uint32_t le = __vcmpltu4(v, ob);  // 0xff in each byte < o
+    const uint32_t lo = start > w ? start - w : 0u, hi = end - w;  // valid bytes [lo, min(hi, 4))
+    const uint32_t vm = shl32(0xffffffffu, 8 * lo) & (hi >= 4 ? 0xffffffffu : shl32(1u, 8 * hi) - 1u);
+    cnt += __popc(le & vm) >> 3;
+  }
+  return code + start + cnt;
+}
+
 // Warp-specialised: warp kRecConsumerWarps is the TMA producer, warps
 // 0..kRecConsumerWarps-1 consume.  full[s] completes when stage s holds its
 // chunk's main words; empty[s] completes when every consumer warp is done with
 // stage s.  No CTA-wide barrier after the prologue.  XS: X_M staged in shared
 // memory (tables up to kRecSmemXBytes), else gathered through L2.
-template <int NB, bool XS>
+// XMODE (XMode): where the main-code translation comes from.  The compact
+// modes decide on the device, from |U'|, whether XC fits the shared-memory
+// budget xc_budget: XM_XC_SMEM runs only if it does, its companion
+// (XM_XC_GLOBAL or XM_RAW_GLOBAL launched with xc_budget != 0) only if not.
+template <int NB, int XMODE>
 __global__ void __launch_bounds__(kRecThreads) k_recompress(const uint64_t* __restrict__ M, uint64_t n_main, uint32_t b,
                                                             uint64_t dict_len, const uint32_t* __restrict__ XM,
                                                             const uint32_t* __restrict__ XD,
                                                             const uint32_t* __restrict__ rank, uint64_t n_delta,
                                                             uint64_t* __restrict__ Mout, dm_header* hdr,
-                                                            uint32_t in_stage_bytes, uint32_t fixed_bits) {
+                                                            uint32_t in_stage_bytes, uint32_t fixed_bits,
+                                                            const uint4* __restrict__ xrec,
+                                                            const uint8_t* __restrict__ xoffs, uint32_t xc_budget) {
   constexpr int G = kRecGroups;
-  constexpr int S = kRecStages;
+  constexpr int S = XMODE == XM_XC_SMEM ? kRecStagesXc : kRecStages;
   constexpr int CW = kRecConsumerWarps;
   constexpr int U = G / CW;  // groups per consumer warp per chunk, all in flight together
+  constexpr bool XS = XMODE == XM_RAW_SMEM;
   static_assert(G % CW == 0, "groups must split evenly over consumer warps");
   const uint32_t hb = fixed_bits ? fixed_bits : hdr->merged_bits;
   if (NB && hb != (uint32_t)NB) return;
   const uint32_t nb = NB ? (uint32_t)NB : hb;
+  const uint64_t nsb = (dict_len + kXcSuper - 1) / kXcSuper;
+  uint64_t xc_offs_bytes = 0;
+  if (xc_budget) {
+    const uint64_t n_new = hdr->merged_dict_len - dict_len;
+    xc_offs_bytes = (n_new + 15) & ~15ull;
+    const bool fits = nsb * 16 + xc_offs_bytes <= xc_budget;
+    if ((XMODE == XM_XC_SMEM) != fits) return;
+  }
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
@@ -94,6 +145,14 @@ __global__ void __launch_bounds__(kRecThreads) k_recompress(const uint64_t* __re
   }
   if (XS) {
     for (uint32_t i = threadIdx.x; i < dict_len; i += blockDim.x) sx[i] = __ldg(XM + i);
+  }
+  uint4* srec = reinterpret_cast<uint4*>(sx);
+  const uint32_t* soffs = reinterpret_cast<const uint32_t*>(srec + nsb);
+  if (XMODE == XM_XC_SMEM) {
+    for (uint64_t i = threadIdx.x; i < nsb; i += blockDim.x) srec[i] = __ldg(xrec + i);
+    uint4* so = srec + nsb;
+    const uint4* go = reinterpret_cast<const uint4*>(xoffs);
+    for (uint64_t i = threadIdx.x; i < xc_offs_bytes / 16; i += blockDim.x) so[i] = __ldg(go + i);
   }
   __syncthreads();
 
@@ -146,7 +205,14 @@ __global__ void __launch_bounds__(kRecThreads) k_recompress(const uint64_t* __re
           bad = true;
           code = 0;
         }
-        v[u] = XS ? sx[code] : ld_gather_u32(XM + code, pol_x);
+        if constexpr (XMODE == XM_RAW_SMEM)
+          v[u] = sx[code];
+        else if constexpr (XMODE == XM_XC_SMEM)
+          v[u] = xc_lookup<true>(code, srec, soffs, XM, pol_x);
+        else if constexpr (XMODE == XM_XC_GLOBAL)
+          v[u] = xc_lookup<false>(code, xrec, reinterpret_cast<const uint32_t*>(xoffs), XM, pol_x);
+        else
+          v[u] = ld_gather_u32(XM + code, pol_x);
       } else if (row < n_total) {
         v[u] = __ldg(XD + __ldg(rank + (row - n_main)));
       } else {
@@ -195,32 +261,64 @@ __global__ void __launch_bounds__(256) k_unpack(const uint32_t* __restrict__ wor
   }
 }
 
+// Shared-memory bytes left for XC next to a kRecStagesXc-deep ring.
+static uint32_t xc_smem_budget(uint32_t in_stage) {
+  static int optin = [] {
+    int d = 0, v = 0;
+    cudaGetDevice(&d);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, d);
+    return v;
+  }();
+  const int64_t b = (int64_t)optin - 1024 - 128 - (int64_t)kRecStagesXc * in_stage;
+  return b > 0 ? (uint32_t)(b & ~15ll) : 0u;
+}
+
 template <int NB>
 cudaError_t launch_nb(const dm_column_in* in, const dm_column_out* out, const uint32_t* xm, const uint32_t* xd,
-                      const uint32_t* rank, dm_header* hdr, cudaStream_t st, uint32_t nb_cap, uint32_t fixed_bits) {
-  (void)nb_cap;
+                      const uint32_t* rank, dm_header* hdr, cudaStream_t st, uint32_t fixed_bits, const uint4* xrec,
+                      const uint8_t* xoffs) {
   const uint32_t in_stage = kRecGroups * in->main_bits * 4 + 16;
-  const bool xs = in->dict_len * 4 <= kRecSmemXBytes;
-  const size_t smem = 128 + (size_t)kRecStages * in_stage + (xs ? in->dict_len * 4 : 0);
   const int sms = device_sms();
   const uint64_t n_total = in->n_main + in->n_delta;
   const uint64_t nchunks = (n_total + 32ull * kRecGroups - 1) / (32ull * kRecGroups);
-  auto go = [&](auto kern) {
+  auto go = [&](auto kern, size_t smem, uint32_t budget) {
     const int occ = occupancy((const void*)kern, kRecThreads, smem);
     const unsigned grid = (unsigned)std::min<uint64_t>(nchunks, (uint64_t)sms * occ);
     kern<<<grid, kRecThreads, smem, st>>>(in->main_codes, in->n_main, in->main_bits, in->dict_len, xm, xd, rank,
-                                          in->n_delta, out->merged_codes, hdr, in_stage, fixed_bits);
+                                          in->n_delta, out->merged_codes, hdr, in_stage, fixed_bits, xrec, xoffs,
+                                          budget);
+    note_launch();
   };
-  if (xs)
-    go(k_recompress<NB, true>);
+  const size_t ring = 128 + (size_t)kRecStages * in_stage;
+  if (in->dict_len * 4 <= kRecSmemXBytes) {
+    go(k_recompress<NB, XM_RAW_SMEM>, ring + in->dict_len * 4, 0);
+    return cudaGetLastError();
+  }
+  const int knob = tuning(0);
+  if (!xrec || knob == 1) {
+    go(k_recompress<NB, XM_RAW_GLOBAL>, ring, 0);
+    return cudaGetLastError();
+  }
+  // compact table available: the smem variant (if its records can fit at all)
+  // plus an L2 companion; which one runs is decided on the device from |U'|
+  const bool want_smem = knob == 2;  // measured slower than the L2 gather on cfg2: opt-in
+  if (knob == 0 && in->dict_len * 4 <= kXcGlobalMinBytes) {
+    go(k_recompress<NB, XM_RAW_GLOBAL>, ring, 0);
+    return cudaGetLastError();
+  }
+  const uint32_t budget0 = want_smem ? xc_smem_budget(in_stage) : 0u;
+  const uint32_t budget = (uint64_t)xc_nsb(in->dict_len) * 16 <= budget0 ? budget0 : 0u;
+  if (budget) go(k_recompress<NB, XM_XC_SMEM>, 128 + (size_t)kRecStagesXc * in_stage + budget, budget);
+  const bool xc_l2 = knob == 2 || knob == 3 || in->dict_len * 4 > kXcGlobalMinBytes;
+  if (xc_l2)
+    go(k_recompress<NB, XM_XC_GLOBAL>, ring, budget);
   else
-    go(k_recompress<NB, false>);
-  note_launch();
+    go(k_recompress<NB, XM_RAW_GLOBAL>, ring, budget);
   return cudaGetLastError();
 }
 
 using LaunchFn = cudaError_t (*)(const dm_column_in*, const dm_column_out*, const uint32_t*, const uint32_t*,
-                                 const uint32_t*, dm_header*, cudaStream_t, uint32_t, uint32_t);
+                                 const uint32_t*, dm_header*, cudaStream_t, uint32_t, const uint4*, const uint8_t*);
 template <int... I>
 constexpr auto make_table(std::integer_sequence<int, I...>) {
   return std::array<LaunchFn, sizeof...(I)>{&launch_nb<I>...};
@@ -230,21 +328,21 @@ constexpr auto make_table(std::integer_sequence<int, I...>) {
 
 cudaError_t launch_recompress(const dm_column_in* in, const dm_column_out* out, const uint32_t* xm,
                               const uint32_t* xd, const uint32_t* rank, dm_header* hdr, cudaStream_t st,
-                              uint32_t fixed_bits) {
+                              uint32_t fixed_bits, const uint4* xc_rec, const uint8_t* xc_offs) {
   if (in->n_main + in->n_delta == 0) return cudaSuccess;
   static const auto table = make_table(std::make_integer_sequence<int, 33>{});  // [0] = runtime width
-  if (fixed_bits) return table[fixed_bits](in, out, xm, xd, rank, hdr, st, fixed_bits, fixed_bits);
+  if (fixed_bits) return table[fixed_bits](in, out, xm, xd, rank, hdr, st, fixed_bits, nullptr, nullptr);
   const uint64_t lo_len = std::max<uint64_t>(in->dict_len, in->n_delta ? 1 : 0);
   const uint32_t nb_lo = host_width(lo_len), nb_hi = host_width(in->dict_len + in->n_delta);
   if (nb_hi > 32) return cudaErrorInvalidValue;  // caller checks DM_E_TOO_WIDE first
   if (nb_hi - nb_lo <= 2) {
     for (uint32_t nb = nb_lo; nb <= nb_hi; ++nb) {
-      cudaError_t e = table[nb](in, out, xm, xd, rank, hdr, st, nb_hi, 0);
+      cudaError_t e = table[nb](in, out, xm, xd, rank, hdr, st, 0, xc_rec, xc_offs);
       if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
   }
-  return table[0](in, out, xm, xd, rank, hdr, st, nb_hi, 0);
+  return table[0](in, out, xm, xd, rank, hdr, st, 0, xc_rec, xc_offs);
 }
 
 cudaError_t launch_pack(const uint32_t* codes, uint64_t n, uint32_t bits, uint64_t* words, cudaStream_t st) {

@@ -1,0 +1,126 @@
+"""Compact translation table XC vs the oracle, bit-exact.
+
+XC replaces the Step 2(b) gather X_M[c] by c + #{new dictionary values inserted
+at or before main position c} (the closed form of X_M; DESIGN.md
+§7).  It must never change a result, so every case runs under each placement
+knob (auto / plain X_M / XC with shared-memory preference / XC from L2) and is
+compared element by element with the oracle.  The cases aim at the format's
+edges: insertions before the first and after the last main entry, at 256- and
+2048-code boundaries, blocks with exactly kXcMaxBlock (32) and 33 insertions,
+superblocks with 255 and 256 insertions (byte overflow -> flagged), dictionary
+sizes that are and are not multiples of the block sizes, and a new-value count
+too large for shared memory (L2 companion kernel).
+"""
+import numpy as np
+import pytest
+import torch
+
+import datagen
+import oracle
+from tests.parity import compare, run_gpu
+
+pytestmark = pytest.mark.gpu
+
+KNOBS = (0, 1, 2, 3)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1109_6885_b200  # noqa: F401
+    oracle.build()
+
+
+@pytest.fixture(autouse=True)
+def _reset_knob():
+    yield
+    import paper_1109_6885_b200 as dm
+    dm.set_tuning(0, 0)
+
+
+SPACING = 1000  # U_M[i] = SPACING * (i + 1): value SPACING*p + k (0 < k < SPACING) lands before U_M[p]
+
+
+def _column(n_dict, n_main, insert_at, n_reuse, seed, key="u64"):
+    """insert_at: list of (position p, count) -> `count` distinct new values before U_M[p]."""
+    rng = np.random.default_rng(seed)
+    UM = (np.arange(n_dict, dtype=np.uint64) + 1) * np.uint64(SPACING)
+    new = []
+    for p, cnt in insert_at:
+        ks = rng.choice(np.arange(1, SPACING), size=cnt, replace=False).astype(np.uint64)
+        new.append(np.uint64(SPACING) * np.uint64(p) + ks)
+    new = np.concatenate(new) if new else np.zeros(0, np.uint64)
+    reuse = UM[rng.integers(0, n_dict, size=n_reuse)] if n_dict else np.zeros(0, np.uint64)
+    D = np.concatenate([new, new[: len(new) // 3], reuse])  # some new values repeat
+    D = D[rng.permutation(D.size)]
+    codes = rng.integers(0, n_dict, size=n_main, dtype=np.uint64).astype(np.uint32)
+    bits = datagen.width_hint(n_dict)
+    if key == "u64":
+        return datagen.Column("u64", UM, codes, bits, D)
+    to16 = lambda v: datagen.hilo_to_bytes(np.zeros_like(v), v)
+    return datagen.Column("b16", to16(UM), codes, bits, to16(D))
+
+
+def _run_all_knobs(col):
+    import paper_1109_6885_b200 as dm
+    ref = None
+    for k in KNOBS:
+        dm.set_tuning(0, k)
+        M, r = run_gpu(col)
+        ref = compare(col, M, r, ref=ref)
+
+
+def _spread(n_dict, n_new, seed):
+    rng = np.random.default_rng(seed)
+    pos = rng.integers(0, n_dict + 1, size=n_new)
+    p, c = np.unique(pos, return_counts=True)
+    return list(zip(p.tolist(), c.tolist()))
+
+
+@pytest.mark.parametrize("key", ["u64", "b16"])
+def test_xc_uniform_insertions(key):
+    # X_M = 1.2 MB (> 96 KB smem staging) with ~1% new values: XC in shared memory
+    n = 300_001
+    col = _column(n, 1_000_003, _spread(n, 3000, 1), 20_000, seed=1, key=key)
+    _run_all_knobs(col)
+
+
+def test_xc_boundaries_and_overflow():
+    n = 2048 * 40 + 77  # ragged last superblock
+    ins = [(0, 5), (255, 3), (256, 4), (2047, 2), (2048, 6),  # block / superblock edges
+           (2048 * 3 + 10, 32),                                 # exactly kXcMaxBlock in one block
+           (2048 * 5 + 300, 33),                                # one over: superblock flagged
+           ]
+    # 255 insertions in one superblock, <= 32 per block: fits exactly
+    ins += [(2048 * 7 + 256 * t + 5, 32 if t < 7 else 31) for t in range(8)]
+    # 256 in one superblock (byte overflow -> flagged), spread over its blocks
+    ins += [(2048 * 9 + 256 * t + 7, 32) for t in range(8)]
+    ins += [(n - 1, 9), (n, 11)]                               # before the last entry, after it
+    col = _column(n, 400_000, ins, 5000, seed=2)
+    _run_all_knobs(col)
+
+
+def test_xc_dictionary_multiple_of_superblock_and_tail_inserts():
+    n = 2048 * 64  # 131072: multiple of both block sizes; new values after the last entry
+    col = _column(n, 300_000, [(n, 40), (n - 256, 3), (1, 1)] + _spread(n, 500, 3), 1000, seed=3)
+    _run_all_knobs(col)
+
+
+def test_xc_too_large_for_shared_memory():
+    # 300k distinct new values: XC exceeds the smem budget -> the L2 companion runs
+    n = 100_000
+    col = _column(n, 500_000, _spread(n, 300_000, 4), 1000, seed=4)
+    _run_all_knobs(col)
+
+
+def test_xc_no_new_values_and_all_new():
+    n = 50_000
+    _run_all_knobs(_column(n, 200_000, [], 30_000, seed=5))          # X_M = identity
+    _run_all_knobs(_column(n, 200_000, _spread(n, 20_000, 6), 0, seed=6))
+
+
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_xc_configs_scaled(cfg):
+    col = datagen.make_config(cfg, scale=0.1)
+    _run_all_knobs(col)
