@@ -189,6 +189,7 @@ dm_status dm_merge_column_host(dm_ctx* ctx, const dm_column_in* in, dm_column_ou
  *     the plain X_M through L2;
  *   1 plain X_M only;  2 XC, staged in shared memory when it fits, else L2;
  *   3 XC through L2.
+ * The process starts with knob 0 = $DM_XMODE if set (0..3), else 0.
  * Returns DM_OK, or DM_E_INVALID for an unknown knob or value.  Affects calls
  * made after it returns (a captured CUDA graph keeps the kernels it recorded). */
 int dm_set_tuning(int knob, int value);

@@ -329,29 +329,26 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_write(const void* __res
 }
 
 // XC superblock records (NEXT3) from the block samples R(g) = rblk[g]:
-// {R(8s), cum bytes 0..3, cum bytes 4..7, flag}, cum[t] = R(8s+t+1) - R(8s).
-// Flag = the counts do not fit a byte, or one block holds more than
-// kXcMaxBlock insertions (bounds the per-lookup scan); flagged superblocks are
-// looked up in the plain X_M.
+// {R(4s) | flag << 31, cum bytes 0..3}, cum[t] = R(4s+t+1) - R(4s).  Flag = the
+// counts do not fit a byte, or one block holds more than kXcMaxBlock
+// insertions (bounds the per-lookup scan); flagged superblocks are looked up
+// in the plain X_M.
 __global__ void __launch_bounds__(256) k_xc_records(const uint32_t* __restrict__ rblk, uint64_t nblk, uint64_t nsb,
-                                                    uint4* __restrict__ rec) {
+                                                    uint2* __restrict__ rec) {
   const uint64_t sb = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (sb >= nsb) return;
   constexpr uint32_t BPS = kXcSuper / kXcBlock;
   const uint64_t g0 = sb * BPS;
   const uint32_t R0 = rblk[g0];
-  uint32_t prev = 0, lo = 0, hi = 0, flag = 0;
+  uint32_t prev = 0, cum = 0, flag = R0 >> 31;
 #pragma unroll
   for (uint32_t t = 0; t < BPS; ++t) {
     const uint32_t c = rblk[umin64(g0 + t + 1, nblk)] - R0;
     if (c > 255u || c - prev > kXcMaxBlock) flag = 1;
-    if (t < 4)
-      lo |= (c & 255u) << (8 * t);
-    else
-      hi |= (c & 255u) << (8 * (t - 4));
+    cum |= (c & 255u) << (8 * t);
     prev = c;
   }
-  rec[sb] = make_uint4(R0, lo, hi, flag);
+  rec[sb] = make_uint2(R0 | (flag << 31), cum);
 }
 
 __global__ void k_empty_header(dm_header* hdr) {
@@ -378,14 +375,14 @@ cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, const void*
   k_partition<KT><<<(unsigned)((nt + 1 + 7) / 8), 256, 0, st>>>(in->main_dict, in->dict_len, udict, hdr, nt + 1,
                                                                    part);
   const size_t smem_count = sizeof(K) * (kMergeTile + 1) + 3 * sizeof(uint32_t) * (kMergeTile + 2);
-  ensure_smem((const void*)k_merge_count<KT>);
+  ensure_smem((const void*)k_merge_count<KT>, true);
   k_merge_count<KT><<<(unsigned)nt, kMergeThreads, smem_count, st>>>(in->main_dict, in->dict_len, udict, part, hdr,
                                                                      cnt);
   k_scan_counts<<<(unsigned)((nt + 2047) / 2048), 256, 0, st>>>(
       cnt, nt, excl, reinterpret_cast<uint64_t*>(ws + L.status_merge),
       reinterpret_cast<uint32_t*>(ws + L.counters) + CNT_MERGE, in->dict_len, hdr);
   const size_t smem_write = smem_count;
-  ensure_smem((const void*)k_merge_write<KT>);
+  ensure_smem((const void*)k_merge_write<KT>, true);
   const bool xc = xc_wanted(in->dict_len);
   uint32_t* rblk = xc ? reinterpret_cast<uint32_t*>(ws + L.xc_rblk) : nullptr;
   uint8_t* offs = xc ? reinterpret_cast<uint8_t*>(ws + L.xc_offs) : nullptr;
@@ -395,7 +392,7 @@ cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, const void*
   if (xc) {
     const uint64_t nsb = xc_nsb(in->dict_len);
     k_xc_records<<<(unsigned)((nsb + 255) / 256), 256, 0, st>>>(rblk, xc_nblk(in->dict_len), nsb,
-                                                                reinterpret_cast<uint4*>(ws + L.xc_rec));
+                                                                reinterpret_cast<uint2*>(ws + L.xc_rec));
     note_launch();
   }
   return cudaGetLastError();

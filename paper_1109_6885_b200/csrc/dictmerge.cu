@@ -39,8 +39,8 @@ int current_device() {
 }
 }  // namespace
 
-void ensure_smem(const void* func) {
-  const FuncKey k{func, current_device(), 0, -1};
+void ensure_smem(const void* func, bool max_carveout) {
+  const FuncKey k{func, current_device(), 0, max_carveout ? -3 : -1};
   std::lock_guard<std::mutex> lk(g_cache_mu);
   if (g_func_cache.count(k)) return;
   int optin = 0;
@@ -48,6 +48,12 @@ void ensure_smem(const void* func) {
   cudaFuncAttributes fa{};
   cudaFuncGetAttributes(&fa, func);
   cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
+  // Full shared-memory carveout on request: otherwise the driver may pick a
+  // smaller split and cap residency (k_merge_write ran 3 CTAs/SM instead of 5,
+  // ncu r01).  Not for the gather kernels: k_recompress's L2 gathers need the
+  // L1 capacity (measured 440 -> 787 us on cfg2 with the full carveout).
+  if (max_carveout)
+    cudaFuncSetAttribute(func, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   g_func_cache[k] = 1;
 }
 
@@ -83,7 +89,12 @@ uint32_t host_width(uint64_t n) {
 }
 uint64_t host_words(uint64_t n, uint32_t bits) { return (n * (uint64_t)bits + 63) / 64; }
 
-static std::atomic<int> g_tuning[4] = {};
+// Knob defaults may come from the environment (DM_XMODE for knob 0; experiments).
+static std::atomic<int> g_tuning[4] = {[] {
+  const char* s = std::getenv("DM_XMODE");
+  const int v = s ? std::atoi(s) : 0;
+  return (v >= 0 && v <= 3) ? v : 0;
+}()};
 int tuning(int knob) { return (knob >= 0 && knob < 4) ? g_tuning[knob].load(std::memory_order_relaxed) : 0; }
 
 int sort_variant() {
@@ -137,7 +148,7 @@ WsLayout ws_layout(const dm_column_in* in) {
   L.xm = take(in->dict_len * 4);
   L.xd = take(nD * 4);
   L.xc_rblk = take((xc_nblk(in->dict_len) + 1) * 4);
-  L.xc_rec = take(xc_nsb(in->dict_len) * 16);
+  L.xc_rec = take(xc_nsb(in->dict_len) * kXcRecBytes);
   L.xc_offs = take(nD + 16);
   L.total = o;
   return L;
@@ -208,7 +219,7 @@ static dm_status merge_async(const dm_column_in* in, const dm_column_out* out, v
   // Step 2(b): M' (Eq 11).
   const bool xc = xc_wanted(in->dict_len);
   if (with_step2 && (e = launch_recompress(in, out, xm, xd, rank, d_header, st, 0,
-                                           xc ? reinterpret_cast<const uint4*>(w + L.xc_rec) : nullptr,
+                                           xc ? reinterpret_cast<const uint2*>(w + L.xc_rec) : nullptr,
                                            xc ? reinterpret_cast<const uint8_t*>(w + L.xc_offs) : nullptr)) !=
                          cudaSuccess)
     return cuda_fail(e);

@@ -26,19 +26,20 @@ constexpr int kRecThreads = 32 * (kRecConsumerWarps + 1);  // + one TMA producer
 constexpr int kRecGroups = 128;                          // 32-row groups per chunk (4096 rows)
 constexpr int kRecStages = 4;                            // TMA input ring depth
 constexpr uint32_t kRecSmemXBytes = 96 * 1024;           // X_M staged in shared memory up to this size
-constexpr int kRecStagesXc = 3;                          // ring depth when the compact X_M takes the smem
+constexpr int kRecStagesXc = 4;                          // ring depth when the compact X_M takes the smem
 
 // Compact translation table "XC": X_M[c] = c + #{new values
 // inserted at or before main position c} (insertion point p of a new value =
-// #U_M below it; it raises X_M[c] for c >= p).  Per 2048-code superblock s one
-// 16-byte record {R, cum[0..3], cum[4..7], flag}: R = #{p <= 2048s}, cum[t] =
-// #{2048s < p <= 2048s + 256(t+1)}; per new value (sorted order) one byte,
-// (p - 1) mod 256.  A
-// superblock whose counts do not fit (> 255, or > kXcMaxBlock in one block) is
-// flagged and its lookups read the plain X_M.
+// #U_M below it; it raises X_M[c] for c >= p).  Per 1024-code superblock s one
+// 8-byte record: word 0 = R = #{p <= 1024s} (bit 31: flag), word 1 = four
+// bytes cum[t] = #{1024s < p <= 1024s + 256(t+1)}; per new value (sorted
+// order) one byte, (p - 1) mod 256.  A superblock whose counts do not fit
+// (> 255, or > kXcMaxBlock in one 256-code block) is flagged and its lookups
+// read the plain X_M.
 constexpr uint32_t kXcBlock = 256;
-constexpr uint32_t kXcSuper = 2048;
+constexpr uint32_t kXcSuper = 1024;
 constexpr uint32_t kXcMaxBlock = 32;
+constexpr uint32_t kXcRecBytes = 8;
 constexpr uint64_t kXcGlobalMinBytes = 64ull << 20;     // plain X_M above this: use XC from L2
 enum XMode { XM_RAW_GLOBAL = 0, XM_RAW_SMEM = 1, XM_XC_SMEM = 2, XM_XC_GLOBAL = 3 };
 // Tuning knobs (dm_set_tuning): index 0 = X_M placement (0 auto, 1 plain only,
@@ -91,7 +92,7 @@ struct WsLayout {
   size_t xm;             // X_M u32[dict_len]
   size_t xd;             // X_D u32[n_delta]
   size_t xc_rblk;        // XC: u32[nblk + 1], new values inserted before each 256-block
-  size_t xc_rec;         // XC: uint4[nsb] superblock records
+  size_t xc_rec;         // XC: uint2[nsb] superblock records
   size_t xc_offs;        // XC: u8[n_delta] insertion position mod 256 per new value
   size_t total;
   uint64_t ntiles_sort, ntiles_unique, ntiles_merge;
@@ -107,7 +108,7 @@ uint64_t host_words(uint64_t n, uint32_t bits);
 // ---- launch bookkeeping (host; cached so a merge issues no per-launch driver queries)
 void note_launch(int n = 1);
 // Raise the dynamic shared memory limit of `func` to the device maximum, once per device.
-void ensure_smem(const void* func);
+void ensure_smem(const void* func, bool max_carveout = false);
 int device_sms();
 int occupancy(const void* func, int threads, size_t smem);
 cudaError_t last_error_check();
@@ -125,7 +126,7 @@ cudaError_t launch_dictionary_merge(const dm_column_in* in, const dm_column_out*
 // xc_rec / xc_offs: the compact table (NULL: plain X_M only).
 cudaError_t launch_recompress(const dm_column_in* in, const dm_column_out* out, const uint32_t* xm,
                               const uint32_t* xd, const uint32_t* rank, dm_header* hdr, cudaStream_t st,
-                              uint32_t fixed_bits = 0, const uint4* xc_rec = nullptr,
+                              uint32_t fixed_bits = 0, const uint2* xc_rec = nullptr,
                               const uint8_t* xc_offs = nullptr);
 cudaError_t launch_pack(const uint32_t* codes, uint64_t n, uint32_t bits, uint64_t* words, cudaStream_t st);
 cudaError_t launch_unpack(const uint64_t* words, uint64_t n, uint32_t bits, uint32_t* codes, cudaStream_t st);

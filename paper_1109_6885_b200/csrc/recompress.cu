@@ -27,6 +27,7 @@
 // specialisations that |U'|'s bounds allow and each exits unless it matches.
 #include <algorithm>
 #include <array>
+#include <cstdlib>
 #include <utility>
 
 #include "dm_device.cuh"
@@ -53,37 +54,49 @@ __device__ __forceinline__ uint32_t warp_pack(uint32_t v, uint32_t nb, uint32_t 
 // Compact X_M lookup (XC, NEXT3; layout in dm_internal.h):
 //   X_M[c] = c + start + #{entries of c's 256-block with offset < c mod 256}
 // where start = R + cum[t-1] = #{new values with insertion point p <= 256g}
-// (g = c's block) and the block's entries are the new values with p in
-// (256g, 256g + 256], stored as (p - 1) mod 256: consecutive bytes
-// [start, end), scanned a word at a time with a SIMD byte compare.  SM: tables in shared memory; else
-// read through L2 (evict-last).  Flagged superblocks use the plain X_M.
-__device__ __forceinline__ uint4 ld_gather_v4(const uint4* p, uint64_t policy) {
-  uint4 v;
-  asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+// (g = c's block) and the block's n entries are the new values with p in
+// (256g, 256g + 256], stored as (p - 1) mod 256: bytes [start, start + n).
+// Branch-free common case: the two words holding bytes [start & ~3, +8) cover
+// the first k = min(n, 8 - start % 4) >= 5 entries, counted with a SIMD byte
+// compare; longer lists (rare: n <= kXcMaxBlock) finish in a loop.  SM: tables
+// in shared memory; else through L2 (evict-last).  Flagged superblocks use the
+// plain X_M.
+__device__ __forceinline__ uint2 ld_gather_v2(const uint2* p, uint64_t policy) {
+  uint2 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;"
+               : "=r"(v.x), "=r"(v.y)
                : "l"(p), "l"(policy));
   return v;
 }
 template <bool SM>
-__device__ __forceinline__ uint32_t xc_lookup(uint32_t code, const uint4* __restrict__ rec,
+__device__ __forceinline__ uint32_t xc_word(const uint32_t* p, uint64_t pol) {
+  return SM ? *p : ld_gather_u32(p, pol);
+}
+template <bool SM>
+__device__ __forceinline__ uint32_t xc_lookup(uint32_t code, const uint2* __restrict__ rec,
                                               const uint32_t* __restrict__ offs32, const uint32_t* __restrict__ XM,
                                               uint64_t pol) {
-  const uint32_t sb = code / kXcSuper, t = (code / kXcBlock) % (kXcSuper / kXcBlock), o = code % kXcBlock;
-  const uint4 r = SM ? rec[sb] : ld_gather_v4(rec + sb, pol);
-  if (r.w) return ld_gather_u32(XM + code, pol);
-  const uint64_t cum = ((uint64_t)r.z << 32) | r.y;
-  const uint32_t start = r.x + (t ? (uint32_t)(cum >> (8 * t - 8)) & 255u : 0u);
-  const uint32_t end = r.x + ((uint32_t)(cum >> (8 * t)) & 255u);
+  const uint32_t sb = code / kXcSuper, t8 = 8 * ((code / kXcBlock) % (kXcSuper / kXcBlock)), o = code % kXcBlock;
+  const uint2 r = SM ? rec[sb] : ld_gather_v2(rec + sb, pol);
+  const bool flagged = r.x >> 31;
+  const uint32_t xm_flagged = flagged ? __ldg(XM + code) : 0u;  // predicated, no divergence
+  const uint32_t s_rel = ((r.y << 8) >> t8) & 255u, e_rel = (r.y >> t8) & 255u;
+  const uint32_t start = (r.x & 0x7fffffffu) + s_rel, n = flagged ? 0u : e_rel - s_rel;
+  const uint32_t wi = start >> 2, sh = 8 * (start & 3u);
+  const uint32_t w0 = xc_word<SM>(offs32 + wi, pol), w1 = xc_word<SM>(offs32 + wi + 1, pol);
+  const uint32_t a = __funnelshift_r(w0, w1, sh), b = w1 >> sh;  // bytes start.., start+4..
+  const uint32_t k = umin32(n, 8u - (start & 3u));
+  const uint32_t ka = umin32(k, 4u);
   const uint32_t ob = o * 0x01010101u;
-  uint32_t cnt = 0;
-  for (uint32_t w = start & ~3u; w < end; w += 4) {
-    const uint32_t v = SM ? offs32[w >> 2] : ld_gather_u32(offs32 + (w >> 2), pol);
-    const uint32_t le = __vcmpltu4(v, ob);  // 0xff in each byte < o
-    const uint32_t lo = start > w ? start - w : 0u, hi = end - w;  // valid bytes [lo, min(hi, 4))
-    const uint32_t vm = shl32(0xffffffffu, 8 * lo) & (hi >= 4 ? 0xffffffffu : shl32(1u, 8 * hi) - 1u);
-    cnt += __popc(le & vm) >> 3;
+  uint32_t cnt = __popc(__vcmpltu4(a, ob) & (shl32(1u, 8 * ka) - 1u)) +
+                 __popc(__vcmpltu4(b, ob) & (shl32(1u, 8 * (k - ka)) - 1u));
+  if (__builtin_expect(n > k, 0)) {
+    for (uint32_t q = start + k; q < start + n; ++q) {  // rare tail (n <= kXcMaxBlock)
+      const uint32_t w = xc_word<SM>(offs32 + (q >> 2), pol);
+      cnt += ((w >> (8 * (q & 3u))) & 255u) < o ? 8u : 0u;
+    }
   }
-  return code + start + cnt;
+  return flagged ? xm_flagged : code + start + (cnt >> 3);
 }
 
 // Warp-specialised: warp kRecConsumerWarps is the TMA producer, warps
@@ -95,18 +108,28 @@ __device__ __forceinline__ uint32_t xc_lookup(uint32_t code, const uint4* __rest
 // modes decide on the device, from |U'|, whether XC fits the shared-memory
 // budget xc_budget: XM_XC_SMEM runs only if it does, its companion
 // (XM_XC_GLOBAL or XM_RAW_GLOBAL launched with xc_budget != 0) only if not.
+template <int XMODE>
+__host__ __device__ constexpr int rec_consumer_warps() { return XMODE == XM_XC_SMEM ? 28 : kRecConsumerWarps; }
+// 32-row groups per chunk: a multiple of 4 (16-byte aligned chunks at any width)
+// and of the consumer warp count
+template <int XMODE>
+__host__ __device__ constexpr int rec_groups() { return XMODE == XM_XC_SMEM ? 112 : kRecGroups; }
+template <int XMODE>
+__host__ __device__ constexpr int rec_threads() { return 32 * (rec_consumer_warps<XMODE>() + 1); }
+
 template <int NB, int XMODE>
-__global__ void __launch_bounds__(kRecThreads) k_recompress(const uint64_t* __restrict__ M, uint64_t n_main, uint32_t b,
+__global__ void __launch_bounds__(rec_threads<XMODE>()) k_recompress(const uint64_t* __restrict__ M, uint64_t n_main, uint32_t b,
                                                             uint64_t dict_len, const uint32_t* __restrict__ XM,
                                                             const uint32_t* __restrict__ XD,
                                                             const uint32_t* __restrict__ rank, uint64_t n_delta,
                                                             uint64_t* __restrict__ Mout, dm_header* hdr,
                                                             uint32_t in_stage_bytes, uint32_t fixed_bits,
-                                                            const uint4* __restrict__ xrec,
-                                                            const uint8_t* __restrict__ xoffs, uint32_t xc_budget) {
-  constexpr int G = kRecGroups;
+                                                            const uint2* __restrict__ xrec,
+                                                            const uint8_t* __restrict__ xoffs, uint32_t xc_budget,
+                                                            int raw_warps) {
+  constexpr int G = rec_groups<XMODE>();
   constexpr int S = XMODE == XM_XC_SMEM ? kRecStagesXc : kRecStages;
-  constexpr int CW = kRecConsumerWarps;
+  constexpr int CW = rec_consumer_warps<XMODE>();
   constexpr int U = G / CW;  // groups per consumer warp per chunk, all in flight together
   constexpr bool XS = XMODE == XM_RAW_SMEM;
   static_assert(G % CW == 0, "groups must split evenly over consumer warps");
@@ -118,7 +141,8 @@ __global__ void __launch_bounds__(kRecThreads) k_recompress(const uint64_t* __re
   if (xc_budget) {
     const uint64_t n_new = hdr->merged_dict_len - dict_len;
     xc_offs_bytes = (n_new + 15) & ~15ull;
-    const bool fits = nsb * 16 + xc_offs_bytes <= xc_budget;
+    // + 16: the two-word read may touch up to 8 bytes past the last entry
+    const bool fits = ((nsb * kXcRecBytes + 15) & ~15ull) + xc_offs_bytes + 16 <= xc_budget;
     if ((XMODE == XM_XC_SMEM) != fits) return;
   }
 
@@ -146,12 +170,15 @@ __global__ void __launch_bounds__(kRecThreads) k_recompress(const uint64_t* __re
   if (XS) {
     for (uint32_t i = threadIdx.x; i < dict_len; i += blockDim.x) sx[i] = __ldg(XM + i);
   }
-  uint4* srec = reinterpret_cast<uint4*>(sx);
-  const uint32_t* soffs = reinterpret_cast<const uint32_t*>(srec + nsb);
+  uint2* srec = reinterpret_cast<uint2*>(sx);
+  const uint64_t rec_pad = (nsb * kXcRecBytes + 15) & ~15ull;
+  const uint32_t* soffs = reinterpret_cast<const uint32_t*>(reinterpret_cast<unsigned char*>(sx) + rec_pad);
   if (XMODE == XM_XC_SMEM) {
-    for (uint64_t i = threadIdx.x; i < nsb; i += blockDim.x) srec[i] = __ldg(xrec + i);
-    uint4* so = srec + nsb;
+    const uint4* src = reinterpret_cast<const uint4*>(xrec);  // records, then the offsets
+    uint4* dst = reinterpret_cast<uint4*>(sx);
+    for (uint64_t i = threadIdx.x; i < rec_pad / 16; i += blockDim.x) dst[i] = __ldg(src + i);
     const uint4* go = reinterpret_cast<const uint4*>(xoffs);
+    uint4* so = dst + rec_pad / 16;
     for (uint64_t i = threadIdx.x; i < xc_offs_bytes / 16; i += blockDim.x) so[i] = __ldg(go + i);
   }
   __syncthreads();
@@ -185,6 +212,10 @@ __global__ void __launch_bounds__(kRecThreads) k_recompress(const uint64_t* __re
   const uint32_t pr0 = (32 * lane) / nb, pop = 32 * lane - pr0 * nb;
   uint32_t* out32 = reinterpret_cast<uint32_t*>(Mout);
   bool bad = false;
+  // XM_XC_SMEM: the first raw_warps consumer warps gather the plain X_M through
+  // L2 (bound by the L1 request pipeline), the others decode XC from shared
+  // memory (bound by instruction issue) -- two different limits run in parallel.
+  const bool raw_warp = (int)warp < raw_warps;
 
   for (uint64_t k = 0;; ++k) {
     const uint64_t c = blockIdx.x + k * gridDim.x;
@@ -194,29 +225,41 @@ __global__ void __launch_bounds__(kRecThreads) k_recompress(const uint64_t* __re
     const uint32_t* sin = reinterpret_cast<const uint32_t*>(in_ring + (size_t)s * in_stage_bytes);
     const uint64_t row_base = c * R;
     uint32_t v[U];
+    auto translate = [&](uint32_t code) -> uint32_t {
+      if (code >= dict_len) {
+        bad = true;
+        code = 0;
+      }
+      if constexpr (XMODE == XM_RAW_SMEM)
+        return sx[code];
+      else if constexpr (XMODE == XM_XC_SMEM)
+        return raw_warp ? ld_gather_u32(XM + code, pol_x) : xc_lookup<true>(code, srec, soffs, XM, pol_x);
+      else if constexpr (XMODE == XM_XC_GLOBAL)
+        return xc_lookup<false>(code, xrec, reinterpret_cast<const uint32_t*>(xoffs), XM, pol_x);
+      else
+        return ld_gather_u32(XM + code, pol_x);
+    };
+    if (row_base + R <= n_main) {
+      // all-main chunk (all but the last one or two): no per-row bounds
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int g = warp + CW * u;
-      const uint64_t row = row_base + (uint64_t)g * 32 + lane;
-      if (row < n_main) {
+      for (int u = 0; u < U; ++u) {
+        const int g = warp + CW * u;
         const uint32_t lo = sin[g * b + uw0], hi = sin[g * b + uw0 + 1];
-        uint32_t code = __funnelshift_r(lo, hi, uo) & umask;
-        if (code >= dict_len) {
-          bad = true;
-          code = 0;
+        v[u] = translate(__funnelshift_r(lo, hi, uo) & umask);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int g = warp + CW * u;
+        const uint64_t row = row_base + (uint64_t)g * 32 + lane;
+        if (row < n_main) {
+          const uint32_t lo = sin[g * b + uw0], hi = sin[g * b + uw0 + 1];
+          v[u] = translate(__funnelshift_r(lo, hi, uo) & umask);
+        } else if (row < n_total) {
+          v[u] = __ldg(XD + __ldg(rank + (row - n_main)));
+        } else {
+          v[u] = 0;
         }
-        if constexpr (XMODE == XM_RAW_SMEM)
-          v[u] = sx[code];
-        else if constexpr (XMODE == XM_XC_SMEM)
-          v[u] = xc_lookup<true>(code, srec, soffs, XM, pol_x);
-        else if constexpr (XMODE == XM_XC_GLOBAL)
-          v[u] = xc_lookup<false>(code, xrec, reinterpret_cast<const uint32_t*>(xoffs), XM, pol_x);
-        else
-          v[u] = ld_gather_u32(XM + code, pol_x);
-      } else if (row < n_total) {
-        v[u] = __ldg(XD + __ldg(rank + (row - n_main)));
-      } else {
-        v[u] = 0;
       }
     }
     __syncwarp();
@@ -261,6 +304,18 @@ __global__ void __launch_bounds__(256) k_unpack(const uint32_t* __restrict__ wor
   }
 }
 
+// Consumer warps of the XC shared-memory kernel that gather the plain X_M
+// instead (DM_XC_RAW_WARPS, experiments).  Default 0: with XC holding ~220 KB
+// of shared memory the L1 is too small for L2 gathers (cfg2: 8 raw warps
+// 0.50 ms, 28 raw warps 0.79 ms, 0 raw warps 0.433 ms).
+static int xc_raw_warps() {
+  static const int v = [] {
+    const char* e = std::getenv("DM_XC_RAW_WARPS");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+
 // Shared-memory bytes left for XC next to a kRecStagesXc-deep ring.
 static uint32_t xc_smem_budget(uint32_t in_stage) {
   static int optin = [] {
@@ -275,18 +330,20 @@ static uint32_t xc_smem_budget(uint32_t in_stage) {
 
 template <int NB>
 cudaError_t launch_nb(const dm_column_in* in, const dm_column_out* out, const uint32_t* xm, const uint32_t* xd,
-                      const uint32_t* rank, dm_header* hdr, cudaStream_t st, uint32_t fixed_bits, const uint4* xrec,
+                      const uint32_t* rank, dm_header* hdr, cudaStream_t st, uint32_t fixed_bits, const uint2* xrec,
                       const uint8_t* xoffs) {
   const uint32_t in_stage = kRecGroups * in->main_bits * 4 + 16;
+  const uint32_t in_stage_xc = rec_groups<XM_XC_SMEM>() * in->main_bits * 4 + 16;
   const int sms = device_sms();
   const uint64_t n_total = in->n_main + in->n_delta;
-  const uint64_t nchunks = (n_total + 32ull * kRecGroups - 1) / (32ull * kRecGroups);
-  auto go = [&](auto kern, size_t smem, uint32_t budget) {
-    const int occ = occupancy((const void*)kern, kRecThreads, smem);
+  auto go = [&](auto kern, size_t smem, uint32_t budget, int threads = kRecThreads, int groups = kRecGroups) {
+    const uint64_t nchunks = (n_total + 32ull * groups - 1) / (32ull * groups);
+    const int occ = occupancy((const void*)kern, threads, smem);
     const unsigned grid = (unsigned)std::min<uint64_t>(nchunks, (uint64_t)sms * occ);
-    kern<<<grid, kRecThreads, smem, st>>>(in->main_codes, in->n_main, in->main_bits, in->dict_len, xm, xd, rank,
-                                          in->n_delta, out->merged_codes, hdr, in_stage, fixed_bits, xrec, xoffs,
-                                          budget);
+    kern<<<grid, threads, smem, st>>>(in->main_codes, in->n_main, in->main_bits, in->dict_len, xm, xd, rank,
+                                          in->n_delta, out->merged_codes, hdr,
+                                          groups == kRecGroups ? in_stage : in_stage_xc, fixed_bits, xrec, xoffs,
+                                          budget, xc_raw_warps());
     note_launch();
   };
   const size_t ring = 128 + (size_t)kRecStages * in_stage;
@@ -306,9 +363,11 @@ cudaError_t launch_nb(const dm_column_in* in, const dm_column_out* out, const ui
     go(k_recompress<NB, XM_RAW_GLOBAL>, ring, 0);
     return cudaGetLastError();
   }
-  const uint32_t budget0 = want_smem ? xc_smem_budget(in_stage) : 0u;
-  const uint32_t budget = (uint64_t)xc_nsb(in->dict_len) * 16 <= budget0 ? budget0 : 0u;
-  if (budget) go(k_recompress<NB, XM_XC_SMEM>, 128 + (size_t)kRecStagesXc * in_stage + budget, budget);
+  const uint32_t budget0 = want_smem ? xc_smem_budget(in_stage_xc) : 0u;
+  const uint32_t budget = (uint64_t)xc_nsb(in->dict_len) * kXcRecBytes + 16 <= budget0 ? budget0 : 0u;
+  if (budget)
+    go(k_recompress<NB, XM_XC_SMEM>, 128 + (size_t)kRecStagesXc * in_stage_xc + budget, budget,
+       rec_threads<XM_XC_SMEM>(), rec_groups<XM_XC_SMEM>());
   const bool xc_l2 = knob == 2 || knob == 3 || in->dict_len * 4 > kXcGlobalMinBytes;
   if (xc_l2)
     go(k_recompress<NB, XM_XC_GLOBAL>, ring, budget);
@@ -318,7 +377,7 @@ cudaError_t launch_nb(const dm_column_in* in, const dm_column_out* out, const ui
 }
 
 using LaunchFn = cudaError_t (*)(const dm_column_in*, const dm_column_out*, const uint32_t*, const uint32_t*,
-                                 const uint32_t*, dm_header*, cudaStream_t, uint32_t, const uint4*, const uint8_t*);
+                                 const uint32_t*, dm_header*, cudaStream_t, uint32_t, const uint2*, const uint8_t*);
 template <int... I>
 constexpr auto make_table(std::integer_sequence<int, I...>) {
   return std::array<LaunchFn, sizeof...(I)>{&launch_nb<I>...};
@@ -328,7 +387,7 @@ constexpr auto make_table(std::integer_sequence<int, I...>) {
 
 cudaError_t launch_recompress(const dm_column_in* in, const dm_column_out* out, const uint32_t* xm,
                               const uint32_t* xd, const uint32_t* rank, dm_header* hdr, cudaStream_t st,
-                              uint32_t fixed_bits, const uint4* xc_rec, const uint8_t* xc_offs) {
+                              uint32_t fixed_bits, const uint2* xc_rec, const uint8_t* xc_offs) {
   if (in->n_main + in->n_delta == 0) return cudaSuccess;
   static const auto table = make_table(std::make_integer_sequence<int, 33>{});  // [0] = runtime width
   if (fixed_bits) return table[fixed_bits](in, out, xm, xd, rank, hdr, st, fixed_bits, nullptr, nullptr);

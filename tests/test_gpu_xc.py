@@ -6,8 +6,8 @@ at or before main position c} (the closed form of X_M; DESIGN.md
 knob (auto / plain X_M / XC with shared-memory preference / XC from L2) and is
 compared element by element with the oracle.  The cases aim at the format's
 edges: insertions before the first and after the last main entry, at 256- and
-2048-code boundaries, blocks with exactly kXcMaxBlock (32) and 33 insertions,
-superblocks with 255 and 256 insertions (byte overflow -> flagged), dictionary
+1024-code boundaries, blocks with exactly kXcMaxBlock (32) and 33 insertions
+(flagged), list lengths 0..12 against the two-word read window, dictionary
 sizes that are and are not multiples of the block sizes, and a new-value count
 too large for shared memory (L2 companion kernel).
 """
@@ -87,22 +87,25 @@ def test_xc_uniform_insertions(key):
 
 
 def test_xc_boundaries_and_overflow():
-    n = 2048 * 40 + 77  # ragged last superblock
-    ins = [(0, 5), (255, 3), (256, 4), (2047, 2), (2048, 6),  # block / superblock edges
-           (2048 * 3 + 10, 32),                                 # exactly kXcMaxBlock in one block
-           (2048 * 5 + 300, 33),                                # one over: superblock flagged
+    n = 1024 * 80 + 77  # ragged last superblock
+    ins = [(0, 5), (1, 2), (255, 3), (256, 4), (257, 1), (1023, 2), (1024, 6), (1025, 1),  # block / superblock edges
+           (1024 * 3 + 10, 32),                                 # exactly kXcMaxBlock in one block
+           (1024 * 5 + 300, 33),                                # one over: superblock flagged
+           (1024 * 6 + 700, 6), (1024 * 6 + 701, 3),            # 9 entries: past the two-word window
            ]
-    # 255 insertions in one superblock, <= 32 per block: fits exactly
-    ins += [(2048 * 7 + 256 * t + 5, 32 if t < 7 else 31) for t in range(8)]
-    # 256 in one superblock (byte overflow -> flagged), spread over its blocks
-    ins += [(2048 * 9 + 256 * t + 7, 32) for t in range(8)]
+    # 128 insertions in one superblock, 32 per block: fits
+    ins += [(1024 * 7 + 256 * t + 5, 32) for t in range(4)]
+    # every list length 0..12 at every start alignment (window edge k = 8 - start % 4)
+    base = 1024 * 20
+    for L in range(13):
+        ins.append((base + 256 * L + 128, L))
     ins += [(n - 1, 9), (n, 11)]                               # before the last entry, after it
-    col = _column(n, 400_000, ins, 5000, seed=2)
+    col = _column(n, 400_000, [x for x in ins if x[1] > 0], 5000, seed=2)
     _run_all_knobs(col)
 
 
 def test_xc_dictionary_multiple_of_superblock_and_tail_inserts():
-    n = 2048 * 64  # 131072: multiple of both block sizes; new values after the last entry
+    n = 1024 * 128  # 131072: multiple of both block sizes; new values after the last entry
     col = _column(n, 300_000, [(n, 40), (n - 256, 3), (1, 1)] + _spread(n, 500, 3), 1000, seed=3)
     _run_all_knobs(col)
 
