@@ -189,7 +189,11 @@ dm_status dm_merge_column_host(dm_ctx* ctx, const dm_column_in* in, dm_column_ou
  *     the plain X_M through L2;
  *   1 plain X_M only;  2 XC, staged in shared memory when it fits, else L2;
  *   3 XC through L2.
- * The process starts with knob 0 = $DM_XMODE if set (0..3), else 0.
+ * knob 1 = Step 1(b) variant: 0 (default) bitmap-slot tiles in two passes
+ *   (count, prefix sum, write: P:302-314); 1 the first GPU form (rank tiles,
+ *   three kernels); 2 bitmap-slot tiles in one pass with decoupled look-back.
+ * The process starts with knob 0 = $DM_XMODE and knob 1 = $DM_MERGE when set
+ * (experiments), else 0.
  * Returns DM_OK, or DM_E_INVALID for an unknown knob or value.  Affects calls
  * made after it returns (a captured CUDA graph keeps the kernels it recorded). */
 int dm_set_tuning(int knob, int value);

@@ -34,6 +34,14 @@ def build_trace() -> str:
     return out
 
 
+def build_check() -> str:
+    """Diagnostic variant with device-side bounds assertions (-DDM_CHECK); load it
+    with DM_LIB_PATH.  Not used by the product path."""
+    out = os.path.join(HERE, "libdictmerge_check.so")
+    subprocess.check_call([NVCC, *FLAGS, "-DDM_CHECK", *sources(), "-o", out])
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return LIB

@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_write(const void* __res
                                                                void* __restrict__ U, uint32_t* __restrict__ XM,
                                                                uint32_t* __restrict__ XD, dm_header* hdr,
                                                                uint32_t* __restrict__ rblk,
-                                                               uint8_t* __restrict__ offs) {
+                                                               uint8_t* __restrict__ offs, uint32_t xs) {
   using K = typename KT::K;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t s_warp[kMergeThreads / 32 + 1];
@@ -301,8 +301,8 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_write(const void* __res
     if (rblk) {
       // XC: R(g) = #{new values with insertion point p <= 256g} = X_M[256g] - 256g,
       // and after the last main entry (the end of the last list).
-      if ((i & (kXcBlock - 1)) == 0) rblk[i / kXcBlock] = (uint32_t)(u - i);
-      if (i == nA - 1) rblk[(nA + kXcBlock - 1) / kXcBlock] = (uint32_t)(u - i);
+      if ((i & ((1u << xs) - 1)) == 0) rblk[i >> xs] = (uint32_t)(u - i);
+      if (i == nA - 1) rblk[(nA + (1u << xs) - 1) >> xs] = (uint32_t)(u - i);
     }
     // strictly increasing U_M over the pairs this tile owns
     if ((a > 0 || tr.has_prev) && !KT::lt(a > 0 ? tr.A_(a - 1) : tr.sk[0], v)) unsorted = true;
@@ -321,11 +321,255 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_write(const void* __res
         // (u - p)-th new value in sorted order.  It raises X_M[c] for c >= p;
         // stored in the list of the block holding p - 1 (blocks own (256g, 256g+256])
         const uint64_t p = tr.i0 + tr.b_q(j);
-        offs[base + o - p] = (uint8_t)((p - 1) & (kXcBlock - 1));
+        offs[base + o - p] = (uint8_t)((p - 1) & ((1u << xs) - 1));
       }
     }
   }
   if (__any_sync(FULL, unsorted) && lane_id() == 0) atomicMin(&hdr->status, (int)DM_E_UNSORTED);
+}
+
+// ------------------------------------------------------------ single-pass merge
+// One merge-path tile per CTA (tiles claimed in order), all of Step 1(b) in one
+// pass: the tile's smaller side S is binary-searched in its larger side G
+// (q = #G before it), which fixes every S element's slot in the tile's share
+// of U'; those slots are set in a 2048-bit bitmap, and the G elements fill the
+// remaining slots in order -- slot p holds G element p - #{S slots < p}, one
+// popcount per element.  The tile's duplicate count (a U_D value equal to a
+// U_M value) is published as soon as it is known and the
+// exclusive count of earlier tiles arrives by decoupled look-back (the GPU
+// form of P:302-308's counts + prefix sum, without the second pass).
+//   small side B (U_D sparse; cfg2, cfg5): q_j = #{A <= B_j}, dup_j = B_j equals
+//       the A before it; E = exclusive scan of dup over B; slot(B_j) = j + q_j - E_j
+//   small side A (U_D dense): l_a = #{B < A_a}; B_l is a dup if it equals A_a;
+//       E over B as above; slot(A_a) = a + l_a - E[l_a]; non-dup B fill the rest
+// MODE 0: single pass (look-back); 1: count pass only (writes cnt[tile]);
+// 2: write pass with the exclusive counts excl[] of k_scan_counts.
+template <class KT, int MODE>
+__global__ void __launch_bounds__(kMergeThreads) k_merge(const void* __restrict__ A, uint64_t nA,
+                                                         const void* __restrict__ B,
+                                                         const uint64_t* __restrict__ part, uint64_t ntiles,
+                                                         uint64_t* status, uint32_t* counter,
+                                                         uint32_t* __restrict__ cnt,
+                                                         const uint64_t* __restrict__ excl,
+                                                         void* __restrict__ U, uint32_t* __restrict__ XM,
+                                                         uint32_t* __restrict__ XD, dm_header* hdr,
+                                                         uint32_t* __restrict__ rblk, uint8_t* __restrict__ offs,
+                                                         uint32_t xs) {
+  using K = typename KT::K;
+  constexpr uint32_t T = kMergeTile, NT = kMergeThreads, IT = kMergeItems, NW = T / 32;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  K* sk = reinterpret_cast<K*>(smem_raw);                      // [0] = A[i0-1], A tile, B tile
+  uint32_t* sq = reinterpret_cast<uint32_t*>(sk + (T + 1));    // per S element: q (or l)
+  uint32_t* se = sq + T;                                       // dup flags over B -> exclusive scan (+1)
+  uint32_t* snd = se + (T + 1);                                // dense case: non-dup B indices
+  __shared__ uint32_t s_bm[NW], s_wpre[NW];
+  __shared__ uint32_t s_warp[NT / 32 + 1];
+  __shared__ uint32_t s_tile;
+  __shared__ uint64_t s_D0;
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+
+  if (MODE == 0 && threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
+  for (uint32_t w = threadIdx.x; w < NW; w += NT) s_bm[w] = 0;
+  __syncthreads();
+  const uint64_t tile = MODE == 0 ? (uint64_t)s_tile : (uint64_t)blockIdx.x;
+  const uint64_t nB = hdr->delta_dict_len, total = nA + nB;
+  // the grid is sized from N_D >= |U_D|: surplus CTAs claim the last ids, after
+  // every real tile, so nothing waits on them
+  const uint64_t nreal = (total + T - 1) / T;
+  if (tile >= nreal) {
+    if (MODE == 1 && threadIdx.x == 0) cnt[tile] = 0;
+    return;
+  }
+  const uint64_t d0 = tile * T, d1 = umin64(d0 + T, total);
+  const uint64_t i0 = part[tile], i1 = part[tile + 1], j0 = d0 - i0;
+  const uint32_t na = (uint32_t)(i1 - i0), nb = (uint32_t)((d1 - i1) - j0);
+  DM_ASSERT(tile < ntiles && nreal <= ntiles && i1 >= i0 && i1 <= nA && d1 >= i1 + j0 && na + nb <= T && j0 + nb <= nB,
+            "tile %llu i0 %llu i1 %llu j0 %llu na %u nb %u nA %llu nB %llu", (unsigned long long)tile,
+            (unsigned long long)i0, (unsigned long long)i1, (unsigned long long)j0, na, nb, (unsigned long long)nA,
+            (unsigned long long)nB);
+  const bool has_prev = i0 > 0;
+  auto A_ = [&](uint32_t a) -> K { return sk[1 + a]; };
+  auto B_ = [&](uint32_t j) -> K { return sk[1 + na + j]; };
+  {
+    K v[IT];
+#pragma unroll
+    for (int r = 0; r < IT; ++r) {
+      const uint32_t k = threadIdx.x + r * NT;
+      const bool in_a = k < na || nb == 0;
+      v[r] = (na + nb == 0) ? K{} : in_a ? KT::load(A, i0 + umin32(k, na - 1)) : KT::load(B, j0 + umin32(k - na, nb - 1));
+    }
+    if (threadIdx.x == 0 && has_prev) sk[0] = KT::load(A, i0 - 1);
+#pragma unroll
+    for (int r = 0; r < IT; ++r) {
+      const uint32_t k = threadIdx.x + r * NT;
+      if (k < na + nb) sk[1 + k] = v[r];
+    }
+  }
+  for (uint32_t k = threadIdx.x; k <= nb; k += NT) se[k] = 0;
+  __syncthreads();
+  const bool small_b = nb <= na;
+  if (small_b) {
+    for (uint32_t j = threadIdx.x; j < nb; j += NT) {
+      const K v = B_(j);
+      uint32_t lo = 0, hi = na;  // upper bound: #{A <= v}
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (KT::le(A_(mid), v)) lo = mid + 1; else hi = mid;
+      }
+      sq[j] = lo;
+      se[j] = lo > 0 ? KT::eq(A_(lo - 1), v) : (has_prev && KT::eq(sk[0], v));
+    }
+  } else {
+    for (uint32_t a = threadIdx.x; a < na; a += NT) {
+      const K v = A_(a);
+      uint32_t lo = 0, hi = nb;  // lower bound: #{B < v}
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (KT::lt(B_(mid), v)) lo = mid + 1; else hi = mid;
+      }
+      sq[a] = lo;
+      if (lo < nb && KT::eq(B_(lo), v)) se[lo] = 1;
+    }
+    if (threadIdx.x == 0 && has_prev && nb > 0 && KT::eq(B_(0), sk[0])) se[0] = 1;
+  }
+  __syncthreads();
+  // exclusive scan of the dup flags over B (blocked, IT per thread); se[nb] = total
+  {
+    const uint32_t b0 = umin32(threadIdx.x * IT, nb), b1 = umin32(b0 + IT, nb);
+    uint32_t f[IT], sum = 0;
+#pragma unroll
+    for (int r = 0; r < IT; ++r) {
+      f[r] = b0 + r < b1 ? se[b0 + r] : 0u;
+      sum += f[r];
+    }
+    uint32_t tot;
+    uint32_t run = block_exclusive_scan<NT>(sum, s_warp, tot);
+#pragma unroll
+    for (int r = 0; r < IT; ++r) {
+      if (b0 + r < b1) se[b0 + r] = run;
+      run += f[r];
+    }
+    if (threadIdx.x == 0) se[nb] = tot;
+  }
+  __syncthreads();
+  const uint32_t dups = se[nb];
+  if constexpr (MODE == 1) {
+    if (threadIdx.x == 0) cnt[tile] = dups;
+    return;
+  }
+  if (MODE == 0 && warp == 0) {
+    const uint64_t e = lookback_exclusive(status, tile, dups);
+    if (lane == 0) s_D0 = e;
+  }
+  if (MODE == 2 && threadIdx.x == 0) s_D0 = excl[tile];
+  // meanwhile: the small side's slots into the bitmap (independent of D0)
+  if (small_b) {
+    for (uint32_t j = threadIdx.x; j < nb; j += NT) {
+      if (se[j + 1] == se[j]) {
+        const uint32_t slot = j + sq[j] - se[j];
+        atomicOr(&s_bm[slot >> 5], 1u << (slot & 31));
+      }
+    }
+  } else {
+    for (uint32_t a = threadIdx.x; a < na; a += NT) {
+      const uint32_t l = sq[a], slot = a + l - se[l];
+      atomicOr(&s_bm[slot >> 5], 1u << (slot & 31));
+    }
+    for (uint32_t j = threadIdx.x; j < nb; j += NT)
+      if (se[j + 1] == se[j]) snd[j - se[j]] = j;
+  }
+  __syncthreads();
+  if (warp == 1 || (NT == 32)) {  // word prefix of the bitmap (NW = 64 words, 2 per lane)
+    const uint32_t c0 = __popc(s_bm[2 * lane]), c1 = __popc(s_bm[2 * lane + 1]);
+    uint32_t x = c0 + c1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, x, o);
+      if (lane >= (unsigned)o) x += y;
+    }
+    s_wpre[2 * lane] = x - c0 - c1;
+    s_wpre[2 * lane + 1] = x - c1;
+  }
+  __syncthreads();
+  const uint64_t D0 = s_D0;
+  const uint64_t base = d0 - D0;  // U' index of the tile's first slot
+  const uint32_t nU = na + nb - dups;
+  DM_ASSERT(D0 <= j0 && dups <= nb, "tile %llu D0 %llu j0 %llu dups %u nb %u", (unsigned long long)tile,
+            (unsigned long long)D0, (unsigned long long)j0, dups, nb);
+  const unsigned lt = lanemask_lt();
+  bool unsorted = false;
+  // fill: slot p not taken by S holds the (p - #S slots before p)-th G element
+#pragma unroll
+  for (int r = 0; r < IT; ++r) {
+    const uint32_t p = r * NT + threadIdx.x;
+    if (p >= nU) break;
+    const uint32_t bits = s_bm[p >> 5];
+    if ((bits >> lane) & 1u) continue;
+    const uint32_t before = s_wpre[p >> 5] + __popc(bits & lt);  // S slots before p
+    const uint32_t g = p - before;
+    const uint64_t u = base + p;
+    DM_ASSERT(small_b ? g < na : g < nb - dups, "fill tile %llu p %u g %u na %u nb %u dups %u small %d",
+              (unsigned long long)tile, p, g, na, nb, dups, (int)small_b);
+    if (small_b) {
+      const K v = A_(g);
+      const uint64_t i = i0 + g;
+      KT::store(U, u, v);
+      XM[i] = (uint32_t)u;
+      if (rblk) {
+        if ((i & ((1u << xs) - 1)) == 0) rblk[i >> xs] = (uint32_t)(u - i);
+        if (i == nA - 1) rblk[(nA + (1u << xs) - 1) >> xs] = (uint32_t)(u - i);
+      }
+      if ((g > 0 || has_prev) && !KT::lt(g > 0 ? A_(g - 1) : sk[0], v)) unsorted = true;
+    } else {
+      const uint32_t j = snd[g];
+      KT::store(U, u, B_(j));
+      XD[j0 + j] = (uint32_t)u;
+      if (offs) {
+        const uint64_t P = i0 + before;  // U_M entries below this new value
+        offs[u - P] = (uint8_t)((P - 1) & ((1u << xs) - 1));
+      }
+    }
+  }
+  // the small side
+  if (small_b) {
+    for (uint32_t j = threadIdx.x; j < nb; j += NT) {
+      const uint32_t e = se[j];
+      if (se[j + 1] != e) {
+        XD[j0 + j] = (uint32_t)(base + sq[j] - 1 + (j - e));  // its U_M twin's slot
+      } else {
+        const uint32_t slot = j + sq[j] - e;
+        const uint64_t u = base + slot;
+        KT::store(U, u, B_(j));
+        XD[j0 + j] = (uint32_t)u;
+        if (offs) {
+          const uint64_t P = i0 + sq[j];
+          offs[u - P] = (uint8_t)((P - 1) & ((1u << xs) - 1));
+        }
+      }
+    }
+  } else {
+    for (uint32_t a = threadIdx.x; a < na; a += NT) {
+      const uint32_t l = sq[a], slot = a + l - se[l];
+      const uint64_t u = base + slot, i = i0 + a;
+      const K v = A_(a);
+      KT::store(U, u, v);
+      XM[i] = (uint32_t)u;
+      if (l < nb && se[l + 1] != se[l] && KT::eq(B_(l), v)) XD[j0 + l] = (uint32_t)u;
+      if (rblk) {
+        if ((i & ((1u << xs) - 1)) == 0) rblk[i >> xs] = (uint32_t)(u - i);
+        if (i == nA - 1) rblk[(nA + (1u << xs) - 1) >> xs] = (uint32_t)(u - i);
+      }
+      if ((a > 0 || has_prev) && !KT::lt(a > 0 ? A_(a - 1) : sk[0], v)) unsorted = true;
+    }
+    if (threadIdx.x == 0 && has_prev && nb > 0 && KT::eq(B_(0), sk[0])) XD[j0] = (uint32_t)(base - 1);
+  }
+  if (__any_sync(FULL, unsorted) && lane == 0) atomicMin(&hdr->status, (int)DM_E_UNSORTED);
+  if (tile == nreal - 1 && threadIdx.x == 0) {
+    const uint64_t m = total - (D0 + dups);
+    hdr->merged_dict_len = m;
+    hdr->merged_bits = dev_width(m);
+    if (m > (1ull << 32)) atomicMin(&hdr->status, (int)DM_E_TOO_WIDE);
+  }
 }
 
 // XC superblock records (NEXT3) from the block samples R(g) = rblk[g]:
@@ -337,7 +581,7 @@ __global__ void __launch_bounds__(256) k_xc_records(const uint32_t* __restrict__
                                                     uint2* __restrict__ rec) {
   const uint64_t sb = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (sb >= nsb) return;
-  constexpr uint32_t BPS = kXcSuper / kXcBlock;
+  constexpr uint32_t BPS = 4;
   const uint64_t g0 = sb * BPS;
   const uint32_t R0 = rblk[g0];
   uint32_t prev = 0, cum = 0, flag = R0 >> 31;
@@ -370,6 +614,35 @@ cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, const void*
   }
   const uint64_t nt = L.ntiles_merge;
   uint64_t* part = reinterpret_cast<uint64_t*>(ws + L.part);
+  const bool xc = xc_wanted(in->dict_len);
+  uint32_t* rblk = xc ? reinterpret_cast<uint32_t*>(ws + L.xc_rblk) : nullptr;
+  uint8_t* offs = xc ? reinterpret_cast<uint8_t*>(ws + L.xc_offs) : nullptr;
+  const uint32_t xs = xc_shift(in);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(ws + L.mcount);
+  uint64_t* excl = reinterpret_cast<uint64_t*>(ws + L.mexcl);
+  uint64_t* status = reinterpret_cast<uint64_t*>(ws + L.status_merge);
+  uint32_t* counter = reinterpret_cast<uint32_t*>(ws + L.counters) + CNT_MERGE;
+  const int variant = tuning(1);
+  if (variant == 0 || variant == 2) {  // lean tiles: two passes (default) or single pass
+    k_partition<KT><<<(unsigned)((nt + 1 + 7) / 8), 256, 0, st>>>(in->main_dict, in->dict_len, udict, hdr, nt + 1,
+                                                                     part);
+    const size_t smem = sizeof(K) * (kMergeTile + 1) + sizeof(uint32_t) * (3 * kMergeTile + 1);
+    auto go = [&](auto kern) {
+      ensure_smem((const void*)kern, true);
+      kern<<<(unsigned)nt, kMergeThreads, smem, st>>>(in->main_dict, in->dict_len, udict, part, nt, status, counter,
+                                                      cnt, excl, U, xm, xd, hdr, rblk, offs, xs);
+    };
+    if (variant == 2) {
+      go(k_merge<KT, 0>);
+      note_launch(2);
+    } else {
+      go(k_merge<KT, 1>);
+      k_scan_counts<<<(unsigned)((nt + 2047) / 2048), 256, 0, st>>>(cnt, nt, excl, status, counter, in->dict_len,
+                                                                    hdr);
+      go(k_merge<KT, 2>);
+      note_launch(4);
+    }
+  } else {
   uint32_t* cnt = reinterpret_cast<uint32_t*>(ws + L.mcount);
   uint64_t* excl = reinterpret_cast<uint64_t*>(ws + L.mexcl);
   k_partition<KT><<<(unsigned)((nt + 1 + 7) / 8), 256, 0, st>>>(in->main_dict, in->dict_len, udict, hdr, nt + 1,
@@ -383,15 +656,13 @@ cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, const void*
       reinterpret_cast<uint32_t*>(ws + L.counters) + CNT_MERGE, in->dict_len, hdr);
   const size_t smem_write = smem_count;
   ensure_smem((const void*)k_merge_write<KT>, true);
-  const bool xc = xc_wanted(in->dict_len);
-  uint32_t* rblk = xc ? reinterpret_cast<uint32_t*>(ws + L.xc_rblk) : nullptr;
-  uint8_t* offs = xc ? reinterpret_cast<uint8_t*>(ws + L.xc_offs) : nullptr;
   k_merge_write<KT><<<(unsigned)nt, kMergeThreads, smem_write, st>>>(in->main_dict, in->dict_len, udict, part, excl,
-                                                                     U, xm, xd, hdr, rblk, offs);
+                                                                     U, xm, xd, hdr, rblk, offs, xs);
   note_launch(4);
+  }
   if (xc) {
-    const uint64_t nsb = xc_nsb(in->dict_len);
-    k_xc_records<<<(unsigned)((nsb + 255) / 256), 256, 0, st>>>(rblk, xc_nblk(in->dict_len), nsb,
+    const uint64_t nsb = xc_nsb(in->dict_len, xs);
+    k_xc_records<<<(unsigned)((nsb + 255) / 256), 256, 0, st>>>(rblk, xc_nblk(in->dict_len, xs), nsb,
                                                                 reinterpret_cast<uint2*>(ws + L.xc_rec));
     note_launch();
   }

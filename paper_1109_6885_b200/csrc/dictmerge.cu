@@ -5,6 +5,8 @@
 // dict_merge.cu and recompress.cu; this file only plans and launches.
 #include <algorithm>
 #include <atomic>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -90,11 +92,12 @@ uint32_t host_width(uint64_t n) {
 uint64_t host_words(uint64_t n, uint32_t bits) { return (n * (uint64_t)bits + 63) / 64; }
 
 // Knob defaults may come from the environment (DM_XMODE for knob 0; experiments).
-static std::atomic<int> g_tuning[4] = {[] {
-  const char* s = std::getenv("DM_XMODE");
+static int env_knob(const char* name, int hi) {
+  const char* s = std::getenv(name);
   const int v = s ? std::atoi(s) : 0;
-  return (v >= 0 && v <= 3) ? v : 0;
-}()};
+  return (v >= 0 && v <= hi) ? v : 0;
+}
+static std::atomic<int> g_tuning[4] = {env_knob("DM_XMODE", 3), env_knob("DM_MERGE", 2)};
 int tuning(int knob) { return (knob >= 0 && knob < 4) ? g_tuning[knob].load(std::memory_order_relaxed) : 0; }
 
 int sort_variant() {
@@ -133,7 +136,7 @@ WsLayout ws_layout(const dm_column_in* in) {
   L.hist = take(16 * 256 * sizeof(uint32_t));
   L.status_sort = take((size_t)L.npass * L.ntiles_sort * 256 * sizeof(uint32_t));
   L.status_unique = take(L.ntiles_unique * sizeof(uint64_t));
-  L.status_merge = take(((L.ntiles_merge + 2047) / 2048 + 1) * sizeof(uint64_t));
+  L.status_merge = take((L.ntiles_merge + 1) * sizeof(uint64_t));  // per tile (single-pass look-back)
   L.zero_bytes = o;
   L.plan = take(sizeof(SortPlan));
   L.keys0 = take(nD * E);
@@ -147,8 +150,8 @@ WsLayout ws_layout(const dm_column_in* in) {
   L.mexcl = take(L.ntiles_merge * sizeof(uint64_t));
   L.xm = take(in->dict_len * 4);
   L.xd = take(nD * 4);
-  L.xc_rblk = take((xc_nblk(in->dict_len) + 1) * 4);
-  L.xc_rec = take(xc_nsb(in->dict_len) * kXcRecBytes);
+  L.xc_rblk = take((xc_nblk(in->dict_len, kXcMinShift) + 1) * 4);  // sized for the smallest blocks
+  L.xc_rec = take(xc_nsb(in->dict_len, kXcMinShift) * kXcRecBytes);
   L.xc_offs = take(nD + 16);
   L.total = o;
   return L;
@@ -210,17 +213,28 @@ static dm_status merge_async(const dm_column_in* in, const dm_column_out* out, v
   uint32_t* rank = out->delta_rank ? out->delta_rank : reinterpret_cast<uint32_t*>(w + L.rank);
   uint32_t* xm = out->x_main ? out->x_main : reinterpret_cast<uint32_t*>(w + L.xm);
   uint32_t* xd = out->x_delta ? out->x_delta : reinterpret_cast<uint32_t*>(w + L.xd);
+  // DM_SYNC_DEBUG=1: synchronise after each step and report which one faulted (debugging only)
+  static const bool sync_debug = std::getenv("DM_SYNC_DEBUG") != nullptr;
+  auto dbg = [&](const char* step) -> cudaError_t {
+    if (!sync_debug) return cudaSuccess;
+    cudaError_t x = cudaStreamSynchronize(st);
+    if (x != cudaSuccess) fprintf(stderr, "dictmerge: %s failed: %s\n", step, cudaGetErrorString(x));
+    return x;
+  };
   // Step 1(a): delta dictionary U_D and ranks r.
   if ((e = launch_delta_dictionary(in, w, L, udict, rank, d_header, st)) != cudaSuccess) return cuda_fail(e);
+  if ((e = dbg("step 1(a)")) != cudaSuccess) return cuda_fail(e);
   mark(1);
   // Step 1(b) + 2(a): U', X_M, X_D, b' (Eq 4).
   if ((e = launch_dictionary_merge(in, out, w, L, udict, xm, xd, d_header, st)) != cudaSuccess) return cuda_fail(e);
+  if ((e = dbg("step 1(b)")) != cudaSuccess) return cuda_fail(e);
   mark(2);
   // Step 2(b): M' (Eq 11).
   const bool xc = xc_wanted(in->dict_len);
   if (with_step2 && (e = launch_recompress(in, out, xm, xd, rank, d_header, st, 0,
                                            xc ? reinterpret_cast<const uint2*>(w + L.xc_rec) : nullptr,
-                                           xc ? reinterpret_cast<const uint8_t*>(w + L.xc_offs) : nullptr)) !=
+                                           xc ? reinterpret_cast<const uint8_t*>(w + L.xc_offs) : nullptr,
+                                           xc_shift(in))) !=
                          cudaSuccess)
     return cuda_fail(e);
   mark(3);
@@ -286,7 +300,7 @@ struct dm_ctx {
 extern "C" {
 
 int dm_set_tuning(int knob, int value) {
-  if (knob != 0 || value < 0 || value > 3) return DM_E_INVALID;
+  if (knob < 0 || knob > 1 || value < 0 || value > (knob == 0 ? 3 : 2)) return DM_E_INVALID;
   g_tuning[knob].store(value);
   return DM_OK;
 }

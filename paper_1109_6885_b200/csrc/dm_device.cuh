@@ -14,6 +14,25 @@
 #error "dictmerge is written for sm_100a (B200) only"
 #endif
 
+// DM_CHECK builds (debugging only, see build.build_check): device-side bounds
+// assertions that print and trap.
+#ifdef DM_CHECK
+#include <cstdio>
+#define DM_ASSERT(cond, ...)                                                    \
+  do {                                                                          \
+    if (!(cond)) {                                                              \
+      printf("DM_ASSERT %s:%d block %d thread %d: ", __FILE__, __LINE__, (int)blockIdx.x, (int)threadIdx.x); \
+      printf(__VA_ARGS__);                                                      \
+      printf("\n");                                                             \
+      __trap();                                                                 \
+    }                                                                           \
+  } while (0)
+#else
+#define DM_ASSERT(cond, ...) \
+  do {                       \
+  } while (0)
+#endif
+
 namespace dm {
 
 constexpr unsigned FULL = 0xffffffffu;

@@ -30,29 +30,36 @@ constexpr int kRecStagesXc = 4;                          // ring depth when the 
 
 // Compact translation table "XC": X_M[c] = c + #{new values
 // inserted at or before main position c} (insertion point p of a new value =
-// #U_M below it; it raises X_M[c] for c >= p).  Per 1024-code superblock s one
-// 8-byte record: word 0 = R = #{p <= 1024s} (bit 31: flag), word 1 = four
-// bytes cum[t] = #{1024s < p <= 1024s + 256(t+1)}; per new value (sorted
-// order) one byte, (p - 1) mod 256.  A superblock whose counts do not fit
-// (> 255, or > kXcMaxBlock in one 256-code block) is flagged and its lookups
-// read the plain X_M.
-constexpr uint32_t kXcBlock = 256;
-constexpr uint32_t kXcSuper = 1024;
+// #U_M below it; it raises X_M[c] for c >= p).  Blocks of 2^xs codes (xs = 7 or
+// 8, chosen per column from N_D / |U_M| so a block holds a few entries), four
+// blocks per superblock s, one 8-byte record per superblock: word 0 = R =
+// #{p <= 4s 2^xs} (bit 31: flag), word 1 = four bytes cum[t] = #{p in the
+// superblock's first t+1 blocks, (4s 2^xs, ...]}; per new value (sorted order)
+// one byte, (p - 1) mod 2^xs.  A superblock whose counts do not fit (> 255, or
+// > kXcMaxBlock in one block) is flagged and its lookups read the plain X_M.
 constexpr uint32_t kXcMaxBlock = 32;
 constexpr uint32_t kXcRecBytes = 8;
+constexpr uint32_t kXcMinShift = 7;
 constexpr uint64_t kXcGlobalMinBytes = 64ull << 20;     // plain X_M above this: use XC from L2
+inline uint64_t xc_nblk(uint64_t dict_len, uint32_t xs) { return (dict_len + (1ull << xs) - 1) >> xs; }
+inline uint64_t xc_nsb(uint64_t dict_len, uint32_t xs) { return (dict_len + (4ull << xs) - 1) >> (xs + 2); }
 enum XMode { XM_RAW_GLOBAL = 0, XM_RAW_SMEM = 1, XM_XC_SMEM = 2, XM_XC_GLOBAL = 3 };
 // Tuning knobs (dm_set_tuning): index 0 = X_M placement (0 auto, 1 plain only,
-// 2 compact (smem if it fits, else L2), 3 compact from L2).
+// 2 compact (smem if it fits, else L2), 3 compact from L2); index 1 = Step 1(b)
+// variant (0 lean two-pass, 1 first three-phase form, 2 lean single pass).
 int tuning(int knob);
-inline uint64_t xc_nblk(uint64_t dict_len) { return (dict_len + kXcBlock - 1) / kXcBlock; }
-inline uint64_t xc_nsb(uint64_t dict_len) { return (dict_len + kXcSuper - 1) / kXcSuper; }
 // Whether a merge builds XC at all: only when the plain X_M is too big for smem.
 inline bool xc_enabled(uint64_t dict_len) { return dict_len * 4 > kRecSmemXBytes; }
 // Whether this merge builds XC: auto only when the plain X_M exceeds kXcGlobalMinBytes.
 inline bool xc_wanted(uint64_t dict_len) {
   const int k = tuning(0);
   return k == 1 ? false : k == 0 ? dict_len * 4 > kXcGlobalMinBytes : xc_enabled(dict_len);
+}
+// Block shift: 256-code blocks when N_D / |U_M| promises <= 6 entries per block
+// (and always for the shared-memory variant, knob 2), else 128-code blocks.
+inline uint32_t xc_shift(const dm_column_in* in) {
+  if (tuning(0) == 2) return 8;
+  return in->n_delta * 256 <= 6 * in->dict_len ? 8u : 7u;
 }
 
 constexpr uint32_t kRadixFlagAgg = 1u << 30;
@@ -127,7 +134,7 @@ cudaError_t launch_dictionary_merge(const dm_column_in* in, const dm_column_out*
 cudaError_t launch_recompress(const dm_column_in* in, const dm_column_out* out, const uint32_t* xm,
                               const uint32_t* xd, const uint32_t* rank, dm_header* hdr, cudaStream_t st,
                               uint32_t fixed_bits = 0, const uint2* xc_rec = nullptr,
-                              const uint8_t* xc_offs = nullptr);
+                              const uint8_t* xc_offs = nullptr, uint32_t xc_shift = 8);
 cudaError_t launch_pack(const uint32_t* codes, uint64_t n, uint32_t bits, uint64_t* words, cudaStream_t st);
 cudaError_t launch_unpack(const uint64_t* words, uint64_t n, uint32_t bits, uint32_t* codes, cudaStream_t st);
 

@@ -72,24 +72,54 @@ template <bool SM>
 __device__ __forceinline__ uint32_t xc_word(const uint32_t* p, uint64_t pol) {
   return SM ? *p : ld_gather_u32(p, pol);
 }
+__device__ __forceinline__ uint4 ld_gather_v4(const uint4* p, uint64_t policy) {
+  uint4 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p), "l"(policy));
+  return v;
+}
+// #{bytes b of word w at window positions [4i, 4i+4) with lo <= pos < hi and b < o}, x8
+__device__ __forceinline__ uint32_t count_lt(uint32_t w, uint32_t ob, int i, uint32_t lo, uint32_t hi) {
+  const uint32_t a = lo > 4u * i ? lo - 4u * i : 0u, z = hi > 4u * i ? hi - 4u * i : 0u;  // byte range [a, z)
+  const uint32_t m = shl32(0xffffffffu, 8 * a) & (z >= 4 ? 0xffffffffu : shl32(1u, 8 * z) - 1u);
+  return __popc(__vcmpltu4(w, ob) & m);
+}
+// xs: block shift (blocks of 2^xs codes, superblocks of 4 blocks).
 template <bool SM>
-__device__ __forceinline__ uint32_t xc_lookup(uint32_t code, const uint2* __restrict__ rec,
+__device__ __forceinline__ uint32_t xc_lookup(uint32_t code, uint32_t xs, const uint2* __restrict__ rec,
                                               const uint32_t* __restrict__ offs32, const uint32_t* __restrict__ XM,
                                               uint64_t pol) {
-  const uint32_t sb = code / kXcSuper, t8 = 8 * ((code / kXcBlock) % (kXcSuper / kXcBlock)), o = code % kXcBlock;
+  const uint32_t sb = code >> (xs + 2), t8 = 8 * ((code >> xs) & 3u), o = code & ((1u << xs) - 1u);
   const uint2 r = SM ? rec[sb] : ld_gather_v2(rec + sb, pol);
   const bool flagged = r.x >> 31;
   const uint32_t xm_flagged = flagged ? __ldg(XM + code) : 0u;  // predicated, no divergence
   const uint32_t s_rel = ((r.y << 8) >> t8) & 255u, e_rel = (r.y >> t8) & 255u;
   const uint32_t start = (r.x & 0x7fffffffu) + s_rel, n = flagged ? 0u : e_rel - s_rel;
-  const uint32_t wi = start >> 2, sh = 8 * (start & 3u);
-  const uint32_t w0 = xc_word<SM>(offs32 + wi, pol), w1 = xc_word<SM>(offs32 + wi + 1, pol);
-  const uint32_t a = __funnelshift_r(w0, w1, sh), b = w1 >> sh;  // bytes start.., start+4..
-  const uint32_t k = umin32(n, 8u - (start & 3u));
-  const uint32_t ka = umin32(k, 4u);
   const uint32_t ob = o * 0x01010101u;
-  uint32_t cnt = __popc(__vcmpltu4(a, ob) & (shl32(1u, 8 * ka) - 1u)) +
-                 __popc(__vcmpltu4(b, ob) & (shl32(1u, 8 * (k - ka)) - 1u));
+  uint32_t cnt, k;
+  if constexpr (SM) {
+    // shared memory: the two words holding bytes [start & ~3, +8)
+    const uint32_t wi = start >> 2, sh = 8 * (start & 3u);
+    const uint32_t w0 = offs32[wi], w1 = offs32[wi + 1];
+    const uint32_t a = __funnelshift_r(w0, w1, sh), b = w1 >> sh;  // bytes start.., start+4..
+    k = umin32(n, 8u - (start & 3u));
+    const uint32_t ka = umin32(k, 4u);
+    cnt = __popc(__vcmpltu4(a, ob) & (shl32(1u, 8 * ka) - 1u)) +
+          __popc(__vcmpltu4(b, ob) & (shl32(1u, 8 * (k - ka)) - 1u));
+  } else {
+    // L2: the aligned 16-byte window holding start, and (predicated, issued
+    // together, no dependent round trip) the next one when the list crosses it
+    const uint32_t s0 = start & 15u;
+    const uint4* base4 = reinterpret_cast<const uint4*>(offs32) + (start >> 4);
+    const uint4 v = ld_gather_v4(base4, pol);
+    const uint4 w = s0 + n > 16u ? ld_gather_v4(base4 + 1, pol) : make_uint4(0, 0, 0, 0);
+    k = umin32(n, 32u - s0);
+    const uint32_t e0 = s0 + k;
+    cnt = count_lt(v.x, ob, 0, s0, e0) + count_lt(v.y, ob, 1, s0, e0) + count_lt(v.z, ob, 2, s0, e0) +
+          count_lt(v.w, ob, 3, s0, e0) + count_lt(w.x, ob, 4, s0, e0) + count_lt(w.y, ob, 5, s0, e0) +
+          count_lt(w.z, ob, 6, s0, e0) + count_lt(w.w, ob, 7, s0, e0);
+  }
   if (__builtin_expect(n > k, 0)) {
     for (uint32_t q = start + k; q < start + n; ++q) {  // rare tail (n <= kXcMaxBlock)
       const uint32_t w = xc_word<SM>(offs32 + (q >> 2), pol);
@@ -99,15 +129,6 @@ __device__ __forceinline__ uint32_t xc_lookup(uint32_t code, const uint2* __rest
   return flagged ? xm_flagged : code + start + (cnt >> 3);
 }
 
-// Warp-specialised: warp kRecConsumerWarps is the TMA producer, warps
-// 0..kRecConsumerWarps-1 consume.  full[s] completes when stage s holds its
-// chunk's main words; empty[s] completes when every consumer warp is done with
-// stage s.  No CTA-wide barrier after the prologue.  XS: X_M staged in shared
-// memory (tables up to kRecSmemXBytes), else gathered through L2.
-// XMODE (XMode): where the main-code translation comes from.  The compact
-// modes decide on the device, from |U'|, whether XC fits the shared-memory
-// budget xc_budget: XM_XC_SMEM runs only if it does, its companion
-// (XM_XC_GLOBAL or XM_RAW_GLOBAL launched with xc_budget != 0) only if not.
 template <int XMODE>
 __host__ __device__ constexpr int rec_consumer_warps() { return XMODE == XM_XC_SMEM ? 28 : kRecConsumerWarps; }
 // 32-row groups per chunk: a multiple of 4 (16-byte aligned chunks at any width)
@@ -118,7 +139,7 @@ template <int XMODE>
 __host__ __device__ constexpr int rec_threads() { return 32 * (rec_consumer_warps<XMODE>() + 1); }
 
 template <int NB, int XMODE>
-__global__ void __launch_bounds__(rec_threads<XMODE>()) k_recompress(const uint64_t* __restrict__ M, uint64_t n_main, uint32_t b,
+__global__ void __launch_bounds__(rec_threads<XMODE>(), XMODE == XM_XC_SMEM ? 1 : 2) k_recompress(const uint64_t* __restrict__ M, uint64_t n_main, uint32_t b,
                                                             uint64_t dict_len, const uint32_t* __restrict__ XM,
                                                             const uint32_t* __restrict__ XD,
                                                             const uint32_t* __restrict__ rank, uint64_t n_delta,
@@ -126,7 +147,7 @@ __global__ void __launch_bounds__(rec_threads<XMODE>()) k_recompress(const uint6
                                                             uint32_t in_stage_bytes, uint32_t fixed_bits,
                                                             const uint2* __restrict__ xrec,
                                                             const uint8_t* __restrict__ xoffs, uint32_t xc_budget,
-                                                            int raw_warps) {
+                                                            int raw_warps, uint32_t xs) {
   constexpr int G = rec_groups<XMODE>();
   constexpr int S = XMODE == XM_XC_SMEM ? kRecStagesXc : kRecStages;
   constexpr int CW = rec_consumer_warps<XMODE>();
@@ -136,7 +157,7 @@ __global__ void __launch_bounds__(rec_threads<XMODE>()) k_recompress(const uint6
   const uint32_t hb = fixed_bits ? fixed_bits : hdr->merged_bits;
   if (NB && hb != (uint32_t)NB) return;
   const uint32_t nb = NB ? (uint32_t)NB : hb;
-  const uint64_t nsb = (dict_len + kXcSuper - 1) / kXcSuper;
+  const uint64_t nsb = (dict_len + (4ull << xs) - 1) >> (xs + 2);
   uint64_t xc_offs_bytes = 0;
   if (xc_budget) {
     const uint64_t n_new = hdr->merged_dict_len - dict_len;
@@ -233,9 +254,9 @@ __global__ void __launch_bounds__(rec_threads<XMODE>()) k_recompress(const uint6
       if constexpr (XMODE == XM_RAW_SMEM)
         return sx[code];
       else if constexpr (XMODE == XM_XC_SMEM)
-        return raw_warp ? ld_gather_u32(XM + code, pol_x) : xc_lookup<true>(code, srec, soffs, XM, pol_x);
+        return raw_warp ? ld_gather_u32(XM + code, pol_x) : xc_lookup<true>(code, xs, srec, soffs, XM, pol_x);
       else if constexpr (XMODE == XM_XC_GLOBAL)
-        return xc_lookup<false>(code, xrec, reinterpret_cast<const uint32_t*>(xoffs), XM, pol_x);
+        return xc_lookup<false>(code, xs, xrec, reinterpret_cast<const uint32_t*>(xoffs), XM, pol_x);
       else
         return ld_gather_u32(XM + code, pol_x);
     };
@@ -331,7 +352,7 @@ static uint32_t xc_smem_budget(uint32_t in_stage) {
 template <int NB>
 cudaError_t launch_nb(const dm_column_in* in, const dm_column_out* out, const uint32_t* xm, const uint32_t* xd,
                       const uint32_t* rank, dm_header* hdr, cudaStream_t st, uint32_t fixed_bits, const uint2* xrec,
-                      const uint8_t* xoffs) {
+                      const uint8_t* xoffs, uint32_t xs) {
   const uint32_t in_stage = kRecGroups * in->main_bits * 4 + 16;
   const uint32_t in_stage_xc = rec_groups<XM_XC_SMEM>() * in->main_bits * 4 + 16;
   const int sms = device_sms();
@@ -343,7 +364,7 @@ cudaError_t launch_nb(const dm_column_in* in, const dm_column_out* out, const ui
     kern<<<grid, threads, smem, st>>>(in->main_codes, in->n_main, in->main_bits, in->dict_len, xm, xd, rank,
                                           in->n_delta, out->merged_codes, hdr,
                                           groups == kRecGroups ? in_stage : in_stage_xc, fixed_bits, xrec, xoffs,
-                                          budget, xc_raw_warps());
+                                          budget, xc_raw_warps(), xs);
     note_launch();
   };
   const size_t ring = 128 + (size_t)kRecStages * in_stage;
@@ -364,11 +385,13 @@ cudaError_t launch_nb(const dm_column_in* in, const dm_column_out* out, const ui
     return cudaGetLastError();
   }
   const uint32_t budget0 = want_smem ? xc_smem_budget(in_stage_xc) : 0u;
-  const uint32_t budget = (uint64_t)xc_nsb(in->dict_len) * kXcRecBytes + 16 <= budget0 ? budget0 : 0u;
+  const uint32_t budget = (uint64_t)xc_nsb(in->dict_len, xs) * kXcRecBytes + 16 <= budget0 ? budget0 : 0u;
   if (budget)
     go(k_recompress<NB, XM_XC_SMEM>, 128 + (size_t)kRecStagesXc * in_stage_xc + budget, budget,
        rec_threads<XM_XC_SMEM>(), rec_groups<XM_XC_SMEM>());
   const bool xc_l2 = knob == 2 || knob == 3 || in->dict_len * 4 > kXcGlobalMinBytes;
+  // (A persisting L2 access-policy window over XC was measured: no gain on
+  // cfg5's Step 2(b), and the set-aside slowed Steps 1(a)/1(b) by 40%.)
   if (xc_l2)
     go(k_recompress<NB, XM_XC_GLOBAL>, ring, budget);
   else
@@ -377,7 +400,7 @@ cudaError_t launch_nb(const dm_column_in* in, const dm_column_out* out, const ui
 }
 
 using LaunchFn = cudaError_t (*)(const dm_column_in*, const dm_column_out*, const uint32_t*, const uint32_t*,
-                                 const uint32_t*, dm_header*, cudaStream_t, uint32_t, const uint2*, const uint8_t*);
+                                 const uint32_t*, dm_header*, cudaStream_t, uint32_t, const uint2*, const uint8_t*, uint32_t);
 template <int... I>
 constexpr auto make_table(std::integer_sequence<int, I...>) {
   return std::array<LaunchFn, sizeof...(I)>{&launch_nb<I>...};
@@ -387,21 +410,21 @@ constexpr auto make_table(std::integer_sequence<int, I...>) {
 
 cudaError_t launch_recompress(const dm_column_in* in, const dm_column_out* out, const uint32_t* xm,
                               const uint32_t* xd, const uint32_t* rank, dm_header* hdr, cudaStream_t st,
-                              uint32_t fixed_bits, const uint2* xc_rec, const uint8_t* xc_offs) {
+                              uint32_t fixed_bits, const uint2* xc_rec, const uint8_t* xc_offs, uint32_t xc_shift) {
   if (in->n_main + in->n_delta == 0) return cudaSuccess;
   static const auto table = make_table(std::make_integer_sequence<int, 33>{});  // [0] = runtime width
-  if (fixed_bits) return table[fixed_bits](in, out, xm, xd, rank, hdr, st, fixed_bits, nullptr, nullptr);
+  if (fixed_bits) return table[fixed_bits](in, out, xm, xd, rank, hdr, st, fixed_bits, nullptr, nullptr, 8);
   const uint64_t lo_len = std::max<uint64_t>(in->dict_len, in->n_delta ? 1 : 0);
   const uint32_t nb_lo = host_width(lo_len), nb_hi = host_width(in->dict_len + in->n_delta);
   if (nb_hi > 32) return cudaErrorInvalidValue;  // caller checks DM_E_TOO_WIDE first
   if (nb_hi - nb_lo <= 2) {
     for (uint32_t nb = nb_lo; nb <= nb_hi; ++nb) {
-      cudaError_t e = table[nb](in, out, xm, xd, rank, hdr, st, 0, xc_rec, xc_offs);
+      cudaError_t e = table[nb](in, out, xm, xd, rank, hdr, st, 0, xc_rec, xc_offs, xc_shift);
       if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
   }
-  return table[0](in, out, xm, xd, rank, hdr, st, 0, xc_rec, xc_offs);
+  return table[0](in, out, xm, xd, rank, hdr, st, 0, xc_rec, xc_offs, xc_shift);
 }
 
 cudaError_t launch_pack(const uint32_t* codes, uint64_t n, uint32_t bits, uint64_t* words, cudaStream_t st) {

@@ -1,0 +1,67 @@
+"""Step 1(b) variants vs the oracle, bit-exact: the single-pass merge (default)
+and the three-phase count / prefix-sum / write form, on tiles where
+U_D is the smaller side, where it is the larger side, duplicate-heavy and
+duplicate-free dictionaries, ties across tile boundaries, and both key types."""
+import numpy as np
+import pytest
+import torch
+
+import datagen
+import oracle
+from tests.parity import compare, run_gpu
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1109_6885_b200  # noqa: F401
+    oracle.build()
+
+
+@pytest.fixture(autouse=True)
+def _reset():
+    yield
+    import paper_1109_6885_b200 as dm
+    dm.set_tuning(1, 0)
+
+
+CASES = [
+    # n_main, dict_len, n_delta, p_new: sparse U_D, dense U_D, all-new, all-reuse, balanced
+    (300_000, 200_000, 20_000, 0.1),
+    (50_000, 3_000, 200_000, 0.9),
+    (10_000, 10_000, 300_000, 1.0),
+    (100_000, 40_000, 100_000, 0.0),
+    (100_000, 60_000, 60_000, 0.5),
+    (7_000, 1, 5_000, 0.3),
+]
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2])
+@pytest.mark.parametrize("key", ["u64", "b16"])
+@pytest.mark.parametrize("case", CASES)
+def test_merge_variant(variant, key, case):
+    import paper_1109_6885_b200 as dm
+    dm.set_tuning(1, variant)
+    n_main, dict_len, n_delta, p_new = case
+    col = datagen.make_random_case(911 + n_delta, n_main, dict_len, n_delta, p_new, key=key)
+    M, r = run_gpu(col)
+    compare(col, M, r)
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2])
+def test_merge_ties_at_every_tile_boundary(variant):
+    # U_D = every other U_M value plus values between: duplicates land on both
+    # sides of many merge-path tile boundaries (tile = 2048 merged elements)
+    import paper_1109_6885_b200 as dm
+    dm.set_tuning(1, variant)
+    UM = np.arange(0, 40_000, 2, dtype=np.uint64) * np.uint64(3)
+    D = np.concatenate([UM[::2], UM[1::5] + np.uint64(1), UM[-1:] + np.uint64(7), np.zeros(1, np.uint64)])
+    rng = np.random.default_rng(5)
+    D = D[rng.permutation(D.size)]
+    codes = rng.integers(0, UM.size, size=60_000, dtype=np.uint64).astype(np.uint32)
+    col = datagen.Column("u64", UM, codes, datagen.width_hint(UM.size), D)
+    M, r = run_gpu(col)
+    compare(col, M, r)

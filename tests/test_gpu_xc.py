@@ -110,6 +110,15 @@ def test_xc_dictionary_multiple_of_superblock_and_tail_inserts():
     _run_all_knobs(col)
 
 
+@pytest.mark.parametrize("dense", [False, True])
+def test_xc_block_shift(dense):
+    # N_D / |U_M| > 6/256 selects 128-code blocks (cfg5's density), else 256
+    n = 1024 * 50 + 3
+    n_new = 4000 if dense else 150
+    col = _column(n, 300_000, _spread(n, n_new, 7), 6000 if dense else 40, seed=7)
+    _run_all_knobs(col)
+
+
 def test_xc_too_large_for_shared_memory():
     # 300k distinct new values: XC exceeds the smem budget -> the L2 companion runs
     n = 100_000
