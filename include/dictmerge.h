@@ -192,8 +192,13 @@ dm_status dm_merge_column_host(dm_ctx* ctx, const dm_column_in* in, dm_column_ou
  * knob 1 = Step 1(b) variant: 0 (default) bitmap-slot tiles in two passes
  *   (count, prefix sum, write: P:302-314); 1 the first GPU form (rank tiles,
  *   three kernels); 2 bitmap-slot tiles in one pass with decoupled look-back.
- * The process starts with knob 0 = $DM_XMODE and knob 1 = $DM_MERGE when set
- * (experiments), else 0.
+ * knob 2 = Step 1(a) front end: 0 (default) auto -- hash
+ *   deduplication of D before the sort for 16-byte keys with N_D >= 65536;
+ *   1 never; 2 always.  Insert every tuple into a device hash table, sort only
+ *   the distinct values, map each tuple to its value's rank (same U_D and r).
+ *   Changes the workspace size: call dm_workspace_bytes after setting it.
+ * The process starts with knobs 0/1/2 = $DM_XMODE / $DM_MERGE / $DM_DEDUP when
+ * set (experiments), else 0.
  * Returns DM_OK, or DM_E_INVALID for an unknown knob or value.  Affects calls
  * made after it returns (a captured CUDA graph keeps the kernels it recorded). */
 int dm_set_tuning(int knob, int value);

@@ -17,6 +17,8 @@
 //                across tiles (32 predecessors per round trip), scatter
 //   k_unique     head flags over the sorted keys (warp ballots), single-pass
 //                scan with look-back -> U_D[rank] and r[original index] = rank
+#include <algorithm>
+
 #include "dm_device.cuh"
 
 #ifdef DM_TRACE
@@ -76,9 +78,12 @@ __device__ void build_plan(const uint32_t* hist, uint64_t n, int npass, SortPlan
 }
 
 template <class KT>
-__global__ void __launch_bounds__(256) k_hist(const void* __restrict__ D, uint64_t n, uint32_t* __restrict__ hist,
-                                              uint32_t* done, SortPlan* __restrict__ plan) {
+__global__ void __launch_bounds__(256) k_hist(const void* __restrict__ D, uint64_t n_host,
+                                              const unsigned long long* __restrict__ n_dev,
+                                              uint32_t* __restrict__ hist, uint32_t* done,
+                                              SortPlan* __restrict__ plan) {
   constexpr int P = KT::kPasses;
+  const uint64_t n = n_dev ? (uint64_t)*n_dev : n_host;
   __shared__ uint32_t s_h[P][256];
   __shared__ bool s_last;
   for (int i = threadIdx.x; i < P * 256; i += blockDim.x) (&s_h[0][0])[i] = 0;
@@ -107,9 +112,13 @@ __global__ void __launch_bounds__(256) k_hist(const void* __restrict__ D, uint64
 // ITEMS keys per thread, tile = NT * ITEMS keys in (warp, item, lane) order.
 template <class KT, int NT, int ITEMS>
 __global__ void __launch_bounds__(NT) k_onesweep(const void* __restrict__ D, void* kbuf0, void* kbuf1,
-                                                uint32_t* vbuf0, uint32_t* vbuf1, uint64_t n, int pass,
+                                                uint32_t* vbuf0, uint32_t* vbuf1, uint64_t n_host,
+                                                const unsigned long long* __restrict__ n_dev, int pass,
                                                 const SortPlan* __restrict__ plan, uint32_t* status,
                                                 uint32_t* counter) {
+  // n_dev: the key count is only known on the device (deduplicated delta); the
+  // grid covers n_host >= n and tiles past n exit (nothing waits on them)
+  const uint64_t n = n_dev ? (uint64_t)*n_dev : n_host;
   using K = typename KT::K;
   constexpr int W = NT / 32;
   constexpr int TILE = NT * ITEMS;
@@ -133,6 +142,7 @@ __global__ void __launch_bounds__(NT) k_onesweep(const void* __restrict__ D, voi
   DM_T(2);
   const uint64_t tile = s_tile;
   const uint64_t base = tile * TILE;
+  if (base >= n) return;
   const int src = plan->src[pass];
   const void* ksrc = src == SEL_BUF0 ? kbuf0 : kbuf1;
   const uint32_t* vsrc = src == SEL_BUF0 ? vbuf0 : vbuf1;
@@ -261,7 +271,8 @@ __global__ void __launch_bounds__(NT) k_onesweep(const void* __restrict__ D, voi
 template <class KT>
 __global__ void __launch_bounds__(kUniqThreads) k_unique(const void* __restrict__ D, const void* kbuf0,
                                                         const void* kbuf1, const uint32_t* vbuf0,
-                                                        const uint32_t* vbuf1, uint64_t n,
+                                                        const uint32_t* vbuf1, uint64_t n_host,
+                                                        const unsigned long long* __restrict__ n_dev,
                                                         const SortPlan* __restrict__ plan, uint64_t* status,
                                                         uint32_t* counter, void* __restrict__ udict,
                                                         uint32_t* __restrict__ rank, dm_header* hdr) {
@@ -274,6 +285,8 @@ __global__ void __launch_bounds__(kUniqThreads) k_unique(const void* __restrict_
   if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
   __syncthreads();
   const uint64_t tile = s_tile;
+  const uint64_t n = n_dev ? (uint64_t)*n_dev : n_host;
+  if (tile * TILE >= n) return;
   const int sel = plan->final_sel;
   const void* ks = sel == SEL_BUF0 ? kbuf0 : kbuf1;
   const uint32_t* vs = sel == SEL_BUF0 ? vbuf0 : vbuf1;
@@ -342,11 +355,86 @@ __global__ void __launch_bounds__(kUniqThreads) k_unique(const void* __restrict_
   }
 }
 
-template <class KT, int NT, int ITEMS>
-void launch_passes(const dm_column_in* in, char* ws, const WsLayout& L, SortPlan* plan, uint32_t* counters,
-                   cudaStream_t st) {
+// ------------------------------------------------------------ dedup front end
+// NEXT1: the paper gets U_D by "extracting the unique values"
+// from a tree it maintained at insert time; a delta with many
+// repeated values (cfg3's Zipf reuse: 5e6 tuples, ~1.5e6 distinct) would spend
+// the 16 radix passes mostly on repeats.  So: insert every tuple into an
+// open-addressing hash table first -- the first inserter of a value claims a
+// slot, takes the next distinct id and stores the value at dkeys[id] -- then
+// sort only the distinct values (count known on the device only) and map each
+// tuple's id to its rank.  Same U_D and r as sorting all of D.
+__device__ __forceinline__ uint64_t dd_mix(uint64_t x) {
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdull;
+  x ^= x >> 33;
+  x *= 0xc4ceb9fe1a85ec53ull;
+  x ^= x >> 33;
+  return x;
+}
+__device__ __forceinline__ uint64_t dd_hash(uint64_t k) { return dd_mix(k); }
+__device__ __forceinline__ uint64_t dd_hash(K128 k) { return dd_mix(k.hi ^ dd_mix(k.lo + 0x9e3779b97f4a7c15ull)); }
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Slot tag: 0 empty; (h & ~3) | 1 claimed; | 3 ready (id and key published).
+template <class KT>
+__global__ void __launch_bounds__(256) k_dedup_insert(const void* __restrict__ D, uint64_t n,
+                                                      uint32_t* __restrict__ tags, uint32_t* __restrict__ ids,
+                                                      uint64_t mask, void* __restrict__ dkeys,
+                                                      uint32_t* __restrict__ tid, unsigned long long* n_dist) {
   using K = typename KT::K;
-  const uint64_t n = in->n_delta;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const K k = KT::load(D, i);
+    const uint64_t h = dd_hash(k);
+    uint64_t slot = (h >> 32) & mask;
+    const uint32_t tg = ((uint32_t)h & ~3u) | 1u;
+    uint32_t id = 0;
+    for (;;) {
+      uint32_t t = ld_acquire_u32(tags + slot);
+      if (t == 0) {
+        t = atomicCAS(tags + slot, 0u, tg);
+        if (t == 0) {  // claimed: publish the value, then the id, then "ready"
+          id = (uint32_t)atomicAdd(n_dist, 1ull);
+          KT::store(dkeys, id, k);
+          ids[slot] = id;
+          __threadfence();
+          st_release_u32(tags + slot, tg | 2u);
+          break;
+        }
+      }
+      if ((t | 2u) == (tg | 2u)) {  // same hash tag: wait until ready, compare the value
+        while (!(t & 2u)) t = ld_acquire_u32(tags + slot);
+        const uint32_t cid = __ldcg(ids + slot);
+        if (KT::eq(KT::load_cg(dkeys, cid), k)) {
+          id = cid;
+          break;
+        }
+      }
+      slot = (slot + 1) & mask;
+    }
+    tid[i] = id;
+  }
+}
+
+// r[k] = rank of tuple k's distinct value = rank_of_id[tid[k]].
+__global__ void __launch_bounds__(256) k_dedup_ranks(const uint32_t* __restrict__ tid,
+                                                     const uint32_t* __restrict__ rank_of_id, uint64_t n,
+                                                     uint32_t* __restrict__ rank) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    rank[i] = __ldg(rank_of_id + __ldg(tid + i));
+}
+
+template <class KT, int NT, int ITEMS>
+void launch_passes(const void* D, uint64_t n, const unsigned long long* n_dev, char* ws, const WsLayout& L,
+                   SortPlan* plan, uint32_t* counters, cudaStream_t st) {
+  using K = typename KT::K;
   constexpr int TILE = NT * ITEMS;
   const size_t dsmem = (sizeof(K) + sizeof(uint32_t)) * TILE;
   ensure_smem((const void*)k_onesweep<KT, NT, ITEMS>);
@@ -354,8 +442,8 @@ void launch_passes(const dm_column_in* in, char* ws, const WsLayout& L, SortPlan
   for (int p = 0; p < KT::kPasses; ++p) {
     uint32_t* status = reinterpret_cast<uint32_t*>(ws + L.status_sort) + (uint64_t)p * ntiles * 256;
     k_onesweep<KT, NT, ITEMS><<<(unsigned)ntiles, NT, dsmem, st>>>(
-        in->delta, ws + L.keys0, ws + L.keys1, reinterpret_cast<uint32_t*>(ws + L.vals0),
-        reinterpret_cast<uint32_t*>(ws + L.vals1), n, p, plan, status, counters + CNT_SORT + p);
+        D, ws + L.keys0, ws + L.keys1, reinterpret_cast<uint32_t*>(ws + L.vals0),
+        reinterpret_cast<uint32_t*>(ws + L.vals1), n, n_dev, p, plan, status, counters + CNT_SORT + p);
     note_launch();
   }
 }
@@ -367,22 +455,44 @@ cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, void* udict
   uint32_t* counters = reinterpret_cast<uint32_t*>(ws + L.counters);
   uint32_t* hist = reinterpret_cast<uint32_t*>(ws + L.hist);
   SortPlan* plan = reinterpret_cast<SortPlan*>(ws + L.plan);
+  // Sorted input: D itself, or (dedup) its distinct values dkeys, whose count
+  // n_dist exists on the device only; ranks then go to rank_of_id first.
+  const void* D = in->delta;
+  const unsigned long long* n_dev = nullptr;
+  uint32_t* sort_rank = rank;
+  if (L.dedup) {
+    unsigned long long* n_dist = reinterpret_cast<unsigned long long*>(counters + CNT_DEDUP);
+    const int sms = device_sms();
+    k_dedup_insert<KT><<<(unsigned)std::min<uint64_t>((n + 255) / 256, (uint64_t)sms * 8), 256, 0, st>>>(
+        in->delta, n, reinterpret_cast<uint32_t*>(ws + L.dd_tags), reinterpret_cast<uint32_t*>(ws + L.dd_ids),
+        L.dd_cap - 1, ws + L.dd_keys, reinterpret_cast<uint32_t*>(ws + L.dd_tid), n_dist);
+    note_launch();
+    D = ws + L.dd_keys;
+    n_dev = n_dist;
+    sort_rank = reinterpret_cast<uint32_t*>(ws + L.dd_rank);
+  }
   const int hist_blocks = (int)std::min<uint64_t>((n + 4095) / 4096, 148 * 4);
-  k_hist<KT><<<hist_blocks, 256, 0, st>>>(in->delta, n, hist, counters + CNT_HIST, plan);
+  k_hist<KT><<<hist_blocks, 256, 0, st>>>(D, n, n_dev, hist, counters + CNT_HIST, plan);
   note_launch();
   constexpr bool U64 = KT::kBytes == 8;
   switch (sort_variant()) {  // must match sort_tile_keys() (workspace layout)
-    case 1: launch_passes<KT, 256, U64 ? 16 : 8>(in, ws, L, plan, counters, st); break;
-    case 2: launch_passes<KT, 256, U64 ? 8 : 4>(in, ws, L, plan, counters, st); break;
-    case 3: launch_passes<KT, 1024, U64 ? 8 : 4>(in, ws, L, plan, counters, st); break;
-    default: launch_passes<KT, 512, U64 ? 16 : 8>(in, ws, L, plan, counters, st); break;
+    case 1: launch_passes<KT, 256, U64 ? 16 : 8>(D, n, n_dev, ws, L, plan, counters, st); break;
+    case 2: launch_passes<KT, 256, U64 ? 8 : 4>(D, n, n_dev, ws, L, plan, counters, st); break;
+    case 3: launch_passes<KT, 1024, U64 ? 8 : 4>(D, n, n_dev, ws, L, plan, counters, st); break;
+    default: launch_passes<KT, 512, U64 ? 16 : 8>(D, n, n_dev, ws, L, plan, counters, st); break;
   }
   const uint64_t utiles = (n + kUniqThreads * kUniqItems - 1) / (kUniqThreads * kUniqItems);
   k_unique<KT><<<(unsigned)utiles, kUniqThreads, 0, st>>>(
-      in->delta, ws + L.keys0, ws + L.keys1, reinterpret_cast<const uint32_t*>(ws + L.vals0),
-      reinterpret_cast<const uint32_t*>(ws + L.vals1), n, plan, reinterpret_cast<uint64_t*>(ws + L.status_unique),
-      counters + CNT_UNIQUE, udict, rank, hdr);
+      D, ws + L.keys0, ws + L.keys1, reinterpret_cast<const uint32_t*>(ws + L.vals0),
+      reinterpret_cast<const uint32_t*>(ws + L.vals1), n, n_dev, plan,
+      reinterpret_cast<uint64_t*>(ws + L.status_unique), counters + CNT_UNIQUE, udict, sort_rank, hdr);
   note_launch();
+  if (L.dedup) {
+    const int sms = device_sms();
+    k_dedup_ranks<<<(unsigned)std::min<uint64_t>((n + 255) / 256, (uint64_t)sms * 8), 256, 0, st>>>(
+        reinterpret_cast<const uint32_t*>(ws + L.dd_tid), sort_rank, n, rank);
+    note_launch();
+  }
   return cudaGetLastError();
 }
 

@@ -97,7 +97,7 @@ static int env_knob(const char* name, int hi) {
   const int v = s ? std::atoi(s) : 0;
   return (v >= 0 && v <= hi) ? v : 0;
 }
-static std::atomic<int> g_tuning[4] = {env_knob("DM_XMODE", 3), env_knob("DM_MERGE", 2)};
+static std::atomic<int> g_tuning[4] = {env_knob("DM_XMODE", 3), env_knob("DM_MERGE", 2), env_knob("DM_DEDUP", 2)};
 int tuning(int knob) { return (knob >= 0 && knob < 4) ? g_tuning[knob].load(std::memory_order_relaxed) : 0; }
 
 int sort_variant() {
@@ -153,6 +153,17 @@ WsLayout ws_layout(const dm_column_in* in) {
   L.xc_rblk = take((xc_nblk(in->dict_len, kXcMinShift) + 1) * 4);  // sized for the smallest blocks
   L.xc_rec = take(xc_nsb(in->dict_len, kXcMinShift) * kXcRecBytes);
   L.xc_offs = take(nD + 16);
+  L.dedup = dedup_wanted(in);
+  if (L.dedup) {
+    uint64_t cap = 1024;
+    while (cap < 2 * nD) cap <<= 1;
+    L.dd_cap = cap;
+    L.dd_tags = take(cap * 4);
+    L.dd_ids = take(cap * 4);
+    L.dd_keys = take(nD * E);
+    L.dd_tid = take(nD * 4);
+    L.dd_rank = take(nD * 4);
+  }
   L.total = o;
   return L;
 }
@@ -207,6 +218,7 @@ static dm_status merge_async(const dm_column_in* in, const dm_column_out* out, v
   };
   mark(0);
   cudaError_t e = cudaMemsetAsync(w, 0, L.zero_bytes, st);
+  if (e == cudaSuccess && L.dedup) e = cudaMemsetAsync(w + L.dd_tags, 0, L.dd_cap * 4, st);
   if (e == cudaSuccess && zero_header) e = cudaMemsetAsync(d_header, 0, sizeof(dm_header), st);
   if (e != cudaSuccess) return cuda_fail(e);
   void* udict = out->delta_dict ? out->delta_dict : (void*)(w + L.udict);
@@ -300,7 +312,7 @@ struct dm_ctx {
 extern "C" {
 
 int dm_set_tuning(int knob, int value) {
-  if (knob < 0 || knob > 1 || value < 0 || value > (knob == 0 ? 3 : 2)) return DM_E_INVALID;
+  if (knob < 0 || knob > 2 || value < 0 || value > (knob == 0 ? 3 : 2)) return DM_E_INVALID;
   g_tuning[knob].store(value);
   return DM_OK;
 }

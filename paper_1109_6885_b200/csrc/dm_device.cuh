@@ -49,6 +49,10 @@ struct KeyU64 {
   __device__ __forceinline__ static void store(void* p, uint64_t i, K k) {
     static_cast<uint64_t*>(p)[i] = k;
   }
+  // coherent (L2) load of a value written by another SM in the same kernel
+  __device__ __forceinline__ static K load_cg(const void* p, uint64_t i) {
+    return __ldcg(static_cast<const uint64_t*>(p) + i);
+  }
   __device__ __forceinline__ static uint32_t digit(K k, int pass) {
     return (uint32_t)(k >> (8 * pass)) & 0xffu;
   }
@@ -80,6 +84,10 @@ struct KeyB16 {
   }
   __device__ __forceinline__ static void store(void* p, uint64_t i, K k) {
     static_cast<ulonglong2*>(p)[i] = make_ulonglong2(bswap(k.hi), bswap(k.lo));
+  }
+  __device__ __forceinline__ static K load_cg(const void* p, uint64_t i) {
+    const ulonglong2 v = __ldcg(static_cast<const ulonglong2*>(p) + i);
+    return K{bswap(v.x), bswap(v.y)};
   }
   __device__ __forceinline__ static uint32_t digit(K k, int pass) {
     return pass < 8 ? (uint32_t)(k.lo >> (8 * pass)) & 0xffu : (uint32_t)(k.hi >> (8 * (pass - 8))) & 0xffu;

@@ -46,7 +46,8 @@ inline uint64_t xc_nsb(uint64_t dict_len, uint32_t xs) { return (dict_len + (4ul
 enum XMode { XM_RAW_GLOBAL = 0, XM_RAW_SMEM = 1, XM_XC_SMEM = 2, XM_XC_GLOBAL = 3 };
 // Tuning knobs (dm_set_tuning): index 0 = X_M placement (0 auto, 1 plain only,
 // 2 compact (smem if it fits, else L2), 3 compact from L2); index 1 = Step 1(b)
-// variant (0 lean two-pass, 1 first three-phase form, 2 lean single pass).
+// variant (0 lean two-pass, 1 first three-phase form, 2 lean single pass);
+// index 2 = Step 1(a) dedup front end (0 auto, 1 off, 2 on).
 int tuning(int knob);
 // Whether a merge builds XC at all: only when the plain X_M is too big for smem.
 inline bool xc_enabled(uint64_t dict_len) { return dict_len * 4 > kRecSmemXBytes; }
@@ -54,6 +55,13 @@ inline bool xc_enabled(uint64_t dict_len) { return dict_len * 4 > kRecSmemXBytes
 inline bool xc_wanted(uint64_t dict_len) {
   const int k = tuning(0);
   return k == 1 ? false : k == 0 ? dict_len * 4 > kXcGlobalMinBytes : xc_enabled(dict_len);
+}
+// Step 1(a) dedup front end (NEXT1): knob 2 = 0 auto (16-byte keys with
+// N_D >= 2^16: 16 radix passes make repeats expensive), 1 off, 2 on.
+inline bool dedup_wanted(const dm_column_in* in) {
+  const int k = tuning(2);
+  if (in->n_delta == 0 || k == 1) return false;
+  return k == 2 || (in->key == DM_KEY_B16 && in->n_delta >= (1u << 16));
 }
 // Block shift: 256-code blocks when N_D / |U_M| promises <= 6 entries per block
 // (and always for the shared-memory variant, knob 2), else 128-code blocks.
@@ -101,12 +109,19 @@ struct WsLayout {
   size_t xc_rblk;        // XC: u32[nblk + 1], new values inserted before each 256-block
   size_t xc_rec;         // XC: uint2[nsb] superblock records
   size_t xc_offs;        // XC: u8[n_delta] insertion position mod 256 per new value
+  size_t dd_tags;        // dedup (NEXT1): u32[dd_cap] slot tags (memset per call)
+  size_t dd_ids;         // dedup: u32[dd_cap] distinct id per slot
+  size_t dd_keys;        // dedup: distinct values, raw layout, n_delta capacity
+  size_t dd_tid;         // dedup: u32[n_delta] distinct id per tuple
+  size_t dd_rank;        // dedup: u32[n_delta] rank of each distinct id
+  uint64_t dd_cap;       // dedup: table slots (power of two >= 2 n_delta), 0 = no dedup
+  bool dedup;
   size_t total;
   uint64_t ntiles_sort, ntiles_unique, ntiles_merge;
   int npass;
 };
 
-enum { CNT_SORT = 0, CNT_UNIQUE = 16, CNT_MERGE = 17, CNT_HIST = 18 };
+enum { CNT_SORT = 0, CNT_UNIQUE = 16, CNT_MERGE = 17, CNT_HIST = 18, CNT_DEDUP = 20 /* u64, 2 slots */ };
 
 WsLayout ws_layout(const dm_column_in* in);
 uint32_t host_width(uint64_t n);

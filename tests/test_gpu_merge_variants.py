@@ -65,3 +65,41 @@ def test_merge_ties_at_every_tile_boundary(variant):
     col = datagen.Column("u64", UM, codes, datagen.width_hint(UM.size), D)
     M, r = run_gpu(col)
     compare(col, M, r)
+
+
+# ------------------------------------------------- Step 1(a) dedup front end (NEXT1)
+@pytest.fixture()
+def _reset_dedup():
+    yield
+    import paper_1109_6885_b200 as dm
+    dm.set_tuning(2, 0)
+
+
+DEDUP_CASES = CASES + [
+    (50_000, 1000, 120_000, 0.01),   # heavy repeats: ~1.2k distinct of 120k
+    (1000, 5, 70_000, 0.0),          # 5 distinct values
+    (0, 1, 9_000, 1.0),              # empty main
+]
+
+
+@pytest.mark.parametrize("key", ["u64", "b16"])
+@pytest.mark.parametrize("case", DEDUP_CASES)
+def test_dedup_front_end(key, case, _reset_dedup):
+    import paper_1109_6885_b200 as dm
+    dm.set_tuning(2, 2)  # always deduplicate
+    n_main, dict_len, n_delta, p_new = case
+    col = datagen.make_random_case(311 + n_delta, n_main, dict_len, n_delta, p_new, key=key)
+    M, r = run_gpu(col)
+    compare(col, M, r)
+
+
+def test_dedup_all_equal_and_zipf_strings(_reset_dedup):
+    import paper_1109_6885_b200 as dm
+    dm.set_tuning(2, 0)  # auto: on for 16-byte keys with N_D >= 65536
+    col = datagen.make_config(3, scale=0.02)  # Zipf reuse, 100k delta strings
+    M, r = run_gpu(col)
+    compare(col, M, r)
+    col = datagen.make_random_case(3, 20000, 500, 0, 0.0, key="b16")
+    col.delta = np.repeat(col.main_dict[7:8], 70_000, axis=0)  # one value, 70k times
+    M, r = run_gpu(col)
+    compare(col, M, r)
