@@ -40,6 +40,8 @@ WORKLOADS = {
     "cfg3": "cfg3: single 16-byte string column, N_M=1e8 @20b over |U_M|=1e6 (Zipf(1) codes), N_D=5e6 (20% new)",
     "cfg4": "cfg4: 300-column table, N_M=1e7 + N_D=1e5 per column, card log-uniform [2,1e7], 240 u64 + 60 strings",
     "cfg5": "cfg5: single u64 column, N_M=|U_M|=2^30 @30b (all unique), N_D=5e7 all new -> 31 bits (reading A12)",
+    "cfg2e4": "cfg2 shape with 4-byte values (E=4, SURVEY NEXT4): N_M=1e8 @24b over |U_M|=1e7 in [0,2^32), "
+              "N_D=1e6 (10% new)",
 }
 METRIC = "merged tuples/sec per column (N_M+N_D)"
 UNIT = "tuples/s"
@@ -122,7 +124,12 @@ def host_info():
 
 # ------------------------------------------------------------------------ inputs
 def cfg_number(workload: str) -> int:
-    return int(workload[3:])
+    return int(workload[3])  # "cfg2e4" -> 2 (the E = 4 variant of cfg2)
+
+
+def key_dtype(workload: str) -> str:
+    """The arithmetic type the path computes in: key compares and u32 codes."""
+    return "u32" if workload.endswith("e4") else "u8x16" if cfg_number(workload) == 3 else "u64"
 
 
 def host_columns(workload: str, rank: int, world: int):
@@ -136,15 +143,18 @@ def host_columns(workload: str, rank: int, world: int):
             costs.append(column_cost(10**7, 10**5, card, datagen.width_hint(card), 8 if key == "u64" else 16))
         mine = lpt_partition(costs, world)[rank]
         return [datagen.make_config(4, column=j) for j in mine]
+    if workload.endswith("e4"):
+        return [datagen.make_config_e4(seed=datagen.BASE_SEED + 7 * rank)]
     return [datagen.make_config(cfg, seed=datagen.BASE_SEED + 7 * rank)]
 
 
 def device_inputs(col, dev):
     import torch
     import paper_1109_6885_b200 as dm
-    if col.key == "u64":
-        UM = torch.from_numpy(col.main_dict.view(np.int64)).to(dev)
-        D = torch.from_numpy(col.delta.view(np.int64)).to(dev)
+    if col.key in ("u64", "u32"):
+        it = np.int64 if col.key == "u64" else np.int32
+        UM = torch.from_numpy(col.main_dict.view(it)).to(dev)
+        D = torch.from_numpy(col.delta.view(it)).to(dev)
     else:
         UM = torch.from_numpy(np.ascontiguousarray(col.main_dict)).to(dev)
         D = torch.from_numpy(np.ascontiguousarray(col.delta)).to(dev)
@@ -171,7 +181,7 @@ def oracle_sample(workload: str):
             "8 of the 300 cfg4 columns at full size (0,60,120,180,239 u64; 240,270,299 strings)"
     if cfg == 5:
         return [datagen.make_config(5, scale=1 / 16)], "cfg5 at 1/16 scale (2^26 main rows, 3.1e6 delta)"
-    col = datagen.make_config(cfg)
+    col = datagen.make_config_e4() if workload.endswith("e4") else datagen.make_config(cfg)
     return [col], f"the full {workload} column (N'={col.n_main + col.n_delta})"
 
 
@@ -202,7 +212,7 @@ def reference_arm(args, rank, world):
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u64" if cfg_number(args.workload) != 3 else "u8x16",
+        "vs_baseline": None, "dtype": key_dtype(args.workload),
         "data": "synthetic (datagen, seeded)", "config": {"workload": WORKLOADS[args.workload]},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
                          "sample": f"{sample}; oracle linear mode, 1 thread of {ncpu} ({cpu})"},
@@ -223,6 +233,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--naive-step2", action="store_true",
+                    help="also time the paper's unoptimized Step 2 (binary search per tuple, P:206-212)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -332,7 +344,7 @@ def main():
     pk = peaks()
     peak_hbm = pk["hbm_gbs"] if pk else 6650.0
     results = merger.results() if table else [merger.result()]
-    key_bytes = [(UM.shape[1] if UM.dim() == 2 else 8) for (UM, _, _, _, _) in dev_cols]
+    key_bytes = [(UM.shape[1] if UM.dim() == 2 else UM.element_size()) for (UM, _, _, _, _) in dev_cols]
     sb = sum(strict_bytes(n_m, b, D.shape[0], kb, UM.shape[0], r.merged_len, r.merged_bits)
              for (UM, _, n_m, b, D), kb, r in zip(dev_cols, key_bytes, results))
     s2b = sum(step2_bytes(n_m, b, D.shape[0], UM.shape[0], r.merged_bits, r.delta_dict_len)
@@ -359,6 +371,32 @@ def main():
                     "peak": peak_hbm, "unit": "GB/s", "frac": achieved / peak_hbm, "traffic": None,
                     "algorithmic_bytes_per_launch": sb}
 
+    # ---- optional: the paper's unoptimized Step 2 on the same merge (NEXT4)
+    naive = None
+    if args.naive_step2 and not table:
+        dm.set_tuning(dm.KNOB_STEP2, 1)
+        nm = dm.ColumnMerger(*dev_cols[0])
+        nm.run_async()
+        torch.cuda.synchronize()
+        nev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+        for row in nev:
+            for e in row:
+                e.record()
+        torch.cuda.synchronize()
+        for k in range(args.steps):
+            flush.zero_()
+            nm.run_async_timed(nev[k])
+        torch.cuda.synchronize()
+        dm.set_tuning(dm.KNOB_STEP2, 0)
+        nr = nm.result()
+        same = bool(torch.equal(nr.merged_codes, results[0].merged_codes))
+        n2 = statistics.mean(nev[k][2].elapsed_time(nev[k][3]) for k in range(args.steps))
+        o2 = statistics.mean(s2)
+        naive = {"step2_naive_ms": n2, "step2_opt_ms": o2, "opt_over_naive": n2 / o2, "identical_output": same,
+                 "note": "UnOpt = binary search of every tuple's value in U' (P:206-212); Opt = X_M/X_D "
+                         "recompression (Eq 11, P:272); paper's claim: 9-10x (P:336)"}
+        del nm
+
     # ---- e2e through the public host-buffer API (H2D inputs + D2H results inside)
     e2e = None
     if not args.no_e2e and not table:
@@ -366,7 +404,7 @@ def main():
         ctx = dm.HostContext(local)
         hUM, hD, hM = UM.cpu().pin_memory(), D.cpu().pin_memory(), M.cpu().pin_memory()
         kb = key_bytes[0]
-        hU = (torch.empty(UM.shape[0] + D.shape[0], dtype=torch.int64) if kb == 8 else
+        hU = (torch.empty(UM.shape[0] + D.shape[0], dtype=UM.dtype) if UM.dim() == 1 else
               torch.empty((UM.shape[0] + D.shape[0], 16), dtype=torch.uint8)).pin_memory()
         hMo = torch.empty(dm.words(n_tuples, 32), dtype=torch.int64).pin_memory()
         ctx.merge(hUM, hM, n_m, b, hD, hU, hMo)  # warm-up (allocations)
@@ -409,10 +447,11 @@ def main():
             "metric": METRIC if not table else "merged column-tuples/sec (sum over columns of N_M+N_D)",
             "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u64" if cfg != 3 else "u8x16",
+            "vs_baseline": None, "dtype": key_dtype(args.workload),
             "data": f"synthetic (datagen, seeded; BASELINE configs[{cfg - 1}])", "config": cfgd,
             "hbm_fraction_strict": sb / (ms_per_step / 1e3) / 1e9 / peak_hbm,
             "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e,
+            **({"step2_naive_vs_opt": naive} if naive else {}),
             "gpu_launches": int(round(launches_per_merge * args.steps)),
             "gpu_launches_per_step": launches_per_merge,
             "clocks": clk.summary(),

@@ -183,7 +183,7 @@ def _distinct_strings(seed: int, stream: int, count: int, exclude: Optional[np.n
 @dataclasses.dataclass
 class Column:
     """One column's merge inputs (unpacked codes; each side packs them itself)."""
-    key: str                    # "u64" | "b16"
+    key: str                    # "u64" | "u32" | "b16"
     main_dict: np.ndarray       # sorted, unique. u64 (n,) or u8 (n,16)
     main_codes: np.ndarray      # u32 (N_M,), each < len(main_dict)
     main_bits: int              # code width of the packed main vector
@@ -192,7 +192,7 @@ class Column:
 
     @property
     def key_bytes(self) -> int:
-        return 8 if self.key == "u64" else 16
+        return {"u64": 8, "u32": 4}.get(self.key, 16)
 
     @property
     def n_main(self) -> int:
@@ -338,10 +338,29 @@ def make_config(cfg: int, seed: Optional[int] = None, scale: float = 1.0, column
     raise ValueError(cfg)
 
 
+def u32_column(col: Column) -> Column:
+    """A u64 column whose values are < 2^32, as 4-byte keys (the paper's E = 4)."""
+    assert col.key == "u64" and (col.main_dict.size == 0 or int(col.main_dict.max()) < 2 ** 32)
+    assert col.delta.size == 0 or int(col.delta.max()) < 2 ** 32
+    return Column("u32", col.main_dict.astype(np.uint32), col.main_codes, col.main_bits,
+                  col.delta.astype(np.uint32), col.name)
+
+
+def make_config_e4(seed: Optional[int] = None, scale: float = 1.0) -> Column:
+    """cfg2's shape with 4-byte values (the paper's E = 4 of its Fig 8 value-length
+    sweep): U_M = 1e7 distinct values in [0, 2^32)."""
+    s = config_seed(2, BASE_SEED if seed is None else seed) + 4
+    return u32_column(_u64_column(s, _scaled(10**8, scale), _scaled(10**7, scale, 2), _scaled(10**6, scale), 0.1, 32,
+                                  main_bits=24 if scale == 1.0 else None, name="cfg2e4"))
+
+
 def make_random_case(seed: int, n_main: int, dict_len: int, n_delta: int, p_new: float,
                      key: str = "u64", value_bits: int = 64, main_bits: Optional[int] = None) -> Column:
     """A generic random column (parity sweeps and edge cases)."""
     if key == "u64":
         return _u64_column(seed, n_main, dict_len, n_delta, p_new, value_bits, main_bits=main_bits,
                            name=f"rand{seed}")
+    if key == "u32":
+        return u32_column(_u64_column(seed, n_main, dict_len, n_delta, p_new, min(value_bits, 32),
+                                      main_bits=main_bits, name=f"rand{seed}"))
     return _b16_column(seed, n_main, dict_len, n_delta, p_new, main_bits=main_bits, name=f"rand{seed}")

@@ -28,7 +28,8 @@
  *     bitstream held in little-endian u64 words: code i occupies stream bits
  *     [i*b, (i+1)*b), stream bit s is bit s%64 of word s/64.  Exactly
  *     dm_words(n, b) words are significant and their pad bits are zero.
- *   - DM_KEY_U64 keys are little-endian u64 compared as unsigned integers.
+ *   - DM_KEY_U64 (DM_KEY_U32) keys are little-endian u64 (u32) compared as
+ *     unsigned integers.
  *     DM_KEY_B16 keys are 16 raw bytes compared bytewise (memcmp) over all 16
  *     bytes; zero padding takes part in the order.
  *
@@ -67,7 +68,9 @@ typedef enum {
   DM_E_NCCL = -7         /* reserved for the sharded variant                      */
 } dm_status;
 
-typedef enum { DM_KEY_U64 = 0, DM_KEY_B16 = 1 } dm_key;
+/* Value types: 8-byte unsigned integers, 16-byte memcmp-ordered strings, and
+ * 4-byte unsigned integers (the paper's E = 4 of Fig 8). */
+typedef enum { DM_KEY_U64 = 0, DM_KEY_B16 = 1, DM_KEY_U32 = 2 } dm_key;
 
 /* One column's merge inputs.  All device pointers, read-only. */
 typedef struct {
@@ -197,8 +200,11 @@ dm_status dm_merge_column_host(dm_ctx* ctx, const dm_column_in* in, dm_column_ou
  *   1 never; 2 always.  Insert every tuple into a device hash table, sort only
  *   the distinct values, map each tuple to its value's rank (same U_D and r).
  *   Changes the workspace size: call dm_workspace_bytes after setting it.
- * The process starts with knobs 0/1/2 = $DM_XMODE / $DM_MERGE / $DM_DEDUP when
- * set (experiments), else 0.
+ * knob 3 = Step 2(b) variant: 0 (default) the optimized recompression through
+ *   X_M / X_D (Eq 11); 1 the paper's unoptimized form:
+ *   every tuple's value binary-searched in U' -- a measured baseline only.
+ * The process starts with knobs 0..3 = $DM_XMODE / $DM_MERGE / $DM_DEDUP /
+ * $DM_STEP2 when set (experiments), else 0.
  * Returns DM_OK, or DM_E_INVALID for an unknown knob or value.  Affects calls
  * made after it returns (a captured CUDA graph keeps the kernels it recorded). */
 int dm_set_tuning(int knob, int value);

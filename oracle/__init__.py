@@ -127,7 +127,7 @@ def merge(col, mode: str = "linear", main_words: Optional[np.ndarray] = None) ->
     ``main_words``: the packed main vector; defaults to ``pack(col.main_codes, col.main_bits)``.
     """
     E = col.key_bytes
-    kdt = np.uint64 if E == 8 else np.uint8
+    kdt = {4: np.uint32, 8: np.uint64}.get(E, np.uint8)
     UM = np.ascontiguousarray(col.main_dict, dtype=kdt)
     D = np.ascontiguousarray(col.delta, dtype=kdt)
     nUM = UM.shape[0]
@@ -135,7 +135,7 @@ def merge(col, mode: str = "linear", main_words: Optional[np.ndarray] = None) ->
     nM = int(col.main_codes.shape[0]) if main_words is None else int(col.n_main)
     W = pack(col.main_codes, col.main_bits) if main_words is None else np.ascontiguousarray(main_words, np.uint64)
     cap_bits = width(nUM + nD)
-    shape = (lambda n: (n,)) if E == 8 else (lambda n: (n, 16))
+    shape = (lambda n: (n,)) if E in (4, 8) else (lambda n: (n, 16))
     Uo = np.zeros(shape(max(nUM + nD, 1)), dtype=kdt)
     Mo = np.zeros(max(words(nM + nD, max(cap_bits, 1)), 1), dtype=np.uint64)
     XM = np.zeros(max(nUM, 1), dtype=np.uint32)
@@ -161,7 +161,7 @@ def codes_at(main_dict: np.ndarray, delta: np.ndarray, values: np.ndarray, key_b
     L.dmo_codes_at.restype = ctypes.c_int
     L.dmo_codes_at.argtypes = [ctypes.c_uint32, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_uint64,
                                ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint64)]
-    kdt = np.uint64 if key_bytes == 8 else np.uint8
+    kdt = {4: np.uint32, 8: np.uint64}.get(key_bytes, np.uint8)
     UM = np.ascontiguousarray(main_dict, dtype=kdt)
     D = np.ascontiguousarray(delta, dtype=kdt)
     V = np.ascontiguousarray(values, dtype=kdt)

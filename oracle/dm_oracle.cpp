@@ -233,7 +233,7 @@ int codes_at(const K* UM, uint64_t nUM, const K* D, uint64_t nD, const K* vals, 
 
 bool args_ok(const dmo_in* in, const dmo_out* out) {
   if (!in || !out) return false;
-  if (in->key_bytes != 8 && in->key_bytes != 16) return false;
+  if (in->key_bytes != 4 && in->key_bytes != 8 && in->key_bytes != 16) return false;
   if (in->dict_len && !in->main_dict) return false;
   if (in->n_main && !in->main_words) return false;
   if (in->n_delta && !in->delta) return false;
@@ -267,11 +267,13 @@ int dmo_unpack(const uint64_t* words, uint64_t n, uint32_t bits, uint32_t* codes
 
 int dmo_merge_linear(const dmo_in* in, dmo_out* out) {
   if (!args_ok(in, out)) return DMO_E_INVALID;
+  if (in->key_bytes == 4) return merge_linear<uint32_t>(in, out);
   return in->key_bytes == 8 ? merge_linear<uint64_t>(in, out) : merge_linear<K16>(in, out);
 }
 
 int dmo_merge_definitional(const dmo_in* in, dmo_out* out) {
   if (!args_ok(in, out)) return DMO_E_INVALID;
+  if (in->key_bytes == 4) return merge_definitional<uint32_t>(in, out);
   return in->key_bytes == 8 ? merge_definitional<uint64_t>(in, out) : merge_definitional<K16>(in, out);
 }
 
@@ -280,6 +282,10 @@ int dmo_codes_at(uint32_t key_bytes, const void* main_dict, uint64_t dict_len, c
   if (key_bytes == 8)
     return codes_at<uint64_t>(static_cast<const uint64_t*>(main_dict), dict_len,
                               static_cast<const uint64_t*>(delta), n_delta, static_cast<const uint64_t*>(values),
+                              n_values, codes, merged_len);
+  if (key_bytes == 4)
+    return codes_at<uint32_t>(static_cast<const uint32_t*>(main_dict), dict_len,
+                              static_cast<const uint32_t*>(delta), n_delta, static_cast<const uint32_t*>(values),
                               n_values, codes, merged_len);
   if (key_bytes == 16)
     return codes_at<K16>(static_cast<const K16*>(main_dict), dict_len, static_cast<const K16*>(delta), n_delta,

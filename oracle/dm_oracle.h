@@ -17,8 +17,8 @@
  *   - codes are 0-based dictionary positions              (A2)
  *   - packed vectors are LSB-first bitstreams in little-endian u64 words,
  *     exactly ceil(n*w/64) words, pad bits zero            (A4)
- *   - 8-byte keys: unsigned integers; 16-byte keys: raw bytes compared with
- *     memcmp over all 16 bytes                             (A5)
+ *   - 4- and 8-byte keys: unsigned integers; 16-byte keys: raw bytes compared
+ *     with memcmp over all 16 bytes                        (A5)
  */
 #ifndef DM_ORACLE_H
 #define DM_ORACLE_H
@@ -37,7 +37,7 @@ enum {
 };
 
 typedef struct {
-  uint32_t key_bytes;          /* 8 or 16                                      */
+  uint32_t key_bytes;          /* 4, 8 or 16                                   */
   const void* main_dict;       /* |U_M| keys, strictly increasing              */
   uint64_t dict_len;           /* |U_M|                                        */
   const uint64_t* main_words;  /* M packed at main_bits, ceil(n_main*b/64) words */

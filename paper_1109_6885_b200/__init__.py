@@ -9,7 +9,8 @@ the library's sm_100a kernels.  There is no CPU fallback: importing this
 package without the built library raises.
 
 Key tensors: ``"u64"`` keys are 1-D ``torch.int64`` tensors holding the u64 bit
-patterns (compared unsigned); ``"b16"`` keys are ``torch.uint8`` tensors of
+patterns (compared unsigned); ``"u32"`` keys (the paper's E = 4) are 1-D
+``torch.int32`` tensors holding u32 bit patterns; ``"b16"`` keys are ``torch.uint8`` tensors of
 shape (n, 16) (compared bytewise).  Packed code vectors are 1-D ``torch.int64``
 tensors of little-endian u64 words (LSB-first bitstream).
 """
@@ -30,8 +31,8 @@ __all__ = [
     "ColumnMerger", "HostContext", "launch_count", "lib_path", "set_tuning",
 ]
 
-KEY_U64, KEY_B16 = 0, 1
-_KEY = {"u64": KEY_U64, "b16": KEY_B16}
+KEY_U64, KEY_B16, KEY_U32 = 0, 1, 2
+_KEY = {"u64": KEY_U64, "b16": KEY_B16, "u32": KEY_U32}
 
 
 class Status:
@@ -128,11 +129,14 @@ def launch_count() -> int:
 
 
 XM_AUTO, XM_PLAIN, XM_COMPACT, XM_COMPACT_L2 = 0, 1, 2, 3
+KNOB_XMODE, KNOB_MERGE, KNOB_DEDUP, KNOB_STEP2 = 0, 1, 2, 3
 
 
 def set_tuning(knob: int, value: int) -> None:
-    """dm_set_tuning: knob 0 = Step 2(b) translation-table placement (XM_* above).
-    Never changes results; used by tests to force each kernel variant."""
+    """dm_set_tuning (include/dictmerge.h): knob 0 = Step 2(b) translation-table
+    placement (XM_* above), 1 = Step 1(b) variant, 2 = Step 1(a) dedup front end,
+    3 = Step 2 variant (1 = the paper's naive binary-search baseline).  Never
+    changes results; used by tests and experiments to select kernel variants."""
     st = _lib().dm_set_tuning(knob, value)
     if st != Status.OK:
         raise DictMergeError(st, "dm_set_tuning")
@@ -143,7 +147,9 @@ def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
 
 
 def _key_of(t: torch.Tensor) -> int:
-    return KEY_B16 if (t.dtype == torch.uint8 and t.dim() == 2) else KEY_U64
+    if t.dtype == torch.uint8 and t.dim() == 2:
+        return KEY_B16
+    return KEY_U32 if t.dtype == torch.int32 else KEY_U64
 
 
 def _make_in(main_dict, main_codes, n_main, main_bits, delta) -> _In:
@@ -168,6 +174,8 @@ def _stream_handle(stream) -> Optional[int]:
 def _empty_keys(key: int, n: int, device) -> torch.Tensor:
     if key == KEY_U64:
         return torch.empty(max(n, 2), dtype=torch.int64, device=device)
+    if key == KEY_U32:
+        return torch.empty(max(n, 4), dtype=torch.int32, device=device)
     return torch.empty((max(n, 1), 16), dtype=torch.uint8, device=device)
 
 

@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(kUniqThreads) k_unique(const void* __restrict_
     const uint64_t p = wbase + (uint64_t)i * 32 + lane;
     // previous element: lane-1 of this item, lane 31 of the previous item, or `before`
     K prev;
-    if constexpr (sizeof(K) == 8) {
+    if constexpr (sizeof(K) <= 8) {
       uint64_t up = __shfl_up_sync(FULL, (uint64_t)key[i], 1);
       uint64_t last = i > 0 ? __shfl_sync(FULL, (uint64_t)key[i > 0 ? i - 1 : 0], 31) : (uint64_t)before;
       if (i == 0) last = __shfl_sync(FULL, (uint64_t)before, 0);
@@ -474,7 +474,7 @@ cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, void* udict
   const int hist_blocks = (int)std::min<uint64_t>((n + 4095) / 4096, 148 * 4);
   k_hist<KT><<<hist_blocks, 256, 0, st>>>(D, n, n_dev, hist, counters + CNT_HIST, plan);
   note_launch();
-  constexpr bool U64 = KT::kBytes == 8;
+  constexpr bool U64 = KT::kBytes <= 8;  // tile shape: 8-byte and 4-byte keys alike
   switch (sort_variant()) {  // must match sort_tile_keys() (workspace layout)
     case 1: launch_passes<KT, 256, U64 ? 16 : 8>(D, n, n_dev, ws, L, plan, counters, st); break;
     case 2: launch_passes<KT, 256, U64 ? 8 : 4>(D, n, n_dev, ws, L, plan, counters, st); break;
@@ -501,8 +501,11 @@ cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, void* udict
 cudaError_t launch_delta_dictionary(const dm_column_in* in, char* ws, const WsLayout& L, void* udict, uint32_t* rank,
                                     dm_header* hdr, cudaStream_t st) {
   if (in->n_delta == 0) return cudaSuccess;
-  return in->key == DM_KEY_U64 ? run<KeyU64>(in, ws, L, udict, rank, hdr, st)
-                               : run<KeyB16>(in, ws, L, udict, rank, hdr, st);
+  switch (in->key) {
+    case DM_KEY_U64: return run<KeyU64>(in, ws, L, udict, rank, hdr, st);
+    case DM_KEY_U32: return run<KeyU32>(in, ws, L, udict, rank, hdr, st);
+    default: return run<KeyB16>(in, ws, L, udict, rank, hdr, st);
+  }
 }
 
 }  // namespace dm

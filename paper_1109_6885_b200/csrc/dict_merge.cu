@@ -673,8 +673,11 @@ cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, const void*
 
 cudaError_t launch_dictionary_merge(const dm_column_in* in, const dm_column_out* out, char* ws, const WsLayout& L,
                                     const void* udict, uint32_t* xm, uint32_t* xd, dm_header* hdr, cudaStream_t st) {
-  return in->key == DM_KEY_U64 ? run<KeyU64>(in, ws, L, udict, out->merged_dict, xm, xd, hdr, st)
-                               : run<KeyB16>(in, ws, L, udict, out->merged_dict, xm, xd, hdr, st);
+  switch (in->key) {
+    case DM_KEY_U64: return run<KeyU64>(in, ws, L, udict, out->merged_dict, xm, xd, hdr, st);
+    case DM_KEY_U32: return run<KeyU32>(in, ws, L, udict, out->merged_dict, xm, xd, hdr, st);
+    default: return run<KeyB16>(in, ws, L, udict, out->merged_dict, xm, xd, hdr, st);
+  }
 }
 
 }  // namespace dm

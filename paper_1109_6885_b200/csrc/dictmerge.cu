@@ -97,7 +97,8 @@ static int env_knob(const char* name, int hi) {
   const int v = s ? std::atoi(s) : 0;
   return (v >= 0 && v <= hi) ? v : 0;
 }
-static std::atomic<int> g_tuning[4] = {env_knob("DM_XMODE", 3), env_knob("DM_MERGE", 2), env_knob("DM_DEDUP", 2)};
+static std::atomic<int> g_tuning[4] = {env_knob("DM_XMODE", 3), env_knob("DM_MERGE", 2), env_knob("DM_DEDUP", 2),
+                                       env_knob("DM_STEP2", 1)};
 int tuning(int knob) { return (knob >= 0 && knob < 4) ? g_tuning[knob].load(std::memory_order_relaxed) : 0; }
 
 int sort_variant() {
@@ -111,16 +112,16 @@ int sort_variant() {
 
 uint64_t sort_tile_keys(int key) {
   const SortShape& s = kSortShapes[sort_variant()];
-  return (uint64_t)s.threads * (key == DM_KEY_U64 ? s.items_u64 : s.items_b16);
+  return (uint64_t)s.threads * (key == DM_KEY_B16 ? s.items_b16 : s.items_u64);
 }
 
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 WsLayout ws_layout(const dm_column_in* in) {
   WsLayout L{};
-  const size_t E = in->key == DM_KEY_U64 ? 8 : 16;
+  const size_t E = key_bytes(in->key);
   const uint64_t nD = in->n_delta;
-  L.npass = in->key == DM_KEY_U64 ? 8 : 16;
+  L.npass = (int)E;
   const uint64_t sort_tile = sort_tile_keys(in->key);
   L.ntiles_sort = (nD + sort_tile - 1) / sort_tile;
   L.ntiles_unique = (nD + kUniqThreads * kUniqItems - 1) / (kUniqThreads * kUniqItems);
@@ -179,7 +180,7 @@ static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 
 static dm_status validate(const dm_column_in* in, const dm_column_out* out, bool with_step2 = true) {
   if (!in || !out) return DM_E_INVALID;
-  if (in->key != DM_KEY_U64 && in->key != DM_KEY_B16) return DM_E_INVALID;
+  if (in->key != DM_KEY_U64 && in->key != DM_KEY_B16 && in->key != DM_KEY_U32) return DM_E_INVALID;
   if (in->main_bits < 1 || in->main_bits > 32) return DM_E_INVALID;
   if (in->dict_len >= (1ull << 32)) return DM_E_INVALID;
   if (in->n_delta >= (1ull << 30)) return DM_E_INVALID;
@@ -243,7 +244,9 @@ static dm_status merge_async(const dm_column_in* in, const dm_column_out* out, v
   mark(2);
   // Step 2(b): M' (Eq 11).
   const bool xc = xc_wanted(in->dict_len);
-  if (with_step2 && (e = launch_recompress(in, out, xm, xd, rank, d_header, st, 0,
+  if (with_step2 && tuning(3) == 1) {
+    if ((e = launch_naive_step2(in, out, d_header, st)) != cudaSuccess) return cuda_fail(e);
+  } else if (with_step2 && (e = launch_recompress(in, out, xm, xd, rank, d_header, st, 0,
                                            xc ? reinterpret_cast<const uint2*>(w + L.xc_rec) : nullptr,
                                            xc ? reinterpret_cast<const uint8_t*>(w + L.xc_offs) : nullptr,
                                            xc_shift(in))) !=
@@ -312,7 +315,8 @@ struct dm_ctx {
 extern "C" {
 
 int dm_set_tuning(int knob, int value) {
-  if (knob < 0 || knob > 2 || value < 0 || value > (knob == 0 ? 3 : 2)) return DM_E_INVALID;
+  static const int hi[4] = {3, 2, 2, 1};
+  if (knob < 0 || knob > 3 || value < 0 || value > hi[knob]) return DM_E_INVALID;
   g_tuning[knob].store(value);
   return DM_OK;
 }
@@ -499,7 +503,7 @@ dm_status dm_merge_column_host(dm_ctx* c, const dm_column_in* hin, dm_column_out
   cudaSetDevice(c->impl.device);
   auto& I = c->impl;
   cudaStream_t st = I.stream;
-  const size_t E = hin->key == DM_KEY_U64 ? 8 : 16;
+  const size_t E = key_bytes(hin->key);
   dm_column_in din = *hin;
   dm_column_out dout = *hout;
   const uint64_t in_words = host_words(hin->n_main, hin->main_bits);

@@ -65,6 +65,28 @@ struct KeyU64 {
   }
 };
 
+// 4-byte keys (NEXT4, the paper's E = 4 of Fig 8): little-endian u32,
+// unsigned numeric order.
+struct KeyU32 {
+  using K = uint32_t;
+  static constexpr int kBytes = 4;
+  static constexpr int kPasses = 4;
+  __device__ __forceinline__ static K load(const void* p, uint64_t i) {
+    return __ldg(static_cast<const uint32_t*>(p) + i);
+  }
+  __device__ __forceinline__ static void store(void* p, uint64_t i, K k) { static_cast<uint32_t*>(p)[i] = k; }
+  __device__ __forceinline__ static K load_cg(const void* p, uint64_t i) {
+    return __ldcg(static_cast<const uint32_t*>(p) + i);
+  }
+  __device__ __forceinline__ static uint32_t digit(K k, int pass) { return (k >> (8 * pass)) & 0xffu; }
+  __device__ __forceinline__ static bool lt(K a, K b) { return a < b; }
+  __device__ __forceinline__ static bool eq(K a, K b) { return a == b; }
+  __device__ __forceinline__ static bool le(K a, K b) { return a <= b; }
+  __device__ __forceinline__ static K ld_any(const void* p, uint64_t i, bool /*raw*/) {
+    return static_cast<const uint32_t*>(p)[i];
+  }
+};
+
 // 16-byte keys: raw bytes compared with memcmp (reading A5).  The numeric form
 // is the big-endian (hi, lo) pair, so (hi, lo) lexicographic == memcmp order.
 struct K128 {
@@ -109,6 +131,11 @@ template <>
 struct NumStore<KeyU64> {
   __device__ __forceinline__ static uint64_t ld(const void* p, uint64_t i) { return static_cast<const uint64_t*>(p)[i]; }
   __device__ __forceinline__ static void st(void* p, uint64_t i, uint64_t k) { static_cast<uint64_t*>(p)[i] = k; }
+};
+template <>
+struct NumStore<KeyU32> {
+  __device__ __forceinline__ static uint32_t ld(const void* p, uint64_t i) { return static_cast<const uint32_t*>(p)[i]; }
+  __device__ __forceinline__ static void st(void* p, uint64_t i, uint32_t k) { static_cast<uint32_t*>(p)[i] = k; }
 };
 template <>
 struct NumStore<KeyB16> {

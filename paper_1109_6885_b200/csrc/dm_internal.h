@@ -47,7 +47,8 @@ enum XMode { XM_RAW_GLOBAL = 0, XM_RAW_SMEM = 1, XM_XC_SMEM = 2, XM_XC_GLOBAL = 
 // Tuning knobs (dm_set_tuning): index 0 = X_M placement (0 auto, 1 plain only,
 // 2 compact (smem if it fits, else L2), 3 compact from L2); index 1 = Step 1(b)
 // variant (0 lean two-pass, 1 first three-phase form, 2 lean single pass);
-// index 2 = Step 1(a) dedup front end (0 auto, 1 off, 2 on).
+// index 2 = Step 1(a) dedup front end (0 auto, 1 off, 2 on); index 3 = Step 2
+// variant (0 optimized, 1 naive binary search, the paper's UnOpt baseline).
 int tuning(int knob);
 // Whether a merge builds XC at all: only when the plain X_M is too big for smem.
 inline bool xc_enabled(uint64_t dict_len) { return dict_len * 4 > kRecSmemXBytes; }
@@ -124,6 +125,7 @@ struct WsLayout {
 enum { CNT_SORT = 0, CNT_UNIQUE = 16, CNT_MERGE = 17, CNT_HIST = 18, CNT_DEDUP = 20 /* u64, 2 slots */ };
 
 WsLayout ws_layout(const dm_column_in* in);
+inline size_t key_bytes(int key) { return key == DM_KEY_U64 ? 8 : key == DM_KEY_U32 ? 4 : 16; }
 uint32_t host_width(uint64_t n);
 uint64_t host_words(uint64_t n, uint32_t bits);
 
@@ -150,6 +152,8 @@ cudaError_t launch_recompress(const dm_column_in* in, const dm_column_out* out, 
                               const uint32_t* xd, const uint32_t* rank, dm_header* hdr, cudaStream_t st,
                               uint32_t fixed_bits = 0, const uint2* xc_rec = nullptr,
                               const uint8_t* xc_offs = nullptr, uint32_t xc_shift = 8);
+// Naive Step 2: binary-search every tuple's value in U' (baseline).
+cudaError_t launch_naive_step2(const dm_column_in* in, const dm_column_out* out, dm_header* hdr, cudaStream_t st);
 cudaError_t launch_pack(const uint32_t* codes, uint64_t n, uint32_t bits, uint64_t* words, cudaStream_t st);
 cudaError_t launch_unpack(const uint64_t* words, uint64_t n, uint32_t bits, uint32_t* codes, cudaStream_t st);
 

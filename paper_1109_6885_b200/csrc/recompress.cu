@@ -296,6 +296,58 @@ __global__ void __launch_bounds__(rec_threads<XMODE>(), XMODE == XM_XC_SMEM ? 1 
   if (__any_sync(FULL, bad) && lane == 0) atomicMin(&hdr->status, (int)DM_E_CODE_RANGE);
 }
 
+// Naive Step 2 -- the paper's unoptimized algorithm ("UnOpt" of
+// Fig 7/8): for every tuple take its value (U_M[M[i]] for a main row, D[k] for
+// a delta row) and binary-search it in the merged dictionary U'.  No
+// translation tables; log2|U'| dependent gathers per tuple.  Kept as the
+// baseline for the optimized Step 2 (NEXT4, the paper's 9-10x claim).
+// One warp per 32-row group (grid-stride), codes packed by warp shuffles.
+template <class KT>
+__global__ void __launch_bounds__(256) k_naive_step2(const uint64_t* __restrict__ M, uint64_t n_main, uint32_t b,
+                                                     const void* __restrict__ UM, uint64_t dict_len,
+                                                     const void* __restrict__ D, uint64_t n_delta,
+                                                     const void* __restrict__ Up, uint64_t* __restrict__ Mout,
+                                                     dm_header* hdr) {
+  using K = typename KT::K;
+  const uint32_t nb = hdr->merged_bits;
+  const uint64_t nU = hdr->merged_dict_len, n_total = n_main + n_delta, ngroups = (n_total + 31) / 32;
+  const unsigned lane = lane_id();
+  const uint32_t pr0 = (32 * lane) / nb, pop = 32 * lane - pr0 * nb;
+  const uint32_t umask = b == 32 ? 0xffffffffu : ((1u << b) - 1);
+  const uint32_t* M32 = reinterpret_cast<const uint32_t*>(M);
+  const uint64_t nw32_in = 2 * dwords(n_main, b), nw32 = 2 * dwords(n_total, nb);
+  uint32_t* out32 = reinterpret_cast<uint32_t*>(Mout);
+  bool bad = false;
+  const uint64_t warp0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t g = warp0; g < ngroups; g += nwarps) {
+    const uint64_t row = g * 32 + lane;
+    K v{};
+    if (row < n_main) {
+      const uint64_t s0 = row * b, w = s0 >> 5;
+      const uint32_t lo = M32[w], hi = w + 1 < nw32_in ? M32[w + 1] : 0u;
+      uint32_t code = __funnelshift_r(lo, hi, (uint32_t)(s0 & 31)) & umask;
+      if (code >= dict_len) {
+        bad = true;
+        code = 0;
+      }
+      v = KT::load(UM, code);
+    } else if (row < n_total) {
+      v = KT::load(D, row - n_main);
+    }
+    uint64_t lo = 0, hi = nU;  // lower_bound(U', v)
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (KT::lt(KT::load(Up, mid), v)) lo = mid + 1; else hi = mid;
+    }
+    const uint32_t c = row < n_total ? (uint32_t)lo : 0u;
+    const uint32_t word = warp_pack<0>(c, nb, pr0, pop);
+    const uint64_t ow = g * nb + lane;
+    if (lane < nb && ow < nw32) out32[ow] = word;
+  }
+  if (__any_sync(FULL, bad) && lane == 0) atomicMin(&hdr->status, (int)DM_E_CODE_RANGE);
+}
+
 __global__ void __launch_bounds__(256) k_pack(const uint32_t* __restrict__ codes, uint64_t n, uint32_t bits,
                                               uint32_t* __restrict__ words32, uint64_t nw32) {
   const unsigned lane = lane_id();
@@ -425,6 +477,30 @@ cudaError_t launch_recompress(const dm_column_in* in, const dm_column_out* out, 
     return cudaSuccess;
   }
   return table[0](in, out, xm, xd, rank, hdr, st, 0, xc_rec, xc_offs, xc_shift);
+}
+
+cudaError_t launch_naive_step2(const dm_column_in* in, const dm_column_out* out, dm_header* hdr, cudaStream_t st) {
+  const uint64_t n_total = in->n_main + in->n_delta;
+  if (n_total == 0) return cudaSuccess;
+  const unsigned grid = (unsigned)std::min<uint64_t>((n_total + 255) / 256, (uint64_t)device_sms() * 16);
+  switch (in->key) {
+    case DM_KEY_U64:
+      k_naive_step2<KeyU64><<<grid, 256, 0, st>>>(in->main_codes, in->n_main, in->main_bits, in->main_dict,
+                                                  in->dict_len, in->delta, in->n_delta, out->merged_dict,
+                                                  out->merged_codes, hdr);
+      break;
+    case DM_KEY_U32:
+      k_naive_step2<KeyU32><<<grid, 256, 0, st>>>(in->main_codes, in->n_main, in->main_bits, in->main_dict,
+                                                  in->dict_len, in->delta, in->n_delta, out->merged_dict,
+                                                  out->merged_codes, hdr);
+      break;
+    default:
+      k_naive_step2<KeyB16><<<grid, 256, 0, st>>>(in->main_codes, in->n_main, in->main_bits, in->main_dict,
+                                                  in->dict_len, in->delta, in->n_delta, out->merged_dict,
+                                                  out->merged_codes, hdr);
+  }
+  note_launch();
+  return cudaGetLastError();
 }
 
 cudaError_t launch_pack(const uint32_t* codes, uint64_t n, uint32_t bits, uint64_t* words, cudaStream_t st) {

@@ -14,9 +14,10 @@ import oracle
 
 def to_device(col, dev="cuda"):
     import paper_1109_6885_b200 as dm
-    if col.key == "u64":
-        UM = torch.from_numpy(col.main_dict.view(np.int64).copy()).to(dev)
-        D = torch.from_numpy(col.delta.view(np.int64).copy()).to(dev)
+    if col.key in ("u64", "u32"):
+        it = np.int64 if col.key == "u64" else np.int32
+        UM = torch.from_numpy(col.main_dict.view(it).copy()).to(dev)
+        D = torch.from_numpy(col.delta.view(it).copy()).to(dev)
     else:
         UM = torch.from_numpy(np.ascontiguousarray(col.main_dict).reshape(-1, 16)).to(dev)
         D = torch.from_numpy(np.ascontiguousarray(col.delta).reshape(-1, 16)).to(dev)
@@ -27,7 +28,9 @@ def to_device(col, dev="cuda"):
 
 def keys_np(t: torch.Tensor, key: str) -> np.ndarray:
     a = t.cpu().numpy()
-    return a.view(np.uint64) if key == "u64" else a.reshape(-1, 16)
+    if key in ("u64", "u32"):
+        return a.view(np.uint64 if key == "u64" else np.uint32)
+    return a.reshape(-1, 16)
 
 
 def run_gpu(col, dev="cuda"):

@@ -103,3 +103,38 @@ def test_dedup_all_equal_and_zipf_strings(_reset_dedup):
     col.delta = np.repeat(col.main_dict[7:8], 70_000, axis=0)  # one value, 70k times
     M, r = run_gpu(col)
     compare(col, M, r)
+
+
+# ------------------------------------------- NEXT4: 4-byte keys and the naive Step 2
+@pytest.mark.parametrize("case", CASES)
+def test_u32_keys(case):
+    n_main, dict_len, n_delta, p_new = case
+    col = datagen.make_random_case(733 + n_delta, n_main, dict_len, n_delta, p_new, key="u32")
+    M, r = run_gpu(col)
+    compare(col, M, r)
+
+
+def test_u32_order_edges():
+    UM = np.array([0, 1, 2**31 - 1, 2**31, 2**32 - 2], dtype=np.uint32)
+    D = np.array([2**32 - 1, 2**31 + 1, 0, 5, 2**32 - 1, 2**31 - 1], dtype=np.uint32)
+    codes = np.arange(5, dtype=np.uint32).repeat(7)
+    col = datagen.Column("u32", UM, codes, 3, D)
+    M, r = run_gpu(col)
+    compare(col, M, r)
+
+
+@pytest.fixture()
+def _naive():
+    import paper_1109_6885_b200 as dm
+    dm.set_tuning(3, 1)
+    yield
+    dm.set_tuning(3, 0)
+
+
+@pytest.mark.parametrize("key", ["u64", "b16", "u32"])
+@pytest.mark.parametrize("case", CASES[:4] + [(100_003, 5000, 4097, 0.1)])
+def test_naive_step2(key, case, _naive):
+    n_main, dict_len, n_delta, p_new = case
+    col = datagen.make_random_case(97 + n_main, n_main, dict_len, n_delta, p_new, key=key)
+    M, r = run_gpu(col)
+    compare(col, M, r)

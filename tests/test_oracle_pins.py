@@ -37,7 +37,7 @@ class Col:
         self.main_bits = main_bits
         self.delta = delta
 
-    key_bytes = property(lambda s: 8 if s.key == "u64" else 16)
+    key_bytes = property(lambda s: {"u64": 8, "u32": 4}.get(s.key, 16))
     n_main = property(lambda s: int(s.main_codes.size))
 
 
@@ -52,7 +52,7 @@ def bigint_pack(codes, bits):
 
 
 def keys_as_tuples(a, key):
-    return [int(x) for x in a] if key == "u64" else [bytes(r) for r in a]
+    return [int(x) for x in a] if key in ("u64", "u32") else [bytes(r) for r in a]
 
 
 # ------------------------------------------------------------------------- P1
@@ -152,8 +152,9 @@ def brute(main_dict, main_codes, delta):
     return U, nb, codes, [U.index(v) for v in main_dict], [U.index(v) for v in UD], UD
 
 
-def _check_brute(mode, main_dict, main_codes, delta, bits):
-    col = Col("u64", np.array(main_dict, dtype=np.uint64), main_codes, bits, np.array(delta, dtype=np.uint64))
+def _check_brute(mode, main_dict, main_codes, delta, bits, key="u64"):
+    dt = np.uint64 if key == "u64" else np.uint32
+    col = Col(key, np.array(main_dict, dtype=dt), main_codes, bits, np.array(delta, dtype=dt))
     r = oracle.merge(col, mode)
     assert r.status == oracle.OK
     U, nb, codes, xm, xd, UD = brute(main_dict, main_codes, delta)
@@ -180,6 +181,23 @@ def test_p7_brute_force_exhaustive_tiny(mode):
                         _check_brute(mode, md, cs, list(dl), bits)
                         n += 1
     assert n > 1000
+
+
+@pytest.mark.parametrize("mode", ["linear", "definitional"])
+def test_p7_brute_force_exhaustive_tiny_u32(mode):
+    # 4-byte keys (NEXT4, E = 4): the same exhaustive sweep with u32 order edges
+    dom = [0, 3, 9, 2**31, 2**32 - 1]
+    n = 0
+    for k in range(0, 4):
+        for md in itertools.combinations(dom[:4], k):
+            md = list(md)
+            code_seqs = [[]] if not md else [list(s) for L in range(0, 3) for s in itertools.product(range(len(md)), repeat=L)]
+            for cs in code_seqs:
+                for L in range(0, 3):
+                    for dl in itertools.product(dom, repeat=L):
+                        _check_brute(mode, md, cs, list(dl), oracle.width(max(len(md), 1)), key="u32")
+                        n += 1
+    assert n > 500
 
 
 # -------------------------------------------------------------- P3/P4/P5 random
@@ -214,7 +232,7 @@ def _invariants(col, r):
         assert int(r.merged_words[-1]) >> (nbits % 64) == 0
 
 
-@pytest.mark.parametrize("key", ["u64", "b16"])
+@pytest.mark.parametrize("key", ["u64", "b16", "u32"])
 @pytest.mark.parametrize("seed", range(6))
 def test_p345_random_invariants_and_modes_agree(key, seed):
     rng = np.random.default_rng(seed)
@@ -223,7 +241,7 @@ def test_p345_random_invariants_and_modes_agree(key, seed):
         dict_len = int(rng.integers(1, 600))
         n_delta = int(rng.integers(0, 500))
         p_new = [0.0, 0.001, 0.01, 0.1, 0.5, 1.0][t % 6]
-        vb = int(rng.choice([10, 20, 64]))
+        vb = int(rng.choice([10, 20, 64 if key != "u32" else 32]))
         col = datagen.make_random_case(1000 * seed + t, n_main, dict_len, n_delta, p_new, key=key,
                                        value_bits=vb, main_bits=oracle.width(dict_len) + int(rng.integers(0, 3)))
         a = oracle.merge(col, "linear")
@@ -294,7 +312,7 @@ def test_b16_order_edges():
     assert want.index(b"\x7f" + b"\x00" * 15) < want.index(b"\x80" + b"\x00" * 15)
 
 
-@pytest.mark.parametrize("key", ["u64", "b16"])
+@pytest.mark.parametrize("key", ["u64", "b16", "u32"])
 def test_codes_at_agrees_with_full_merge(key):
     col = datagen.make_random_case(77, 3000, 500, 700, 0.4, key=key)
     r = oracle.merge(col, "definitional")
