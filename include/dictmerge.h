@@ -147,7 +147,8 @@ dm_status dm_merge_table(int ncols, const dm_column_in* in, dm_column_out* out, 
 dm_status dm_merge_table_async(int ncols, const dm_column_in* in, const dm_column_out* out, void* const* ws,
                                const size_t* ws_bytes, dm_header* const* d_headers, void* cuda_stream);
 
-/* Steps 1(a), 1(b) and 2(a) only (no M'): U', X_M, X_D, U_D, r and the header.
+/* Steps 1(a), 1(b) and 2(a) only (no M'): U', X_M, X_D, U_D, r, the header
+ * and (when |U_M| * 4 > 96 KB) the compact table XC in the workspace.
  * out->x_main, out->x_delta and out->delta_rank must be non-NULL;
  * out->merged_codes is ignored.  Used by the row-sharded Step 2 (each device
  * then runs dm_recompress on its row range).  Stream-ordered. */
@@ -165,6 +166,45 @@ dm_status dm_recompress(const uint64_t* main_codes, uint64_t n_main, uint32_t ma
                         const uint32_t* x_main, const uint32_t* x_delta, const uint32_t* delta_rank,
                         uint64_t n_delta, uint32_t new_bits, uint64_t* out_codes, uint64_t out_cap_words,
                         void* cuda_stream);
+
+/* Compact translation table XC (X_M[c] = c + #{new values
+ * inserted at or before main position c}, the closed form of X_M).
+ * Used by the row-sharded Step 2: the root's XC (|U_M|/2^(shift+2)
+ * 8-byte records + one byte per new value, ~67 MB for cfg5) is broadcast
+ * instead of X_M (4.3 GB).  Layout: record s = {u32 R | flag << 31, u32 four
+ * cumulative per-block counts}, R = #{new values with insertion point
+ * p <= s * 4 * 2^shift}; offsets[k] = (p_k - 1) mod 2^shift for the k-th new
+ * value in sorted order.  A flagged record (counts too large) means: read the
+ * plain X_M for that superblock. */
+typedef struct {
+  const void* records;     /* device, n_records * 8 bytes, 16-byte aligned      */
+  uint64_t n_records;      /* ceil(dict_len / (4 << shift))                      */
+  const uint8_t* offsets;  /* device, |U'| - |U_M| bytes used, 16-byte aligned  */
+  uint64_t offsets_cap;    /* bytes readable (n_delta + 16)                      */
+  uint32_t shift;          /* block = 2^shift codes (7 or 8)                     */
+  int32_t built;           /* 1 if a merge with this workspace builds XC        */
+} dm_xc;
+/* Describe the XC inside a workspace after dm_dictionary_merge_async (which
+ * builds it whenever |U_M| * 4 > 96 KB) -- pointers into `ws`, valid while it
+ * lives and until the next call on it.  Host, pure. */
+dm_status dm_xc_export(const dm_column_in* in, const void* ws, size_t ws_bytes, dm_xc* xc);
+/* Gather the X_M slices of flagged superblocks: for each, ids[slot] = its
+ * record index and slices[slot * 4 << shift ...] = its X_M entries; *d_count
+ * (device u64) = number of slots.  Capacities: ids n_records, slices
+ * n_records * (4 << shift).  Stream-ordered. */
+dm_status dm_xc_exceptions_gather(const dm_xc* xc, uint64_t dict_len, const uint32_t* x_main, uint32_t* ids,
+                                  uint32_t* slices, uint64_t* d_count, void* cuda_stream);
+/* The inverse on a receiving rank: write the `count` slices into x_main (a
+ * dict_len-entry buffer whose other entries are never read).  Stream-ordered. */
+dm_status dm_xc_exceptions_scatter(const dm_xc* xc, uint64_t dict_len, const uint32_t* ids, const uint32_t* slices,
+                                   uint64_t count, uint32_t* x_main, void* cuda_stream);
+/* dm_recompress with the main translation read from XC (L2); x_main is read
+ * only for flagged superblocks.  Same arguments and errors otherwise.
+ * Synchronous. */
+dm_status dm_recompress_xc(const uint64_t* main_codes, uint64_t n_main, uint32_t main_bits, uint64_t dict_len,
+                           const dm_xc* xc, const uint32_t* x_main, const uint32_t* x_delta,
+                           const uint32_t* delta_rank, uint64_t n_delta, uint32_t new_bits, uint64_t* out_codes,
+                           uint64_t out_cap_words, void* cuda_stream);
 
 /* Pack n u32 codes (each < 2^bits) into dm_words(n, bits) words at `bits`
  * (device pointers; words need not be zeroed).  Stream-ordered. */

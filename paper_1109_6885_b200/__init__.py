@@ -28,7 +28,8 @@ from . import build as _build
 __all__ = [
     "KEY_U64", "KEY_B16", "Status", "DictMergeError", "width", "words", "merged_codes_cap_words",
     "workspace_bytes", "merge_column", "merge_column_async", "merge_table", "pack_codes", "unpack_codes",
-    "ColumnMerger", "HostContext", "launch_count", "lib_path", "set_tuning",
+    "ColumnMerger", "HostContext", "launch_count", "lib_path", "set_tuning", "XcTables", "recompress_xc",
+    "xc_exceptions_gather", "xc_exceptions_scatter",
 ]
 
 KEY_U64, KEY_B16, KEY_U32 = 0, 1, 2
@@ -60,6 +61,11 @@ class _Out(ctypes.Structure):
                 ("x_main", ctypes.c_void_p), ("x_delta", ctypes.c_void_p), ("delta_dict", ctypes.c_void_p),
                 ("delta_rank", ctypes.c_void_p), ("merged_dict_len", ctypes.c_uint64),
                 ("delta_dict_len", ctypes.c_uint64), ("merged_bits", ctypes.c_uint32)]
+
+
+class _Xc(ctypes.Structure):
+    _fields_ = [("records", ctypes.c_void_p), ("n_records", ctypes.c_uint64), ("offsets", ctypes.c_void_p),
+                ("offsets_cap", ctypes.c_uint64), ("shift", ctypes.c_uint32), ("built", ctypes.c_int32)]
 
 
 class _Hdr(ctypes.Structure):
@@ -103,6 +109,10 @@ def _lib():
             "dm_merge_column_host": (i32, [vp, P(_In), P(_Out)]),
             "dm_launch_count": (u64, []),
             "dm_set_tuning": (i32, [i32, i32]),
+            "dm_xc_export": (i32, [P(_In), vp, ctypes.c_size_t, P(_Xc)]),
+            "dm_xc_exceptions_gather": (i32, [P(_Xc), u64, vp, vp, vp, vp, vp]),
+            "dm_xc_exceptions_scatter": (i32, [P(_Xc), u64, vp, vp, u64, vp, vp]),
+            "dm_recompress_xc": (i32, [vp, u64, u32, u64, P(_Xc), vp, vp, vp, u64, u32, vp, u64, vp]),
             "dm_last_cuda_error": (i32, []),
             "dm_status_str": (ctypes.c_char_p, [i32]),
         }
@@ -379,6 +389,78 @@ class DictionaryMerger:
     def header(self) -> _Hdr:
         raw = self.hdr.cpu().numpy().tobytes()
         return _Hdr.from_buffer_copy(raw[: ctypes.sizeof(_Hdr)])
+
+    def xc(self) -> Optional["XcTables"]:
+        """The compact table XC built by the last run (None when |U_M| * 4 <= 96 KB,
+        where the plain X_M is as small)."""
+        x = _Xc()
+        st = _lib().dm_xc_export(ctypes.byref(self.cin), self.ws.data_ptr(), self.ws_bytes, ctypes.byref(x))
+        if st != Status.OK:
+            raise DictMergeError(st, "dm_xc_export")
+        if not x.built:
+            return None
+        h = self.header()
+        n_new = int(h.merged_dict_len) - int(self.cin.dict_len)
+        base = self.ws.data_ptr()
+        r0 = x.records - base
+        o0 = x.offsets - base
+        return XcTables(self.ws[r0: r0 + x.n_records * 8], self.ws[o0: o0 + ((n_new + 31) // 16) * 16],
+                        int(x.shift), int(x.n_records))
+
+
+@dataclasses.dataclass
+class XcTables:
+    """The compact translation table XC of one merge (``dm_xc``): 8-byte records
+    and one offset byte per new value (include/dictmerge.h).  ``records`` and
+    ``offsets`` are uint8 device tensors (views into a workspace on the root, or
+    received copies on other ranks)."""
+    records: torch.Tensor
+    offsets: torch.Tensor
+    shift: int
+    n_records: int
+
+    def struct(self) -> _Xc:
+        return _Xc(_ptr(self.records), self.n_records, _ptr(self.offsets), self.offsets.numel(), self.shift, 1)
+
+
+def xc_exceptions_gather(xc: XcTables, dict_len: int, x_main: torch.Tensor, stream=None):
+    """X_M slices of XC's flagged superblocks -> (ids int32, slices int32, count)."""
+    dev = x_main.device
+    sb = 4 << xc.shift
+    ids = torch.empty(max(xc.n_records, 1), dtype=torch.int32, device=dev)
+    slices = torch.empty(max(xc.n_records * sb, 1), dtype=torch.int32, device=dev)
+    cnt = torch.zeros(2, dtype=torch.int64, device=dev)
+    st = _lib().dm_xc_exceptions_gather(ctypes.byref(xc.struct()), dict_len, _ptr(x_main), ids.data_ptr(),
+                                        slices.data_ptr(), cnt.data_ptr(), _stream_handle(stream))
+    if st != Status.OK:
+        raise DictMergeError(st, "dm_xc_exceptions_gather")
+    n = int(cnt[0].item())
+    return ids[:max(n, 1)], slices[: max(n * sb, 1)], n
+
+
+def xc_exceptions_scatter(xc: XcTables, dict_len: int, ids: torch.Tensor, slices: torch.Tensor, count: int,
+                          x_main: torch.Tensor, stream=None) -> None:
+    st = _lib().dm_xc_exceptions_scatter(ctypes.byref(xc.struct()), dict_len, _ptr(ids), _ptr(slices), count,
+                                         _ptr(x_main), _stream_handle(stream))
+    if st != Status.OK:
+        raise DictMergeError(st, "dm_xc_exceptions_scatter")
+
+
+def recompress_xc(main_codes: torch.Tensor, n_main: int, main_bits: int, dict_len: int, xc: XcTables,
+                  x_main: torch.Tensor, x_delta: torch.Tensor, delta_rank: torch.Tensor, n_delta: int,
+                  new_bits: int, stream=None) -> torch.Tensor:
+    """Step 2(b) of a row shard through XC (``dm_recompress_xc``); x_main is read
+    only for flagged superblocks."""
+    dev = xc.records.device
+    nw = words(n_main + n_delta, new_bits)
+    out = torch.empty(max(nw, 2), dtype=torch.int64, device=dev)
+    st = _lib().dm_recompress_xc(_ptr(main_codes) if n_main else None, n_main, main_bits, dict_len,
+                                 ctypes.byref(xc.struct()), _ptr(x_main), _ptr(x_delta) if n_delta else None,
+                                 _ptr(delta_rank) if n_delta else None, n_delta, new_bits, out.data_ptr(),
+                                 out.numel(), _stream_handle(stream))
+    if st != Status.OK:
+        raise DictMergeError(st, "dm_recompress_xc")
+    return out[:nw]
 
 
 def recompress(main_codes: torch.Tensor, n_main: int, main_bits: int, dict_len: int, x_main: torch.Tensor,

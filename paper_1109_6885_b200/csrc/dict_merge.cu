@@ -21,6 +21,8 @@
 // Measured alternatives: a per-thread co-rank + serial merge (the CPU pattern)
 // cost ~160 instructions per element; a single pass with decoupled look-back
 // was 1% faster on cfg2 but 11% slower on cfg5 (look-back chains at 5e5 tiles).
+#include <algorithm>
+
 #include "dm_device.cuh"
 
 namespace dm {
@@ -595,6 +597,41 @@ __global__ void __launch_bounds__(256) k_xc_records(const uint32_t* __restrict__
   rec[sb] = make_uint2(R0 | (flag << 31), cum);
 }
 
+// XC exception list (row-sharded Step 2): one warp per superblock; a flagged
+// superblock's X_M slice (4 * 2^xs entries) moves between X_M and a compact
+// slices[] array at slot ids[] (gather: slot from an atomic counter).
+__global__ void __launch_bounds__(256) k_xc_exceptions(bool gather, const uint2* __restrict__ rec, uint64_t nsb,
+                                                       uint32_t xs, uint64_t dict_len, uint32_t* __restrict__ xm,
+                                                       uint32_t* __restrict__ ids, uint32_t* __restrict__ slices,
+                                                       unsigned long long* d_count, uint64_t count) {
+  const unsigned lane = lane_id();
+  const uint64_t warp0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t SB = 4ull << xs;
+  const uint64_t n_items = gather ? nsb : count;
+  for (uint64_t w = warp0; w < n_items; w += nwarps) {
+    uint64_t sb, slot;
+    if (gather) {
+      if (!(rec[w].x >> 31)) continue;
+      unsigned long long sl = 0;
+      if (lane == 0) sl = atomicAdd(d_count, 1ull);
+      slot = __shfl_sync(FULL, sl, 0);
+      sb = w;
+      if (lane == 0) ids[slot] = (uint32_t)sb;
+    } else {
+      slot = w;
+      sb = ids[w];
+    }
+    const uint64_t c0 = sb * SB, n = umin64(SB, dict_len - c0);
+    for (uint64_t i = lane; i < n; i += 32) {
+      if (gather)
+        slices[slot * SB + i] = xm[c0 + i];
+      else
+        xm[c0 + i] = slices[slot * SB + i];
+    }
+  }
+}
+
 __global__ void k_empty_header(dm_header* hdr) {
   // |U_M| + |U_D| == 0: U' is empty and b' = 1 (reading A1)
   if (hdr->delta_dict_len == 0) {
@@ -605,7 +642,7 @@ __global__ void k_empty_header(dm_header* hdr) {
 
 template <class KT>
 cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, const void* udict, void* U, uint32_t* xm,
-                uint32_t* xd, dm_header* hdr, cudaStream_t st) {
+                uint32_t* xd, dm_header* hdr, cudaStream_t st, bool force_xc) {
   using K = typename KT::K;
   if (in->dict_len + in->n_delta == 0) {
     k_empty_header<<<1, 1, 0, st>>>(hdr);
@@ -614,7 +651,7 @@ cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, const void*
   }
   const uint64_t nt = L.ntiles_merge;
   uint64_t* part = reinterpret_cast<uint64_t*>(ws + L.part);
-  const bool xc = xc_wanted(in->dict_len);
+  const bool xc = xc_wanted(in->dict_len) || (force_xc && xc_enabled(in->dict_len));
   uint32_t* rblk = xc ? reinterpret_cast<uint32_t*>(ws + L.xc_rblk) : nullptr;
   uint8_t* offs = xc ? reinterpret_cast<uint8_t*>(ws + L.xc_offs) : nullptr;
   const uint32_t xs = xc_shift(in);
@@ -671,12 +708,24 @@ cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, const void*
 
 }  // namespace
 
+cudaError_t launch_xc_exceptions(bool gather, const uint2* rec, uint64_t nsb, uint32_t xs, uint64_t dict_len,
+                                 uint32_t* xm, uint32_t* ids, uint32_t* slices, unsigned long long* d_count,
+                                 uint64_t count, cudaStream_t st) {
+  const uint64_t items = gather ? nsb : count;
+  if (items == 0) return cudaSuccess;
+  const unsigned grid = (unsigned)std::min<uint64_t>((items + 7) / 8, (uint64_t)device_sms() * 16);
+  k_xc_exceptions<<<grid, 256, 0, st>>>(gather, rec, nsb, xs, dict_len, xm, ids, slices, d_count, count);
+  note_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_dictionary_merge(const dm_column_in* in, const dm_column_out* out, char* ws, const WsLayout& L,
-                                    const void* udict, uint32_t* xm, uint32_t* xd, dm_header* hdr, cudaStream_t st) {
+                                    const void* udict, uint32_t* xm, uint32_t* xd, dm_header* hdr, cudaStream_t st,
+                                    bool force_xc) {
   switch (in->key) {
-    case DM_KEY_U64: return run<KeyU64>(in, ws, L, udict, out->merged_dict, xm, xd, hdr, st);
-    case DM_KEY_U32: return run<KeyU32>(in, ws, L, udict, out->merged_dict, xm, xd, hdr, st);
-    default: return run<KeyB16>(in, ws, L, udict, out->merged_dict, xm, xd, hdr, st);
+    case DM_KEY_U64: return run<KeyU64>(in, ws, L, udict, out->merged_dict, xm, xd, hdr, st, force_xc);
+    case DM_KEY_U32: return run<KeyU32>(in, ws, L, udict, out->merged_dict, xm, xd, hdr, st, force_xc);
+    default: return run<KeyB16>(in, ws, L, udict, out->merged_dict, xm, xd, hdr, st, force_xc);
   }
 }
 

@@ -101,6 +101,15 @@ static std::atomic<int> g_tuning[4] = {env_knob("DM_XMODE", 3), env_knob("DM_MER
                                        env_knob("DM_STEP2", 1)};
 int tuning(int knob) { return (knob >= 0 && knob < 4) ? g_tuning[knob].load(std::memory_order_relaxed) : 0; }
 
+int xc_shift_override() {
+  static const int v = [] {
+    const char* e = std::getenv("DM_XC_SHIFT");
+    const int x = e ? std::atoi(e) : 0;
+    return (x == 7 || x == 8) ? x : 0;
+  }();
+  return v;
+}
+
 int sort_variant() {
   static const int v = [] {
     const char* s = std::getenv("DM_SORT_CFG");
@@ -239,7 +248,8 @@ static dm_status merge_async(const dm_column_in* in, const dm_column_out* out, v
   if ((e = dbg("step 1(a)")) != cudaSuccess) return cuda_fail(e);
   mark(1);
   // Step 1(b) + 2(a): U', X_M, X_D, b' (Eq 4).
-  if ((e = launch_dictionary_merge(in, out, w, L, udict, xm, xd, d_header, st)) != cudaSuccess) return cuda_fail(e);
+  if ((e = launch_dictionary_merge(in, out, w, L, udict, xm, xd, d_header, st, !with_step2)) != cudaSuccess)
+    return cuda_fail(e);
   if ((e = dbg("step 1(b)")) != cudaSuccess) return cuda_fail(e);
   mark(2);
   // Step 2(b): M' (Eq 11).
@@ -262,7 +272,15 @@ struct StreamPool {
   std::vector<cudaEvent_t> join;
   cudaEvent_t fork = nullptr;
 };
-constexpr int kTableStreams = 16;
+// Stream-pool size for dm_merge_table (DM_TABLE_STREAMS overrides; experiments).
+static int table_streams() {
+  static const int v = [] {
+    const char* e = std::getenv("DM_TABLE_STREAMS");
+    const int x = e ? std::atoi(e) : 16;
+    return (x >= 1 && x <= 128) ? x : 16;
+  }();
+  return v;
+}
 
 static StreamPool& stream_pool() {
   static std::mutex mu;
@@ -273,7 +291,7 @@ static StreamPool& stream_pool() {
   StreamPool& p = pools[dev];
   if (p.streams.empty()) {
     cudaEventCreateWithFlags(&p.fork, cudaEventDisableTiming);
-    for (int k = 0; k < kTableStreams; ++k) {
+    for (int k = 0; k < table_streams(); ++k) {
       cudaStream_t s;
       cudaEvent_t e;
       if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) break;
@@ -454,6 +472,83 @@ dm_status dm_recompress(const uint64_t* main_codes, uint64_t n_main, uint32_t ma
   out.merged_codes = out_codes;
   out.merged_codes_cap_words = out_cap_words;
   e = launch_recompress(&in, &out, x_main, x_delta, delta_rank, d_hdr, st, new_bits);
+  dm_header h{};
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&h, d_hdr, sizeof(h), cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(d_hdr, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e);
+  return (dm_status)h.status;
+}
+
+dm_status dm_xc_export(const dm_column_in* in, const void* ws, size_t ws_bytes, dm_xc* xc) {
+  if (!in || !xc) return DM_E_INVALID;
+  const WsLayout L = ws_layout(in);
+  if (!ws || ws_bytes < L.total) return DM_E_CAPACITY;
+  const char* w = static_cast<const char*>(ws);
+  const uint32_t xs = xc_shift(in);
+  xc->records = w + L.xc_rec;
+  xc->n_records = xc_nsb(in->dict_len, xs);
+  xc->offsets = reinterpret_cast<const uint8_t*>(w + L.xc_offs);
+  xc->offsets_cap = in->n_delta + 16;
+  xc->shift = xs;
+  xc->built = xc_enabled(in->dict_len) ? 1 : 0;
+  return DM_OK;
+}
+
+dm_status dm_xc_exceptions_gather(const dm_xc* xc, uint64_t dict_len, const uint32_t* x_main, uint32_t* ids,
+                                  uint32_t* slices, uint64_t* d_count, void* cuda_stream) {
+  if (!xc || !xc->records || (xc->shift != 7 && xc->shift != 8) || !d_count) return DM_E_INVALID;
+  if (xc->n_records && (!x_main || !ids || !slices)) return DM_E_INVALID;
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  cudaError_t e = cudaMemsetAsync(d_count, 0, sizeof(uint64_t), st);
+  if (e == cudaSuccess)
+    e = launch_xc_exceptions(true, static_cast<const uint2*>(xc->records), xc->n_records, xc->shift, dict_len,
+                             const_cast<uint32_t*>(x_main), ids, slices,
+                             reinterpret_cast<unsigned long long*>(d_count), 0, st);
+  return e == cudaSuccess ? DM_OK : cuda_fail(e);
+}
+
+dm_status dm_xc_exceptions_scatter(const dm_xc* xc, uint64_t dict_len, const uint32_t* ids, const uint32_t* slices,
+                                   uint64_t count, uint32_t* x_main, void* cuda_stream) {
+  if (!xc || (xc->shift != 7 && xc->shift != 8)) return DM_E_INVALID;
+  if (count && (!x_main || !ids || !slices)) return DM_E_INVALID;
+  cudaError_t e = launch_xc_exceptions(false, nullptr, xc->n_records, xc->shift, dict_len, x_main,
+                                       const_cast<uint32_t*>(ids), const_cast<uint32_t*>(slices), nullptr, count,
+                                       static_cast<cudaStream_t>(cuda_stream));
+  return e == cudaSuccess ? DM_OK : cuda_fail(e);
+}
+
+dm_status dm_recompress_xc(const uint64_t* main_codes, uint64_t n_main, uint32_t main_bits, uint64_t dict_len,
+                           const dm_xc* xc, const uint32_t* x_main, const uint32_t* x_delta,
+                           const uint32_t* delta_rank, uint64_t n_delta, uint32_t new_bits, uint64_t* out_codes,
+                           uint64_t out_cap_words, void* cuda_stream) {
+  if (main_bits < 1 || main_bits > 32 || new_bits < 1 || new_bits > 32) return DM_E_INVALID;
+  if (!xc || !xc->built || (xc->shift != 7 && xc->shift != 8)) return DM_E_INVALID;
+  if (xc->n_records != xc_nsb(dict_len, xc->shift)) return DM_E_INVALID;
+  if (n_main && (!main_codes || !x_main || !xc->records || !xc->offsets || !aligned16(main_codes) ||
+                 !aligned16(xc->records) || !aligned16(xc->offsets)))
+    return DM_E_INVALID;
+  if (n_delta && (!x_delta || !delta_rank)) return DM_E_INVALID;
+  const uint64_t need = host_words(n_main + n_delta, new_bits);
+  if (need && (!out_codes || !aligned16(out_codes))) return DM_E_INVALID;
+  if (out_cap_words < need) return DM_E_CAPACITY;
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  dm_header* d_hdr = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&d_hdr), sizeof(dm_header), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(d_hdr, 0, sizeof(dm_header), st);
+  if (e != cudaSuccess) return cuda_fail(e);
+  dm_column_in in{};
+  in.key = DM_KEY_U64;
+  in.dict_len = dict_len;
+  in.main_codes = main_codes;
+  in.n_main = n_main;
+  in.main_bits = main_bits;
+  in.n_delta = n_delta;
+  dm_column_out out{};
+  out.merged_codes = out_codes;
+  out.merged_codes_cap_words = out_cap_words;
+  e = launch_recompress_xc(&in, &out, x_main, x_delta, delta_rank, d_hdr, st, new_bits,
+                           static_cast<const uint2*>(xc->records), xc->offsets, xc->shift);
   dm_header h{};
   if (e == cudaSuccess) e = cudaMemcpyAsync(&h, d_hdr, sizeof(h), cudaMemcpyDeviceToHost, st);
   cudaFreeAsync(d_hdr, st);

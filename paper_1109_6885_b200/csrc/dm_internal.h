@@ -66,7 +66,9 @@ inline bool dedup_wanted(const dm_column_in* in) {
 }
 // Block shift: 256-code blocks when N_D / |U_M| promises <= 6 entries per block
 // (and always for the shared-memory variant, knob 2), else 128-code blocks.
+int xc_shift_override();  // DM_XC_SHIFT (experiments), 0 = none
 inline uint32_t xc_shift(const dm_column_in* in) {
+  if (const int o = xc_shift_override()) return (uint32_t)o;
   if (tuning(0) == 2) return 8;
   return in->n_delta * 256 <= 6 * in->dict_len ? 8u : 7u;
 }
@@ -143,8 +145,10 @@ cudaError_t launch_delta_dictionary(const dm_column_in* in, char* ws, const WsLa
                                     dm_header* hdr, cudaStream_t st);
 // Step 1(b) + 2(a): merge-path merge -> U', X_M, X_D, hdr->merged_dict_len / merged_bits.
 // When xc_enabled(dict_len), also builds the compact table XC in the workspace.
+// force_xc: build XC whenever xc_enabled (the row-sharded root exports it).
 cudaError_t launch_dictionary_merge(const dm_column_in* in, const dm_column_out* out, char* ws, const WsLayout& L,
-                                    const void* udict, uint32_t* xm, uint32_t* xd, dm_header* hdr, cudaStream_t st);
+                                    const void* udict, uint32_t* xm, uint32_t* xd, dm_header* hdr, cudaStream_t st,
+                                    bool force_xc = false);
 // Step 2(b): recompress main through X_M and append delta through X_D.
 // fixed_bits != 0: b' given by the caller (dm_recompress); else read from hdr->merged_bits.
 // xc_rec / xc_offs: the compact table (NULL: plain X_M only).
@@ -152,6 +156,15 @@ cudaError_t launch_recompress(const dm_column_in* in, const dm_column_out* out, 
                               const uint32_t* xd, const uint32_t* rank, dm_header* hdr, cudaStream_t st,
                               uint32_t fixed_bits = 0, const uint2* xc_rec = nullptr,
                               const uint8_t* xc_offs = nullptr, uint32_t xc_shift = 8);
+// Step 2(b) of a row shard through XC read from L2 (dm_recompress_xc).
+cudaError_t launch_recompress_xc(const dm_column_in* in, const dm_column_out* out, const uint32_t* xm,
+                                 const uint32_t* xd, const uint32_t* rank, dm_header* hdr, cudaStream_t st,
+                                 uint32_t bits, const uint2* xc_rec, const uint8_t* xc_offs, uint32_t xc_shift);
+// XC exception list: the X_M slices of flagged superblocks (gather on the root,
+// scatter on the receiving ranks).
+cudaError_t launch_xc_exceptions(bool gather, const uint2* rec, uint64_t nsb, uint32_t xs, uint64_t dict_len,
+                                 uint32_t* xm, uint32_t* ids, uint32_t* slices, unsigned long long* d_count,
+                                 uint64_t count, cudaStream_t st);
 // Naive Step 2: binary-search every tuple's value in U' (baseline).
 cudaError_t launch_naive_step2(const dm_column_in* in, const dm_column_out* out, dm_header* hdr, cudaStream_t st);
 cudaError_t launch_pack(const uint32_t* codes, uint64_t n, uint32_t bits, uint64_t* words, cudaStream_t st);

@@ -479,6 +479,24 @@ cudaError_t launch_recompress(const dm_column_in* in, const dm_column_out* out, 
   return table[0](in, out, xm, xd, rank, hdr, st, 0, xc_rec, xc_offs, xc_shift);
 }
 
+cudaError_t launch_recompress_xc(const dm_column_in* in, const dm_column_out* out, const uint32_t* xm,
+                                 const uint32_t* xd, const uint32_t* rank, dm_header* hdr, cudaStream_t st,
+                                 uint32_t bits, const uint2* xc_rec, const uint8_t* xc_offs, uint32_t xs) {
+  if (in->n_main + in->n_delta == 0) return cudaSuccess;
+  const uint32_t in_stage = kRecGroups * in->main_bits * 4 + 16;
+  const size_t smem = 128 + (size_t)kRecStages * in_stage;
+  const uint64_t n_total = in->n_main + in->n_delta;
+  const uint64_t nchunks = (n_total + 32ull * kRecGroups - 1) / (32ull * kRecGroups);
+  auto kern = k_recompress<0, XM_XC_GLOBAL>;
+  const int occ = occupancy((const void*)kern, kRecThreads, smem);
+  const unsigned grid = (unsigned)std::min<uint64_t>(nchunks, (uint64_t)device_sms() * occ);
+  kern<<<grid, kRecThreads, smem, st>>>(in->main_codes, in->n_main, in->main_bits, in->dict_len, xm, xd, rank,
+                                        in->n_delta, out->merged_codes, hdr, in_stage, bits, xc_rec, xc_offs, 0u, 0,
+                                        xs);
+  note_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_naive_step2(const dm_column_in* in, const dm_column_out* out, dm_header* hdr, cudaStream_t st) {
   const uint64_t n_total = in->n_main + in->n_delta;
   if (n_total == 0) return cudaSuccess;

@@ -11,8 +11,10 @@
   the input width b and the output width b' (4096·b and 4096·b' are multiples of
   64, and of 128 bits, so TMA bulk copies stay 16-byte aligned).
   ``sharded_merge_column`` runs Steps 1(a)/1(b)/2(a) on the root device,
-  broadcasts the header and the translation tables over NCCL (torch.distributed),
-  and every rank recompresses its own row range with ``dm_recompress``.
+  broadcasts the header and the translation tables over NCCL (torch.distributed)
+  -- by default the compact table XC (~67 MB for cfg5) instead of the literal X_M
+  (4.3 GB) -- and every rank recompresses its own row range with
+  ``dm_recompress_xc`` (or ``dm_recompress``).
 
 The planning functions are plain Python (tested with gloo on the CPU); the
 merge itself needs CUDA devices.
@@ -101,7 +103,7 @@ def plan_row_shards(n_main: int, n_delta: int, n_shards: int, align: int = ROW_A
 
 
 def sharded_merge_column(main_dict, main_codes_shard, n_main: int, main_bits: int, delta, shard: RowShard,
-                         group=None, root: int = 0):
+                         group=None, root: int = 0, tables: str = "xc"):
     """Row-sharded merge of one column across the ranks of `group` (one GPU each).
 
     Every rank passes its own packed main-code slice (`main_codes_shard`, the words
@@ -109,6 +111,11 @@ def sharded_merge_column(main_dict, main_codes_shard, n_main: int, main_bits: in
     (other ranks may pass empty tensors with the right dtype).  Returns this rank's
     packed output slice (rows [shard.row_begin, shard.row_end) at b'), b', |U'|, and
     on the root U' as well.
+
+    tables="xc" (default): the root broadcasts the compact table XC (8-byte records
+    + one byte per new value; ~67 MB for cfg5) and the X_M slices of the rare
+    flagged superblocks, instead of the literal X_M (4.3 GB for cfg5, SURVEY §8e's
+    control design, tables="plain").  X_D and r follow as before.
     """
     import torch
     import torch.distributed as dist
@@ -116,32 +123,54 @@ def sharded_merge_column(main_dict, main_codes_shard, n_main: int, main_bits: in
 
     rank = dist.get_rank(group)
     dev = torch.device("cuda", torch.cuda.current_device())
-    hdr = torch.zeros(4, dtype=torch.int64, device=dev)  # |U'|, |U_D|, b', |U_M|
-    U = None
+    # |U'|, |U_D|, b', |U_M|, N_D, use_xc, shift, n_records, offset bytes, exception count
+    hdr = torch.zeros(10, dtype=torch.int64, device=dev)
+    U = merger = xc = None
     if rank == root:
         merger = dm.DictionaryMerger(main_dict, n_main, main_bits, delta)
         merger.run_async()
         h = merger.header()
         if h.status != 0:
             raise dm.DictMergeError(h.status, "dm_dictionary_merge_async")
-        hdr.copy_(torch.tensor([h.merged_dict_len, h.delta_dict_len, h.merged_bits, main_dict.shape[0]],
-                               dtype=torch.int64))
         U = merger.U[: h.merged_dict_len]
+        xc = merger.xc() if tables == "xc" else None
+        exc = dm.xc_exceptions_gather(xc, main_dict.shape[0], merger.XM) if xc is not None else None
+        hdr.copy_(torch.tensor([h.merged_dict_len, h.delta_dict_len, h.merged_bits, main_dict.shape[0],
+                                delta.shape[0], int(xc is not None), xc.shift if xc else 0,
+                                xc.n_records if xc else 0, xc.offsets.numel() if xc else 0,
+                                exc[2] if exc else 0], dtype=torch.int64))
     dist.broadcast(hdr, src=root, group=group)
-    n_u, n_ud, nb, dict_len = (int(x) for x in hdr.tolist())
-    n_delta = int(delta.shape[0]) if rank == root else None
-    nd = torch.tensor([n_delta or 0], dtype=torch.int64, device=dev)
-    dist.broadcast(nd, src=root, group=group)
-    n_delta = int(nd.item())
-    xm = merger.XM[:dict_len] if rank == root else torch.empty(max(dict_len, 1), dtype=torch.int32, device=dev)
-    xd = merger.XD[: max(n_ud, 1)] if rank == root else torch.empty(max(n_ud, 1), dtype=torch.int32, device=dev)
-    rk = merger.R[: max(n_delta, 1)] if rank == root else torch.empty(max(n_delta, 1), dtype=torch.int32, device=dev)
-    # The literal translation tables (SURVEY §8e's control design); origin-flag
-    # broadcast with local expansion is the planned bandwidth-saving variant.
-    dist.broadcast(xm, src=root, group=group)
-    if n_delta:
-        dist.broadcast(xd, src=root, group=group)
-        dist.broadcast(rk, src=root, group=group)
-    out = dm.recompress(main_codes_shard, shard.n_main, main_bits, dict_len, xm, xd, rk[shard.delta_begin:],
-                        shard.n_delta, nb)
+    n_u, n_ud, nb, dict_len, n_delta, use_xc, shift, n_rec, n_off, n_exc = (int(x) for x in hdr.tolist())
+
+    def bcast(t_root, shape, dtype):
+        t = t_root if rank == root else torch.empty(shape, dtype=dtype, device=dev)
+        dist.broadcast(t, src=root, group=group)
+        return t
+
+    if use_xc:
+        rec = bcast(xc.records if xc else None, (n_rec * 8,), torch.uint8)
+        offs = bcast(xc.offsets if xc else None, (n_off,), torch.uint8)
+        tabs = dm.XcTables(rec, offs, shift, n_rec)
+        if rank == root:
+            xm = merger.XM[:dict_len]
+        else:
+            xm = torch.empty(max(dict_len, 1), dtype=torch.int32, device=dev)  # only exception slices are read
+        if n_exc:
+            sb = 4 << shift
+            ids = bcast(exc[0] if rank == root else None, (n_exc,), torch.int32)
+            sl = bcast(exc[1] if rank == root else None, (n_exc * sb,), torch.int32)
+            if rank != root:
+                dm.xc_exceptions_scatter(tabs, dict_len, ids, sl, n_exc, xm)
+    else:
+        xm = bcast(merger.XM[:dict_len] if rank == root else None, (max(dict_len, 1),), torch.int32)
+    xd = bcast(merger.XD[: max(n_ud, 1)] if rank == root else None, (max(n_ud, 1),), torch.int32) if n_delta \
+        else torch.empty(1, dtype=torch.int32, device=dev)
+    rk = bcast(merger.R[: max(n_delta, 1)] if rank == root else None, (max(n_delta, 1),), torch.int32) if n_delta \
+        else torch.empty(1, dtype=torch.int32, device=dev)
+    if use_xc:
+        out = dm.recompress_xc(main_codes_shard, shard.n_main, main_bits, dict_len, tabs, xm, xd,
+                               rk[shard.delta_begin:], shard.n_delta, nb)
+    else:
+        out = dm.recompress(main_codes_shard, shard.n_main, main_bits, dict_len, xm, xd, rk[shard.delta_begin:],
+                            shard.n_delta, nb)
     return out, nb, n_u, U

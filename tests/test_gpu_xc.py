@@ -136,3 +136,41 @@ def test_xc_no_new_values_and_all_new():
 def test_xc_configs_scaled(cfg):
     col = datagen.make_config(cfg, scale=0.1)
     _run_all_knobs(col)
+
+
+@pytest.mark.parametrize("key", ["u64", "u32"])
+def test_xc_row_shards_with_exceptions(key):
+    """Row-sharded Step 2 through XC (SURVEY §8e with NEXT3): the root's tables are
+    copied as a receiving rank would get them, and that rank's X_M holds only the
+    exception slices (flagged superblocks) -- every other entry is poisoned, so
+    any read outside the exceptions breaks parity."""
+    import paper_1109_6885_b200 as dm
+    from paper_1109_6885_b200 import sharding
+    from tests.parity import to_device
+    n = 1024 * 80 + 77
+    ins = [(0, 5), (1024 * 3 + 10, 32), (1024 * 5 + 300, 33), (1024 * 11 + 7, 40), (n - 1, 9), (n, 11)]
+    ins += _spread(n, 800, 12)
+    col = _column(n, 400_000, ins, 5000, seed=2, key="u64")
+    if key == "u32":
+        col = datagen.u32_column(col)
+    UM, M, D = to_device(col)
+    ref = oracle.merge(col)
+    dmg = dm.DictionaryMerger(UM, col.n_main, col.main_bits, D)
+    dmg.run_async()
+    h = dmg.header()
+    assert h.status == 0 and h.merged_bits == ref.merged_bits
+    xc = dmg.xc()
+    assert xc is not None
+    ids, sl, cnt = dm.xc_exceptions_gather(xc, col.dict_len, dmg.XM)
+    assert cnt >= 2  # the 33- and 40-insertion blocks
+    tabs = dm.XcTables(xc.records.clone(), xc.offsets.clone(), xc.shift, xc.n_records)
+    xm = torch.full((col.dict_len,), -1, dtype=torch.int32, device="cuda")
+    dm.xc_exceptions_scatter(tabs, col.dict_len, ids.clone(), sl.clone(), cnt, xm)
+    for g in (1, 3, 8):
+        parts = []
+        for s in sharding.plan_row_shards(col.n_main, col.n_delta, g):
+            mslice = M[s.in_word(col.main_bits):] if s.n_main else M
+            parts.append(dm.recompress_xc(mslice, s.n_main, col.main_bits, col.dict_len, tabs, xm, dmg.XD,
+                                          dmg.R[s.delta_begin:], s.n_delta, h.merged_bits))
+        got = torch.cat(parts).cpu().numpy().view(np.uint64)
+        assert np.array_equal(got, ref.merged_words), g

@@ -115,3 +115,48 @@ def test_gloo_two_rank_row_sharded_step2():
     for p in procs:
         p.join(timeout=60)
     assert ok and same_plan
+
+
+def _gpu_worker(rank, world, port, q, tables):
+    """One rank of sharded_merge_column on the (single) GPU: gloo carries the
+    broadcasts of CUDA tensors between the processes; no kernel waits on another
+    rank (every wait is a host-side collective)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1109_6885_b200 as dm  # noqa: F401
+        from tests.parity import to_device
+        torch.cuda.set_device(0)
+        col = datagen.make_random_case(34, 1 << 20, 1 << 16, 60001, 0.6, main_bits=18)
+        UM, M, D = to_device(col)
+        shard = sharding.plan_row_shards(col.n_main, col.n_delta, world)[rank]
+        mslice = M[shard.in_word(col.main_bits):] if shard.n_main else M
+        if rank != 0:
+            UM, D = UM[:0], D[:0]
+        out, nb, n_u, U = sharding.sharded_merge_column(UM, mslice, col.n_main, col.main_bits, D, shard,
+                                                        tables=tables)
+        gathered = [None] * world
+        dist.all_gather_object(gathered, out.cpu().numpy().view(np.uint64).tolist())
+        if rank == 0:
+            ref = oracle.merge(col)
+            full = np.array([w for part in gathered for w in part], dtype=np.uint64)
+            q.put(bool(np.array_equal(full, ref.merged_words)) and nb == ref.merged_bits and n_u == ref.merged_len)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tables", ["xc", "plain"])
+def test_sharded_merge_column_two_ranks_on_one_gpu(tables):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, q, tables)) for r in range(2)]
+    for p in procs:
+        p.start()
+    ok = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+    assert ok
