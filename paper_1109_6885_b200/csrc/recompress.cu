@@ -451,6 +451,14 @@ cudaError_t launch_nb(const dm_column_in* in, const dm_column_out* out, const ui
   return cudaGetLastError();
 }
 
+using XcKernel = void (*)(const uint64_t*, uint64_t, uint32_t, uint64_t, const uint32_t*, const uint32_t*,
+                         const uint32_t*, uint64_t, uint64_t*, dm_header*, uint32_t, uint32_t, const uint2*,
+                         const uint8_t*, uint32_t, int, uint32_t);
+template <int... I>
+constexpr auto make_xc_table(std::integer_sequence<int, I...>) {
+  return std::array<XcKernel, sizeof...(I)>{&k_recompress<I, XM_XC_GLOBAL>...};
+}
+
 using LaunchFn = cudaError_t (*)(const dm_column_in*, const dm_column_out*, const uint32_t*, const uint32_t*,
                                  const uint32_t*, dm_header*, cudaStream_t, uint32_t, const uint2*, const uint8_t*, uint32_t);
 template <int... I>
@@ -487,7 +495,8 @@ cudaError_t launch_recompress_xc(const dm_column_in* in, const dm_column_out* ou
   const size_t smem = 128 + (size_t)kRecStages * in_stage;
   const uint64_t n_total = in->n_main + in->n_delta;
   const uint64_t nchunks = (n_total + 32ull * kRecGroups - 1) / (32ull * kRecGroups);
-  auto kern = k_recompress<0, XM_XC_GLOBAL>;
+  static const auto xc_table = make_xc_table(std::make_integer_sequence<int, 33>{});
+  auto kern = xc_table[bits <= 32 ? bits : 0];  // width-specialised (same instantiations as launch_nb)
   const int occ = occupancy((const void*)kern, kRecThreads, smem);
   const unsigned grid = (unsigned)std::min<uint64_t>(nchunks, (uint64_t)device_sms() * occ);
   kern<<<grid, kRecThreads, smem, st>>>(in->main_codes, in->n_main, in->main_bits, in->dict_len, xm, xd, rank,
