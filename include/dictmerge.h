@@ -148,12 +148,37 @@ dm_status dm_merge_table_async(int ncols, const dm_column_in* in, const dm_colum
                                const size_t* ws_bytes, dm_header* const* d_headers, void* cuda_stream);
 
 /* Steps 1(a), 1(b) and 2(a) only (no M'): U', X_M, X_D, U_D, r, the header
- * and (when |U_M| * 4 > 96 KB) the compact table XC in the workspace.
+ * and (when |U_M| > 0) the compact table XC in the workspace.
  * out->x_main, out->x_delta and out->delta_rank must be non-NULL;
  * out->merged_codes is ignored.  Used by the row-sharded Step 2 (each device
  * then runs dm_recompress on its row range).  Stream-ordered. */
 dm_status dm_dictionary_merge_async(const dm_column_in* in, const dm_column_out* out, void* ws, size_t ws_bytes,
                                     dm_header* d_header, void* cuda_stream);
+
+/* Step 1(a) alone: U_D into out->delta_dict and r into out->delta_rank (both
+ * required when n_delta > 0), |U_D| into d_header.  The root's part of the
+ * sharded Step 1(b).  Stream-ordered. */
+dm_status dm_delta_dictionary_async(const dm_column_in* in, const dm_column_out* out, void* ws, size_t ws_bytes,
+                                    dm_header* d_header, void* cuda_stream);
+
+/* Steps 1(b) and 2(a) for a delta that already IS its dictionary: in->delta
+ * holds U_D itself (sorted, distinct -- the paper reads it off the CSB+ tree's
+ * leaves; the caller's promise, not checked).  X_D is over in->delta;
+ * out->delta_rank is not used; out->x_main and out->x_delta are required.
+ * Builds XC like dm_dictionary_merge_async.  One value range of the sharded
+ * Step 1(b) (NEXT2).  Stream-ordered. */
+dm_status dm_dictionary_merge_sorted_async(const dm_column_in* in, const dm_column_out* out, void* ws,
+                                           size_t ws_bytes, dm_header* d_header, void* cuda_stream);
+
+/* Sharded Step 1(b) helpers (NEXT2), stream-ordered, device pointers:
+ * pos[i] = #{sorted[j] < values[i]} (lower bound) for n_values values of type
+ * `key`; x[i] += add for n u32 entries (rebasing a range's X_M / X_D by the
+ * |U'| of earlier ranges); R += add in n_records XC records, flags kept
+ * (rebasing by the new values of earlier ranges). */
+dm_status dm_lower_bound_async(int key, const void* sorted, uint64_t n, const void* values, uint64_t n_values,
+                               uint64_t* pos, void* cuda_stream);
+dm_status dm_rebase_async(uint32_t* x, uint64_t n, uint32_t add, void* cuda_stream);
+dm_status dm_xc_rebase_async(void* records, uint64_t n_records, uint32_t add, void* cuda_stream);
 
 /* Step 2(b) alone (Eq 11): given translation tables, write
  * M'[i] = x_main[M[i]] for i < n_main and M'[n_main + k] = x_delta[delta_rank[k]]
@@ -184,9 +209,10 @@ typedef struct {
   uint32_t shift;          /* block = 2^shift codes (7 or 8)                     */
   int32_t built;           /* 1 if a merge with this workspace builds XC        */
 } dm_xc;
-/* Describe the XC inside a workspace after dm_dictionary_merge_async (which
- * builds it whenever |U_M| * 4 > 96 KB) -- pointers into `ws`, valid while it
- * lives and until the next call on it.  Host, pure. */
+/* Describe the XC inside a workspace after dm_dictionary_merge_async or
+ * dm_dictionary_merge_sorted_async (which always build it when |U_M| > 0) --
+ * pointers into `ws`, valid while it lives and until the next call on it.
+ * Host, pure. */
 dm_status dm_xc_export(const dm_column_in* in, const void* ws, size_t ws_bytes, dm_xc* xc);
 /* Gather the X_M slices of flagged superblocks: for each, ids[slot] = its
  * record index and slices[slot * 4 << shift ...] = its X_M entries; *d_count
@@ -243,8 +269,10 @@ dm_status dm_merge_column_host(dm_ctx* ctx, const dm_column_in* in, dm_column_ou
  * knob 3 = Step 2(b) variant: 0 (default) the optimized recompression through
  *   X_M / X_D (Eq 11); 1 the paper's unoptimized form:
  *   every tuple's value binary-searched in U' -- a measured baseline only.
- * The process starts with knobs 0..3 = $DM_XMODE / $DM_MERGE / $DM_DEDUP /
- * $DM_STEP2 when set (experiments), else 0.
+ * knob 4 = XC block shift: 0 (default) per column from N_D / |U_M|; 7 or 8
+ *   fixed (the sharded Step 1(b) needs one shift for all value ranges).
+ * The process starts with knobs 0..4 = $DM_XMODE / $DM_MERGE / $DM_DEDUP /
+ * $DM_STEP2 / $DM_XC_SHIFT when set (experiments), else 0.
  * Returns DM_OK, or DM_E_INVALID for an unknown knob or value.  Affects calls
  * made after it returns (a captured CUDA graph keeps the kernels it recorded). */
 int dm_set_tuning(int knob, int value);

@@ -29,7 +29,7 @@ __all__ = [
     "KEY_U64", "KEY_B16", "Status", "DictMergeError", "width", "words", "merged_codes_cap_words",
     "workspace_bytes", "merge_column", "merge_column_async", "merge_table", "pack_codes", "unpack_codes",
     "ColumnMerger", "HostContext", "launch_count", "lib_path", "set_tuning", "XcTables", "recompress_xc",
-    "xc_exceptions_gather", "xc_exceptions_scatter",
+    "xc_exceptions_gather", "xc_exceptions_scatter", "lower_bound", "rebase", "DictionaryMerger",
 ]
 
 KEY_U64, KEY_B16, KEY_U32 = 0, 1, 2
@@ -102,6 +102,11 @@ def _lib():
             "dm_merge_table": (i32, [i32, P(_In), P(_Out), P(vp), P(ctypes.c_size_t), vp]),
             "dm_merge_table_async": (i32, [i32, P(_In), P(_Out), P(vp), P(ctypes.c_size_t), P(vp), vp]),
             "dm_dictionary_merge_async": (i32, [P(_In), P(_Out), vp, ctypes.c_size_t, vp, vp]),
+            "dm_delta_dictionary_async": (i32, [P(_In), P(_Out), vp, ctypes.c_size_t, vp, vp]),
+            "dm_dictionary_merge_sorted_async": (i32, [P(_In), P(_Out), vp, ctypes.c_size_t, vp, vp]),
+            "dm_lower_bound_async": (i32, [i32, vp, u64, vp, u64, vp, vp]),
+            "dm_rebase_async": (i32, [vp, u64, u32, vp]),
+            "dm_xc_rebase_async": (i32, [vp, u64, u32, vp]),
             "dm_pack_codes": (i32, [vp, u64, u32, vp, vp]),
             "dm_unpack_codes": (i32, [vp, u64, u32, vp, vp]),
             "dm_ctx_create": (vp, [i32]),
@@ -139,7 +144,7 @@ def launch_count() -> int:
 
 
 XM_AUTO, XM_PLAIN, XM_COMPACT, XM_COMPACT_L2 = 0, 1, 2, 3
-KNOB_XMODE, KNOB_MERGE, KNOB_DEDUP, KNOB_STEP2 = 0, 1, 2, 3
+KNOB_XMODE, KNOB_MERGE, KNOB_DEDUP, KNOB_STEP2, KNOB_XC_SHIFT = 0, 1, 2, 3, 4
 
 
 def set_tuning(knob: int, value: int) -> None:
@@ -360,9 +365,19 @@ class TableMerger:
 
 class DictionaryMerger:
     """Steps 1(a), 1(b), 2(a) only (``dm_dictionary_merge_async``): U', X_M, X_D,
-    U_D, r and the header -- the root's part of the row-sharded merge."""
+    U_D, r and the header -- the root's part of the row-sharded merge.
 
-    def __init__(self, main_dict: torch.Tensor, n_main: int, main_bits: int, delta: torch.Tensor):
+    mode "delta": Step 1(a) alone (``dm_delta_dictionary_async``: U_D, r);
+    mode "sorted": ``delta`` already is U_D (sorted, distinct), Steps 1(b)/2(a)
+    only (``dm_dictionary_merge_sorted_async``) -- one value range of the
+    sharded Step 1(b)."""
+
+    _ENTRY = {"dict": "dm_dictionary_merge_async", "delta": "dm_delta_dictionary_async",
+              "sorted": "dm_dictionary_merge_sorted_async"}
+
+    def __init__(self, main_dict: torch.Tensor, n_main: int, main_bits: int, delta: torch.Tensor,
+                 mode: str = "dict"):
+        self.mode = mode
         dev = main_dict.device if main_dict.numel() else delta.device
         self.cin = _make_in(main_dict, None, n_main, main_bits, delta)
         self.cin.main_codes = None
@@ -381,10 +396,11 @@ class DictionaryMerger:
         self.inputs = (main_dict, delta)
 
     def run_async(self, stream=None) -> None:
-        st = _lib().dm_dictionary_merge_async(ctypes.byref(self.cin), ctypes.byref(self.cout), self.ws.data_ptr(),
-                                              self.ws_bytes, self.hdr.data_ptr(), _stream_handle(stream))
+        name = self._ENTRY[self.mode]
+        st = getattr(_lib(), name)(ctypes.byref(self.cin), ctypes.byref(self.cout), self.ws.data_ptr(),
+                                   self.ws_bytes, self.hdr.data_ptr(), _stream_handle(stream))
         if st != Status.OK:
-            raise DictMergeError(st, "dm_dictionary_merge_async")
+            raise DictMergeError(st, name)
 
     def header(self) -> _Hdr:
         raw = self.hdr.cpu().numpy().tobytes()
@@ -408,6 +424,25 @@ class DictionaryMerger:
                         int(x.shift), int(x.n_records))
 
 
+def lower_bound(sorted_keys: torch.Tensor, values: torch.Tensor, n: Optional[int] = None, stream=None) -> torch.Tensor:
+    """pos[i] = #{sorted_keys[j] < values[i]} (``dm_lower_bound_async``), int64."""
+    key = _key_of(sorted_keys if sorted_keys.numel() else values)
+    nv = values.shape[0]
+    pos = torch.empty(max(nv, 1), dtype=torch.int64, device=values.device)
+    st = _lib().dm_lower_bound_async(key, _ptr(sorted_keys), sorted_keys.shape[0] if n is None else n,
+                                     _ptr(values), nv, pos.data_ptr(), _stream_handle(stream))
+    if st != Status.OK:
+        raise DictMergeError(st, "dm_lower_bound_async")
+    return pos[:nv]
+
+
+def rebase(x: torch.Tensor, add: int, stream=None) -> None:
+    """x += add in place for an int32 tensor of u32 values (``dm_rebase_async``)."""
+    st = _lib().dm_rebase_async(_ptr(x), x.numel(), add, _stream_handle(stream))
+    if st != Status.OK:
+        raise DictMergeError(st, "dm_rebase_async")
+
+
 @dataclasses.dataclass
 class XcTables:
     """The compact translation table XC of one merge (``dm_xc``): 8-byte records
@@ -421,6 +456,12 @@ class XcTables:
 
     def struct(self) -> _Xc:
         return _Xc(_ptr(self.records), self.n_records, _ptr(self.offsets), self.offsets.numel(), self.shift, 1)
+
+    def rebase(self, add: int, stream=None) -> None:
+        """R += add in every record (``dm_xc_rebase_async``): new values of earlier ranges."""
+        st = _lib().dm_xc_rebase_async(_ptr(self.records), self.n_records, add, _stream_handle(stream))
+        if st != Status.OK:
+            raise DictMergeError(st, "dm_xc_rebase_async")
 
 
 def xc_exceptions_gather(xc: XcTables, dict_len: int, x_main: torch.Tensor, stream=None):

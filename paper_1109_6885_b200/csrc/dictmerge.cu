@@ -97,17 +97,13 @@ static int env_knob(const char* name, int hi) {
   const int v = s ? std::atoi(s) : 0;
   return (v >= 0 && v <= hi) ? v : 0;
 }
-static std::atomic<int> g_tuning[4] = {env_knob("DM_XMODE", 3), env_knob("DM_MERGE", 2), env_knob("DM_DEDUP", 2),
-                                       env_knob("DM_STEP2", 1)};
-int tuning(int knob) { return (knob >= 0 && knob < 4) ? g_tuning[knob].load(std::memory_order_relaxed) : 0; }
+static std::atomic<int> g_tuning[5] = {env_knob("DM_XMODE", 3), env_knob("DM_MERGE", 2), env_knob("DM_DEDUP", 2),
+                                       env_knob("DM_STEP2", 1), env_knob("DM_XC_SHIFT", 8)};
+int tuning(int knob) { return (knob >= 0 && knob < 5) ? g_tuning[knob].load(std::memory_order_relaxed) : 0; }
 
 int xc_shift_override() {
-  static const int v = [] {
-    const char* e = std::getenv("DM_XC_SHIFT");
-    const int x = e ? std::atoi(e) : 0;
-    return (x == 7 || x == 8) ? x : 0;
-  }();
-  return v;
+  const int x = tuning(4);  // knob 4 (DM_XC_SHIFT): the sharded Step 1(b) fixes one shift for all ranges
+  return (x == 7 || x == 8) ? x : 0;
 }
 
 int sort_variant() {
@@ -187,7 +183,12 @@ static dm_status cuda_fail(cudaError_t e) {
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-static dm_status validate(const dm_column_in* in, const dm_column_out* out, bool with_step2 = true) {
+// What one call runs: the whole merge, Steps 1(a)-2(a), Step 1(a) alone, or
+// Steps 1(b)-2(a) on a delta that already is U_D (sorted, distinct).
+enum MergeMode { MM_FULL = 0, MM_DICT = 1, MM_DELTA = 2, MM_SORTED_DICT = 3 };
+
+static dm_status validate(const dm_column_in* in, const dm_column_out* out, int mode = MM_FULL) {
+  const bool with_step2 = mode == MM_FULL;
   if (!in || !out) return DM_E_INVALID;
   if (in->key != DM_KEY_U64 && in->key != DM_KEY_B16 && in->key != DM_KEY_U32) return DM_E_INVALID;
   if (in->main_bits < 1 || in->main_bits > 32) return DM_E_INVALID;
@@ -206,9 +207,14 @@ static dm_status validate(const dm_column_in* in, const dm_column_out* out, bool
     const uint64_t need_words = dm_merged_codes_cap_words(in);
     if (need_words && (!out->merged_codes || !aligned16(out->merged_codes))) return DM_E_INVALID;
     if (out->merged_codes_cap_words < need_words) return DM_E_CAPACITY;
-  } else {
+  } else if (mode == MM_DICT) {
     if (in->dict_len && !out->x_main) return DM_E_INVALID;
     if (in->n_delta && (!out->x_delta || !out->delta_rank)) return DM_E_INVALID;
+  } else if (mode == MM_DELTA) {
+    if (in->n_delta && (!out->delta_dict || !out->delta_rank)) return DM_E_INVALID;
+  } else {  // MM_SORTED_DICT
+    if (in->dict_len && !out->x_main) return DM_E_INVALID;
+    if (in->n_delta && !out->x_delta) return DM_E_INVALID;
   }
   if (out->delta_dict && !aligned16(out->delta_dict)) return DM_E_INVALID;
   return DM_OK;
@@ -216,8 +222,9 @@ static dm_status validate(const dm_column_in* in, const dm_column_out* out, bool
 
 static dm_status merge_async(const dm_column_in* in, const dm_column_out* out, void* ws, size_t ws_bytes,
                              dm_header* d_header, cudaStream_t st, bool zero_header,
-                             void* const* events = nullptr, bool with_step2 = true) {
-  dm_status v = validate(in, out, with_step2);
+                             void* const* events = nullptr, int mode = MM_FULL) {
+  const bool with_step2 = mode == MM_FULL;
+  dm_status v = validate(in, out, mode);
   if (v != DM_OK) return v;
   const WsLayout L = ws_layout(in);
   if (!ws || ws_bytes < L.total) return DM_E_CAPACITY;
@@ -243,10 +250,18 @@ static dm_status merge_async(const dm_column_in* in, const dm_column_out* out, v
     if (x != cudaSuccess) fprintf(stderr, "dictmerge: %s failed: %s\n", step, cudaGetErrorString(x));
     return x;
   };
-  // Step 1(a): delta dictionary U_D and ranks r.
-  if ((e = launch_delta_dictionary(in, w, L, udict, rank, d_header, st)) != cudaSuccess) return cuda_fail(e);
+  // Step 1(a): delta dictionary U_D and ranks r -- or, for a
+  // delta that already is U_D (the paper reads it off the CSB+ tree's leaves,
+  // P:190), just its length.
+  if (mode == MM_SORTED_DICT) {
+    udict = const_cast<void*>(in->delta);
+    if ((e = launch_set_delta_len(d_header, in->n_delta, st)) != cudaSuccess) return cuda_fail(e);
+  } else if ((e = launch_delta_dictionary(in, w, L, udict, rank, d_header, st)) != cudaSuccess) {
+    return cuda_fail(e);
+  }
   if ((e = dbg("step 1(a)")) != cudaSuccess) return cuda_fail(e);
   mark(1);
+  if (mode == MM_DELTA) return DM_OK;
   // Step 1(b) + 2(a): U', X_M, X_D, b' (Eq 4).
   if ((e = launch_dictionary_merge(in, out, w, L, udict, xm, xd, d_header, st, !with_step2)) != cudaSuccess)
     return cuda_fail(e);
@@ -333,8 +348,9 @@ struct dm_ctx {
 extern "C" {
 
 int dm_set_tuning(int knob, int value) {
-  static const int hi[4] = {3, 2, 2, 1};
-  if (knob < 0 || knob > 3 || value < 0 || value > hi[knob]) return DM_E_INVALID;
+  static const int hi[5] = {3, 2, 2, 1, 8};
+  if (knob < 0 || knob > 4 || value < 0 || value > hi[knob]) return DM_E_INVALID;
+  if (knob == 4 && value != 0 && value != 7 && value != 8) return DM_E_INVALID;
   g_tuning[knob].store(value);
   return DM_OK;
 }
@@ -443,7 +459,40 @@ dm_status dm_merge_table_async(int ncols, const dm_column_in* in, const dm_colum
 
 dm_status dm_dictionary_merge_async(const dm_column_in* in, const dm_column_out* out, void* ws, size_t ws_bytes,
                                     dm_header* d_header, void* cuda_stream) {
-  return merge_async(in, out, ws, ws_bytes, d_header, static_cast<cudaStream_t>(cuda_stream), true, nullptr, false);
+  return merge_async(in, out, ws, ws_bytes, d_header, static_cast<cudaStream_t>(cuda_stream), true, nullptr,
+                     MM_DICT);
+}
+
+dm_status dm_delta_dictionary_async(const dm_column_in* in, const dm_column_out* out, void* ws, size_t ws_bytes,
+                                    dm_header* d_header, void* cuda_stream) {
+  return merge_async(in, out, ws, ws_bytes, d_header, static_cast<cudaStream_t>(cuda_stream), true, nullptr,
+                     MM_DELTA);
+}
+
+dm_status dm_dictionary_merge_sorted_async(const dm_column_in* in, const dm_column_out* out, void* ws,
+                                           size_t ws_bytes, dm_header* d_header, void* cuda_stream) {
+  return merge_async(in, out, ws, ws_bytes, d_header, static_cast<cudaStream_t>(cuda_stream), true, nullptr,
+                     MM_SORTED_DICT);
+}
+
+dm_status dm_lower_bound_async(int key, const void* sorted, uint64_t n, const void* values, uint64_t n_values,
+                               uint64_t* pos, void* cuda_stream) {
+  if (key != DM_KEY_U64 && key != DM_KEY_B16 && key != DM_KEY_U32) return DM_E_INVALID;
+  if (n_values && (!values || !pos || (n && !sorted))) return DM_E_INVALID;
+  cudaError_t e = launch_lower_bound(key, sorted, n, values, n_values, pos, static_cast<cudaStream_t>(cuda_stream));
+  return e == cudaSuccess ? DM_OK : cuda_fail(e);
+}
+
+dm_status dm_rebase_async(uint32_t* x, uint64_t n, uint32_t add, void* cuda_stream) {
+  if (n && !x) return DM_E_INVALID;
+  cudaError_t e = launch_add_u32(x, n, add, static_cast<cudaStream_t>(cuda_stream));
+  return e == cudaSuccess ? DM_OK : cuda_fail(e);
+}
+
+dm_status dm_xc_rebase_async(void* records, uint64_t n_records, uint32_t add, void* cuda_stream) {
+  if (n_records && (!records || !aligned16(records))) return DM_E_INVALID;
+  cudaError_t e = launch_xc_rebase(records, n_records, add, static_cast<cudaStream_t>(cuda_stream));
+  return e == cudaSuccess ? DM_OK : cuda_fail(e);
 }
 
 dm_status dm_recompress(const uint64_t* main_codes, uint64_t n_main, uint32_t main_bits, uint64_t dict_len,
@@ -491,7 +540,7 @@ dm_status dm_xc_export(const dm_column_in* in, const void* ws, size_t ws_bytes, 
   xc->offsets = reinterpret_cast<const uint8_t*>(w + L.xc_offs);
   xc->offsets_cap = in->n_delta + 16;
   xc->shift = xs;
-  xc->built = xc_enabled(in->dict_len) ? 1 : 0;
+  xc->built = in->dict_len > 0 ? 1 : 0;  // dictionary-only merges always build it
   return DM_OK;
 }
 

@@ -66,7 +66,7 @@ inline bool dedup_wanted(const dm_column_in* in) {
 }
 // Block shift: 256-code blocks when N_D / |U_M| promises <= 6 entries per block
 // (and always for the shared-memory variant, knob 2), else 128-code blocks.
-int xc_shift_override();  // DM_XC_SHIFT (experiments), 0 = none
+int xc_shift_override();  // knob 4 / DM_XC_SHIFT: 7 or 8, 0 = none
 inline uint32_t xc_shift(const dm_column_in* in) {
   if (const int o = xc_shift_override()) return (uint32_t)o;
   if (tuning(0) == 2) return 8;
@@ -165,6 +165,12 @@ cudaError_t launch_recompress_xc(const dm_column_in* in, const dm_column_out* ou
 cudaError_t launch_xc_exceptions(bool gather, const uint2* rec, uint64_t nsb, uint32_t xs, uint64_t dict_len,
                                  uint32_t* xm, uint32_t* ids, uint32_t* slices, unsigned long long* d_count,
                                  uint64_t count, cudaStream_t st);
+// Sharded Step 1(b) helpers (shard.cu, NEXT2).
+cudaError_t launch_lower_bound(int key, const void* sorted, uint64_t n, const void* values, uint64_t nv,
+                               uint64_t* pos, cudaStream_t st);
+cudaError_t launch_add_u32(uint32_t* x, uint64_t n, uint32_t add, cudaStream_t st);
+cudaError_t launch_xc_rebase(void* rec, uint64_t n, uint32_t add, cudaStream_t st);
+cudaError_t launch_set_delta_len(dm_header* hdr, uint64_t n, cudaStream_t st);
 // Naive Step 2: binary-search every tuple's value in U' (baseline).
 cudaError_t launch_naive_step2(const dm_column_in* in, const dm_column_out* out, dm_header* hdr, cudaStream_t st);
 cudaError_t launch_pack(const uint32_t* codes, uint64_t n, uint32_t bits, uint64_t* words, cudaStream_t st);

@@ -174,3 +174,154 @@ def sharded_merge_column(main_dict, main_codes_shard, n_main: int, main_bits: in
         out = dm.recompress(main_codes_shard, shard.n_main, main_bits, dict_len, xm, xd, rk[shard.delta_begin:],
                             shard.n_delta, nb)
     return out, nb, n_u, U
+
+
+# ----------------------------------------------------------- NEXT2: sharded Step 1(b)
+XC_SUPER = 1024  # U_M ranges start at multiples of every XC superblock size (4 << 7, 4 << 8)
+
+
+def plan_dict_ranges(dict_len: int, n_ranges: int, align: int = XC_SUPER) -> List[tuple]:
+    """Cut U_M's positions [0, |U_M|) into n_ranges contiguous ranges starting at
+    multiples of `align` (so every range's XC superblocks are global ones)."""
+    cuts = [0]
+    for g in range(1, n_ranges):
+        cuts.append(max(cuts[-1], (dict_len * g // n_ranges) // align * align))
+    cuts.append(dict_len)
+    return [(cuts[g], cuts[g + 1]) for g in range(n_ranges)]
+
+
+@dataclasses.dataclass
+class ShardedDictionary:
+    """Result of sharded_dictionary_merge on one rank."""
+    u_slice: object          # this rank's part of U' (its value range), keys
+    u_offset: int            # global U' index of u_slice[0]
+    merged_len: int          # |U'|
+    merged_bits: int         # b'
+    x_main_range: object     # X_M for this rank's U_M range (global codes), int32
+    xc: object               # the global XC (dm.XcTables), identical on every rank
+    x_main_exceptions: object  # a |U_M|-entry int32 X_M holding the flagged superblocks' slices
+    x_delta: object          # the global X_D (over U_D), int32
+    delta_rank: object       # r (N_D), int32
+    delta_dict_len: int      # |U_D|
+
+
+def sharded_dictionary_merge(main_dict_range, range_begin: int, dict_len: int, main_bits: int, delta, group=None,
+                             root: int = 0, shift: int = 7) -> ShardedDictionary:
+    """Step 1(b) sharded by value ranges across the ranks of `group` (SURVEY §8f
+    NEXT2; the paper's parallel merge splits both inputs at matching quantiles,
+    P:302-314).  Rank g holds U_M[range_begin : range_begin + len] (a
+    plan_dict_ranges range, non-empty); the root also holds D.
+
+    1. root: Step 1(a) (U_D, r);
+    2. the first U_M value of every range -> the root -> U_D cut points (lower bound);
+    3. root -> rank g: the U_D values in [U_M[a_g], U_M[a_{g+1}));
+    4. every rank merges its two ranges (dm_dictionary_merge_sorted_async) ->
+       local U', X_M, X_D, XC;
+    5. all-gather of (|U'_g|, new values_g) -> rebase X_M, X_D (by the |U'| of
+       earlier ranges) and the XC records (by their new values);
+    6. all-gather of the XC pieces, X_D pieces and flagged-superblock slices (rank
+       order = value order), broadcast of r: every rank can run Step 2 on any rows.
+    """
+    import torch
+    import torch.distributed as dist
+    import paper_1109_6885_b200 as dm
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    dm.set_tuning(dm.KNOB_XC_SHIFT, shift)
+    SB = 4 << shift
+    L = int(main_dict_range.shape[0])
+    assert L > 0 and range_begin % XC_SUPER == 0
+
+    def bcast(t, src):
+        dist.broadcast(t, src=src, group=group)
+        return t
+
+    def allgather(t):  # equal-shape all-gather from broadcasts (gloo moves CUDA tensors only by broadcast)
+        return [bcast(t.contiguous() if g == rank else torch.empty_like(t), g) for g in range(world)]
+
+    # 1. Step 1(a) on the root
+    meta = torch.zeros(2, dtype=torch.int64, device=dev)  # |U_D|, N_D
+    if rank == root:
+        dd = dm.DictionaryMerger(main_dict_range, 0, main_bits, delta, mode="delta")
+        dd.run_async()
+        h = dd.header()
+        if h.status != 0:
+            raise dm.DictMergeError(h.status, "dm_delta_dictionary_async")
+        meta.copy_(torch.tensor([h.delta_dict_len, delta.shape[0]], dtype=torch.int64))
+    bcast(meta, root)
+    n_ud, n_delta = (int(x) for x in meta.tolist())
+    # 2. cut points of U_D at every range's first U_M value
+    firsts = allgather(main_dict_range[:1])
+    cuts = torch.zeros(world + 1, dtype=torch.int64, device=dev)
+    if rank == root:
+        pos = dm.lower_bound(dd.UD[:n_ud], torch.cat(firsts[1:])) if world > 1 else cuts[:0]
+        cuts[1:world] = pos
+        cuts[world] = n_ud
+    bcast(cuts, root)
+    c = cuts.tolist()
+    # 3. U_D to every rank (one broadcast), each keeps its value range
+    ud = dd.UD[:n_ud].contiguous() if rank == root else \
+        torch.empty((n_ud,) + tuple(main_dict_range.shape[1:]), dtype=main_dict_range.dtype, device=dev)
+    if n_ud:
+        bcast(ud, root)
+    mine = ud[c[rank]:c[rank + 1]].clone()  # own allocation: the ABI wants 16-byte aligned buffers
+    # 4. local merge of the two ranges
+    lm = dm.DictionaryMerger(main_dict_range, 0, main_bits, mine, mode="sorted")
+    lm.run_async()
+    h = lm.header()
+    if h.status != 0:
+        raise dm.DictMergeError(h.status, "dm_dictionary_merge_sorted_async")
+    # 5. counts -> offsets, rebase
+    cnt = torch.tensor([h.merged_dict_len, h.merged_dict_len - L], dtype=torch.int64, device=dev)
+    allc = allgather(cnt)
+    n_u = [int(t[0]) for t in allc]
+    n_new = [int(t[1]) for t in allc]
+    off, new_off = sum(n_u[:rank]), sum(n_new[:rank])
+    dm.rebase(lm.XM[:L], off)
+    if mine.shape[0]:
+        dm.rebase(lm.XD[:mine.shape[0]], off)
+    xc_l = lm.xc()
+    xc_l.rebase(new_off)
+    # 6. the global tables, in rank (= value) order
+    all_len = torch.tensor([L, int(mine.shape[0])], dtype=torch.int64, device=dev)
+    all_l = allgather(all_len)
+    Ls = [int(t[0]) for t in all_l]
+    nds = [int(t[1]) for t in all_l]
+    recs, offs, xds = [], [], []
+    for g in range(world):
+        nrec_g = (Ls[g] + SB - 1) // SB
+        r_t = xc_l.records if g == rank else torch.empty(nrec_g * 8, dtype=torch.uint8, device=dev)
+        recs.append(bcast(r_t.contiguous(), g))
+        o_t = xc_l.offsets[:n_new[g]] if g == rank else torch.empty(n_new[g], dtype=torch.uint8, device=dev)
+        if n_new[g]:
+            offs.append(bcast(o_t.contiguous(), g))
+        x_t = lm.XD[:nds[g]] if g == rank else torch.empty(nds[g], dtype=torch.int32, device=dev)
+        if nds[g]:
+            xds.append(bcast(x_t.contiguous(), g))
+    n_off = sum(n_new)
+    offsets = torch.zeros(((n_off + 31) // 16) * 16, dtype=torch.uint8, device=dev)
+    if offs:
+        offsets[:n_off] = torch.cat(offs)
+    records = torch.cat(recs)
+    xc = dm.XcTables(records, offsets, shift, records.numel() // 8)
+    x_delta = torch.cat(xds) if xds else torch.empty(1, dtype=torch.int32, device=dev)
+    # flagged superblocks: every rank ships its X_M slices, every rank scatters all
+    ids, sl, nexc = dm.xc_exceptions_gather(xc_l, L, lm.XM)
+    if nexc:
+        dm.rebase(ids[:nexc], range_begin // SB)  # local -> global superblock ids
+    ex = torch.tensor([nexc], dtype=torch.int64, device=dev)
+    exs = allgather(ex)
+    x_exc = torch.empty(max(dict_len, 1), dtype=torch.int32, device=dev)
+    for g in range(world):
+        k = int(exs[g].item())
+        if not k:
+            continue
+        i_t = bcast((ids[:k] if g == rank else torch.empty(k, dtype=torch.int32, device=dev)).contiguous(), g)
+        s_t = bcast((sl[:k * SB] if g == rank else torch.empty(k * SB, dtype=torch.int32, device=dev)).contiguous(), g)
+        dm.xc_exceptions_scatter(xc, dict_len, i_t, s_t, k, x_exc)
+    rk = bcast(dd.R[:max(n_delta, 1)].contiguous() if rank == root
+               else torch.empty(max(n_delta, 1), dtype=torch.int32, device=dev), root)
+    total = sum(n_u)
+    return ShardedDictionary(lm.U[: h.merged_dict_len], off, total, dm.width(total), lm.XM[:L], xc, x_exc, x_delta,
+                             rk, n_ud)

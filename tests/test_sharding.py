@@ -160,3 +160,61 @@ def test_sharded_merge_column_two_ranks_on_one_gpu(tables):
     for p in procs:
         p.join(timeout=60)
     assert ok
+
+
+def _next2_worker(rank, world, port, q, key):
+    """NEXT2: Step 1(b) sharded by U_M value ranges over `world` ranks on the one
+    GPU (gloo broadcasts), then Step 2 of each rank's row shard through the
+    assembled global XC; everything compared with the oracle."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1109_6885_b200 as dm
+        from tests.parity import to_device, keys_np
+        torch.cuda.set_device(0)
+        col = datagen.make_random_case(35, 600_000, 200_000, 90_001, 0.5, key=key)
+        UM, M, D = to_device(col)
+        a, b = sharding.plan_dict_ranges(col.dict_len, world)[rank]
+        sd = sharding.sharded_dictionary_merge(UM[a:b], a, col.dict_len, col.main_bits,
+                                               D if rank == 0 else D[:0], shift=7)
+        shard = sharding.plan_row_shards(col.n_main, col.n_delta, world)[rank]
+        mslice = M[shard.in_word(col.main_bits):] if shard.n_main else M
+        out = dm.recompress_xc(mslice, shard.n_main, col.main_bits, col.dict_len, sd.xc, sd.x_main_exceptions,
+                               sd.x_delta, sd.delta_rank[shard.delta_begin:], shard.n_delta, sd.merged_bits)
+        pieces = [None] * world
+        dist.all_gather_object(pieces, (keys_np_list(keys_np(sd.u_slice, key), key), sd.u_offset,
+                                        sd.x_main_range.cpu().numpy().view(np.uint32).tolist(),
+                                        out.cpu().numpy().view(np.uint64).tolist()))
+        if rank == 0:
+            ref = oracle.merge(col)
+            U = [v for p in sorted(pieces, key=lambda p: p[1]) for v in p[0]]
+            want_U = keys_np_list(ref.merged_dict, key)
+            xm = [v for p in pieces for v in p[2]]
+            words = np.array([w for p in pieces for w in p[3]], dtype=np.uint64)
+            xd = sd.x_delta.cpu().numpy().view(np.uint32)[: ref.x_delta.shape[0]]
+            q.put((U == want_U, xm == ref.x_main.tolist(), bool(np.array_equal(xd, ref.x_delta)),
+                   sd.merged_len == ref.merged_len and sd.merged_bits == ref.merged_bits,
+                   bool(np.array_equal(words, ref.merged_words))))
+    finally:
+        dist.destroy_process_group()
+
+
+def keys_np_list(a, key):
+    return a.tolist() if key != "b16" else [bytes(r) for r in a]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,key", [(2, "u64"), (3, "u64"), (3, "b16"), (2, "u32")])
+def test_next2_sharded_dictionary_merge(world, key):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_next2_worker, args=(r, world, port, q, key)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+    assert all(res), res
