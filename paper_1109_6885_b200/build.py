@@ -42,6 +42,13 @@ def build_check() -> str:
     return out
 
 
+def build_variant(name: str, *defines: str) -> str:
+    """Experiment variant libdictmerge_<name>.so built with extra -D flags (load via DM_LIB_PATH)."""
+    out = os.path.join(HERE, f"libdictmerge_{name}.so")
+    subprocess.check_call([NVCC, *FLAGS, *[f"-D{d}" for d in defines], *sources(), "-o", out])
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return LIB

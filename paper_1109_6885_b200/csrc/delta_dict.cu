@@ -82,6 +82,7 @@ __global__ void __launch_bounds__(256) k_hist(const void* __restrict__ D, uint64
                                               const unsigned long long* __restrict__ n_dev,
                                               uint32_t* __restrict__ hist, uint32_t* done,
                                               SortPlan* __restrict__ plan) {
+  pdl_prologue();
   constexpr int P = KT::kPasses;
   const uint64_t n = n_dev ? (uint64_t)*n_dev : n_host;
   __shared__ uint32_t s_h[P][256];
@@ -116,6 +117,7 @@ __global__ void __launch_bounds__(NT) k_onesweep(const void* __restrict__ D, voi
                                                 const unsigned long long* __restrict__ n_dev, int pass,
                                                 const SortPlan* __restrict__ plan, uint32_t* status,
                                                 uint32_t* counter) {
+  pdl_prologue();
   // n_dev: the key count is only known on the device (deduplicated delta); the
   // grid covers n_host >= n and tiles past n exit (nothing waits on them)
   const uint64_t n = n_dev ? (uint64_t)*n_dev : n_host;
@@ -276,6 +278,7 @@ __global__ void __launch_bounds__(kUniqThreads) k_unique(const void* __restrict_
                                                         const SortPlan* __restrict__ plan, uint64_t* status,
                                                         uint32_t* counter, void* __restrict__ udict,
                                                         uint32_t* __restrict__ rank, dm_header* hdr) {
+  pdl_prologue();
   using K = typename KT::K;
   constexpr int NT = kUniqThreads, ITEMS = kUniqItems, W = NT / 32;
   constexpr int TILE = NT * ITEMS;
@@ -389,6 +392,7 @@ __global__ void __launch_bounds__(256) k_dedup_insert(const void* __restrict__ D
                                                       uint32_t* __restrict__ tags, uint32_t* __restrict__ ids,
                                                       uint64_t mask, void* __restrict__ dkeys,
                                                       uint32_t* __restrict__ tid, unsigned long long* n_dist) {
+  pdl_prologue();
   using K = typename KT::K;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const K k = KT::load(D, i);
@@ -427,6 +431,7 @@ __global__ void __launch_bounds__(256) k_dedup_insert(const void* __restrict__ D
 __global__ void __launch_bounds__(256) k_dedup_ranks(const uint32_t* __restrict__ tid,
                                                      const uint32_t* __restrict__ rank_of_id, uint64_t n,
                                                      uint32_t* __restrict__ rank) {
+  pdl_prologue();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
     rank[i] = __ldg(rank_of_id + __ldg(tid + i));
 }
@@ -441,7 +446,7 @@ void launch_passes(const void* D, uint64_t n, const unsigned long long* n_dev, c
   const uint64_t ntiles = (n + TILE - 1) / TILE;
   for (int p = 0; p < KT::kPasses; ++p) {
     uint32_t* status = reinterpret_cast<uint32_t*>(ws + L.status_sort) + (uint64_t)p * ntiles * 256;
-    k_onesweep<KT, NT, ITEMS><<<(unsigned)ntiles, NT, dsmem, st>>>(
+    launch_k(k_onesweep<KT, NT, ITEMS>, (unsigned)ntiles, NT, dsmem, st, 
         D, ws + L.keys0, ws + L.keys1, reinterpret_cast<uint32_t*>(ws + L.vals0),
         reinterpret_cast<uint32_t*>(ws + L.vals1), n, n_dev, p, plan, status, counters + CNT_SORT + p);
     note_launch();
@@ -463,7 +468,7 @@ cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, void* udict
   if (L.dedup) {
     unsigned long long* n_dist = reinterpret_cast<unsigned long long*>(counters + CNT_DEDUP);
     const int sms = device_sms();
-    k_dedup_insert<KT><<<(unsigned)std::min<uint64_t>((n + 255) / 256, (uint64_t)sms * 8), 256, 0, st>>>(
+    launch_k(k_dedup_insert<KT>, (unsigned)std::min<uint64_t>((n + 255) / 256, (uint64_t)sms * 8), 256, 0, st, 
         in->delta, n, reinterpret_cast<uint32_t*>(ws + L.dd_tags), reinterpret_cast<uint32_t*>(ws + L.dd_ids),
         L.dd_cap - 1, ws + L.dd_keys, reinterpret_cast<uint32_t*>(ws + L.dd_tid), n_dist);
     note_launch();
@@ -472,7 +477,7 @@ cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, void* udict
     sort_rank = reinterpret_cast<uint32_t*>(ws + L.dd_rank);
   }
   const int hist_blocks = (int)std::min<uint64_t>((n + 4095) / 4096, 148 * 4);
-  k_hist<KT><<<hist_blocks, 256, 0, st>>>(D, n, n_dev, hist, counters + CNT_HIST, plan);
+  launch_k(k_hist<KT>, hist_blocks, 256, 0, st, D, n, n_dev, hist, counters + CNT_HIST, plan);
   note_launch();
   constexpr bool U64 = KT::kBytes <= 8;  // tile shape: 8-byte and 4-byte keys alike
   switch (sort_variant()) {  // must match sort_tile_keys() (workspace layout)
@@ -482,14 +487,14 @@ cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, void* udict
     default: launch_passes<KT, 512, U64 ? 16 : 8>(D, n, n_dev, ws, L, plan, counters, st); break;
   }
   const uint64_t utiles = (n + kUniqThreads * kUniqItems - 1) / (kUniqThreads * kUniqItems);
-  k_unique<KT><<<(unsigned)utiles, kUniqThreads, 0, st>>>(
+  launch_k(k_unique<KT>, (unsigned)utiles, kUniqThreads, 0, st, 
       D, ws + L.keys0, ws + L.keys1, reinterpret_cast<const uint32_t*>(ws + L.vals0),
       reinterpret_cast<const uint32_t*>(ws + L.vals1), n, n_dev, plan,
       reinterpret_cast<uint64_t*>(ws + L.status_unique), counters + CNT_UNIQUE, udict, sort_rank, hdr);
   note_launch();
   if (L.dedup) {
     const int sms = device_sms();
-    k_dedup_ranks<<<(unsigned)std::min<uint64_t>((n + 255) / 256, (uint64_t)sms * 8), 256, 0, st>>>(
+    launch_k(k_dedup_ranks, (unsigned)std::min<uint64_t>((n + 255) / 256, (uint64_t)sms * 8), 256, 0, st, 
         reinterpret_cast<const uint32_t*>(ws + L.dd_tid), sort_rank, n, rank);
     note_launch();
   }

@@ -37,6 +37,7 @@ template <class KT>
 __global__ void __launch_bounds__(256) k_partition(const void* __restrict__ A, uint64_t nA,
                                                    const void* __restrict__ B, const dm_header* __restrict__ hdr,
                                                    uint64_t nparts, uint64_t* __restrict__ part) {
+  pdl_prologue();
   const uint64_t t = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const unsigned lane = lane_id();
   if (t >= nparts) return;
@@ -219,6 +220,7 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_count(const void* __res
                                                                const uint64_t* __restrict__ part,
                                                                const dm_header* __restrict__ hdr,
                                                                uint32_t* __restrict__ cnt) {
+  pdl_prologue();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t s_warp[kMergeThreads / 32 + 1];
   TileRank<KT> tr;
@@ -236,6 +238,7 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_count(const void* __res
 __global__ void __launch_bounds__(256) k_scan_counts(const uint32_t* __restrict__ cnt, uint64_t n,
                                                      uint64_t* __restrict__ excl, uint64_t* status, uint32_t* counter,
                                                      uint64_t nA, dm_header* hdr) {
+  pdl_prologue();
   constexpr int ITEMS = 8, TILE = 256 * ITEMS;
   __shared__ uint32_t s_warp[9];
   __shared__ uint64_t s_excl;
@@ -281,6 +284,7 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_write(const void* __res
                                                                uint32_t* __restrict__ XD, dm_header* hdr,
                                                                uint32_t* __restrict__ rblk,
                                                                uint8_t* __restrict__ offs, uint32_t xs) {
+  pdl_prologue();
   using K = typename KT::K;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t s_warp[kMergeThreads / 32 + 1];
@@ -357,6 +361,7 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge(const void* __restrict_
                                                          uint32_t* __restrict__ XD, dm_header* hdr,
                                                          uint32_t* __restrict__ rblk, uint8_t* __restrict__ offs,
                                                          uint32_t xs) {
+  pdl_prologue();
   using K = typename KT::K;
   constexpr uint32_t T = kMergeTile, NT = kMergeThreads, IT = kMergeItems, NW = T / 32;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -581,6 +586,7 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge(const void* __restrict_
 // in the plain X_M.
 __global__ void __launch_bounds__(256) k_xc_records(const uint32_t* __restrict__ rblk, uint64_t nblk, uint64_t nsb,
                                                     uint2* __restrict__ rec) {
+  pdl_prologue();
   const uint64_t sb = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (sb >= nsb) return;
   constexpr uint32_t BPS = 4;
@@ -604,6 +610,7 @@ __global__ void __launch_bounds__(256) k_xc_exceptions(bool gather, const uint2*
                                                        uint32_t xs, uint64_t dict_len, uint32_t* __restrict__ xm,
                                                        uint32_t* __restrict__ ids, uint32_t* __restrict__ slices,
                                                        unsigned long long* d_count, uint64_t count) {
+  pdl_prologue();
   const unsigned lane = lane_id();
   const uint64_t warp0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -633,6 +640,7 @@ __global__ void __launch_bounds__(256) k_xc_exceptions(bool gather, const uint2*
 }
 
 __global__ void k_empty_header(dm_header* hdr) {
+  pdl_prologue();
   // |U_M| + |U_D| == 0: U' is empty and b' = 1 (reading A1)
   if (hdr->delta_dict_len == 0) {
     hdr->merged_dict_len = 0;
@@ -645,7 +653,7 @@ cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, const void*
                 uint32_t* xd, dm_header* hdr, cudaStream_t st, bool force_xc) {
   using K = typename KT::K;
   if (in->dict_len + in->n_delta == 0) {
-    k_empty_header<<<1, 1, 0, st>>>(hdr);
+    launch_k(k_empty_header, 1, 1, 0, st, hdr);
     note_launch();
     return cudaGetLastError();
   }
@@ -661,12 +669,12 @@ cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, const void*
   uint32_t* counter = reinterpret_cast<uint32_t*>(ws + L.counters) + CNT_MERGE;
   const int variant = tuning(1);
   if (variant == 0 || variant == 2) {  // lean tiles: two passes (default) or single pass
-    k_partition<KT><<<(unsigned)((nt + 1 + 7) / 8), 256, 0, st>>>(in->main_dict, in->dict_len, udict, hdr, nt + 1,
+    launch_k(k_partition<KT>, (unsigned)((nt + 1 + 7) / 8), 256, 0, st, in->main_dict, in->dict_len, udict, hdr, nt + 1,
                                                                      part);
     const size_t smem = sizeof(K) * (kMergeTile + 1) + sizeof(uint32_t) * (3 * kMergeTile + 1);
     auto go = [&](auto kern) {
       ensure_smem((const void*)kern, true);
-      kern<<<(unsigned)nt, kMergeThreads, smem, st>>>(in->main_dict, in->dict_len, udict, part, nt, status, counter,
+      launch_k(kern, (unsigned)nt, kMergeThreads, smem, st, in->main_dict, in->dict_len, udict, part, nt, status, counter,
                                                       cnt, excl, U, xm, xd, hdr, rblk, offs, xs);
     };
     if (variant == 2) {
@@ -674,7 +682,7 @@ cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, const void*
       note_launch(2);
     } else {
       go(k_merge<KT, 1>);
-      k_scan_counts<<<(unsigned)((nt + 2047) / 2048), 256, 0, st>>>(cnt, nt, excl, status, counter, in->dict_len,
+      launch_k(k_scan_counts, (unsigned)((nt + 2047) / 2048), 256, 0, st, cnt, nt, excl, status, counter, in->dict_len,
                                                                     hdr);
       go(k_merge<KT, 2>);
       note_launch(4);
@@ -682,24 +690,24 @@ cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, const void*
   } else {
   uint32_t* cnt = reinterpret_cast<uint32_t*>(ws + L.mcount);
   uint64_t* excl = reinterpret_cast<uint64_t*>(ws + L.mexcl);
-  k_partition<KT><<<(unsigned)((nt + 1 + 7) / 8), 256, 0, st>>>(in->main_dict, in->dict_len, udict, hdr, nt + 1,
+  launch_k(k_partition<KT>, (unsigned)((nt + 1 + 7) / 8), 256, 0, st, in->main_dict, in->dict_len, udict, hdr, nt + 1,
                                                                    part);
   const size_t smem_count = sizeof(K) * (kMergeTile + 1) + 3 * sizeof(uint32_t) * (kMergeTile + 2);
   ensure_smem((const void*)k_merge_count<KT>, true);
-  k_merge_count<KT><<<(unsigned)nt, kMergeThreads, smem_count, st>>>(in->main_dict, in->dict_len, udict, part, hdr,
+  launch_k(k_merge_count<KT>, (unsigned)nt, kMergeThreads, smem_count, st, in->main_dict, in->dict_len, udict, part, hdr,
                                                                      cnt);
-  k_scan_counts<<<(unsigned)((nt + 2047) / 2048), 256, 0, st>>>(
+  launch_k(k_scan_counts, (unsigned)((nt + 2047) / 2048), 256, 0, st, 
       cnt, nt, excl, reinterpret_cast<uint64_t*>(ws + L.status_merge),
       reinterpret_cast<uint32_t*>(ws + L.counters) + CNT_MERGE, in->dict_len, hdr);
   const size_t smem_write = smem_count;
   ensure_smem((const void*)k_merge_write<KT>, true);
-  k_merge_write<KT><<<(unsigned)nt, kMergeThreads, smem_write, st>>>(in->main_dict, in->dict_len, udict, part, excl,
+  launch_k(k_merge_write<KT>, (unsigned)nt, kMergeThreads, smem_write, st, in->main_dict, in->dict_len, udict, part, excl,
                                                                      U, xm, xd, hdr, rblk, offs, xs);
   note_launch(4);
   }
   if (xc) {
     const uint64_t nsb = xc_nsb(in->dict_len, xs);
-    k_xc_records<<<(unsigned)((nsb + 255) / 256), 256, 0, st>>>(rblk, xc_nblk(in->dict_len, xs), nsb,
+    launch_k(k_xc_records, (unsigned)((nsb + 255) / 256), 256, 0, st, rblk, xc_nblk(in->dict_len, xs), nsb,
                                                                 reinterpret_cast<uint2*>(ws + L.xc_rec));
     note_launch();
   }
@@ -714,7 +722,7 @@ cudaError_t launch_xc_exceptions(bool gather, const uint2* rec, uint64_t nsb, ui
   const uint64_t items = gather ? nsb : count;
   if (items == 0) return cudaSuccess;
   const unsigned grid = (unsigned)std::min<uint64_t>((items + 7) / 8, (uint64_t)device_sms() * 16);
-  k_xc_exceptions<<<grid, 256, 0, st>>>(gather, rec, nsb, xs, dict_len, xm, ids, slices, d_count, count);
+  launch_k(k_xc_exceptions, grid, 256, 0, st, gather, rec, nsb, xs, dict_len, xm, ids, slices, d_count, count);
   note_launch();
   return cudaGetLastError();
 }

@@ -22,6 +22,14 @@ static std::atomic<int> g_last_cuda{0};
 
 void note_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
 
+bool pdl_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("DM_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 namespace {
 std::mutex g_cache_mu;
 struct FuncKey {

@@ -131,6 +131,25 @@ inline size_t key_bytes(int key) { return key == DM_KEY_U64 ? 8 : key == DM_KEY_
 uint32_t host_width(uint64_t n);
 uint64_t host_words(uint64_t n, uint32_t bits);
 
+// ---- launches: cudaLaunchKernelEx with programmatic dependent launch (PDL,
+// see pdl_prologue in dm_device.cuh); DM_PDL=0 turns the attribute off.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  static_assert(sizeof...(KArgs) == sizeof...(Args), "kernel argument count");
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // ---- launch bookkeeping (host; cached so a merge issues no per-launch driver queries)
 void note_launch(int n = 1);
 // Raise the dynamic shared memory limit of `func` to the device maximum, once per device.

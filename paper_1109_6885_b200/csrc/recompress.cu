@@ -148,6 +148,7 @@ __global__ void __launch_bounds__(rec_threads<XMODE>(), XMODE == XM_XC_SMEM ? 1 
                                                             const uint2* __restrict__ xrec,
                                                             const uint8_t* __restrict__ xoffs, uint32_t xc_budget,
                                                             int raw_warps, uint32_t xs) {
+  pdl_prologue();
   constexpr int G = rec_groups<XMODE>();
   constexpr int S = XMODE == XM_XC_SMEM ? kRecStagesXc : kRecStages;
   constexpr int CW = rec_consumer_warps<XMODE>();
@@ -308,6 +309,7 @@ __global__ void __launch_bounds__(256) k_naive_step2(const uint64_t* __restrict_
                                                      const void* __restrict__ D, uint64_t n_delta,
                                                      const void* __restrict__ Up, uint64_t* __restrict__ Mout,
                                                      dm_header* hdr) {
+  pdl_prologue();
   using K = typename KT::K;
   const uint32_t nb = hdr->merged_bits;
   const uint64_t nU = hdr->merged_dict_len, n_total = n_main + n_delta, ngroups = (n_total + 31) / 32;
@@ -350,6 +352,7 @@ __global__ void __launch_bounds__(256) k_naive_step2(const uint64_t* __restrict_
 
 __global__ void __launch_bounds__(256) k_pack(const uint32_t* __restrict__ codes, uint64_t n, uint32_t bits,
                                               uint32_t* __restrict__ words32, uint64_t nw32) {
+  pdl_prologue();
   const unsigned lane = lane_id();
   const uint32_t mask = bits == 32 ? 0xffffffffu : ((1u << bits) - 1);
   const uint32_t pr0 = (32 * lane) / bits, pop = 32 * lane - pr0 * bits;
@@ -368,6 +371,7 @@ __global__ void __launch_bounds__(256) k_pack(const uint32_t* __restrict__ codes
 
 __global__ void __launch_bounds__(256) k_unpack(const uint32_t* __restrict__ words32, uint64_t nw32, uint64_t n,
                                                 uint32_t bits, uint32_t* __restrict__ codes) {
+  pdl_prologue();
   const uint32_t mask = bits == 32 ? 0xffffffffu : ((1u << bits) - 1);
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t s = i * bits;
@@ -413,7 +417,7 @@ cudaError_t launch_nb(const dm_column_in* in, const dm_column_out* out, const ui
     const uint64_t nchunks = (n_total + 32ull * groups - 1) / (32ull * groups);
     const int occ = occupancy((const void*)kern, threads, smem);
     const unsigned grid = (unsigned)std::min<uint64_t>(nchunks, (uint64_t)sms * occ);
-    kern<<<grid, threads, smem, st>>>(in->main_codes, in->n_main, in->main_bits, in->dict_len, xm, xd, rank,
+    launch_k(kern, grid, threads, smem, st, in->main_codes, in->n_main, in->main_bits, in->dict_len, xm, xd, rank,
                                           in->n_delta, out->merged_codes, hdr,
                                           groups == kRecGroups ? in_stage : in_stage_xc, fixed_bits, xrec, xoffs,
                                           budget, xc_raw_warps(), xs);
@@ -499,7 +503,7 @@ cudaError_t launch_recompress_xc(const dm_column_in* in, const dm_column_out* ou
   auto kern = xc_table[bits <= 32 ? bits : 0];  // width-specialised (same instantiations as launch_nb)
   const int occ = occupancy((const void*)kern, kRecThreads, smem);
   const unsigned grid = (unsigned)std::min<uint64_t>(nchunks, (uint64_t)device_sms() * occ);
-  kern<<<grid, kRecThreads, smem, st>>>(in->main_codes, in->n_main, in->main_bits, in->dict_len, xm, xd, rank,
+  launch_k(kern, grid, kRecThreads, smem, st, in->main_codes, in->n_main, in->main_bits, in->dict_len, xm, xd, rank,
                                         in->n_delta, out->merged_codes, hdr, in_stage, bits, xc_rec, xc_offs, 0u, 0,
                                         xs);
   note_launch();
@@ -512,17 +516,17 @@ cudaError_t launch_naive_step2(const dm_column_in* in, const dm_column_out* out,
   const unsigned grid = (unsigned)std::min<uint64_t>((n_total + 255) / 256, (uint64_t)device_sms() * 16);
   switch (in->key) {
     case DM_KEY_U64:
-      k_naive_step2<KeyU64><<<grid, 256, 0, st>>>(in->main_codes, in->n_main, in->main_bits, in->main_dict,
+      launch_k(k_naive_step2<KeyU64>, grid, 256, 0, st, in->main_codes, in->n_main, in->main_bits, in->main_dict,
                                                   in->dict_len, in->delta, in->n_delta, out->merged_dict,
                                                   out->merged_codes, hdr);
       break;
     case DM_KEY_U32:
-      k_naive_step2<KeyU32><<<grid, 256, 0, st>>>(in->main_codes, in->n_main, in->main_bits, in->main_dict,
+      launch_k(k_naive_step2<KeyU32>, grid, 256, 0, st, in->main_codes, in->n_main, in->main_bits, in->main_dict,
                                                   in->dict_len, in->delta, in->n_delta, out->merged_dict,
                                                   out->merged_codes, hdr);
       break;
     default:
-      k_naive_step2<KeyB16><<<grid, 256, 0, st>>>(in->main_codes, in->n_main, in->main_bits, in->main_dict,
+      launch_k(k_naive_step2<KeyB16>, grid, 256, 0, st, in->main_codes, in->n_main, in->main_bits, in->main_dict,
                                                   in->dict_len, in->delta, in->n_delta, out->merged_dict,
                                                   out->merged_codes, hdr);
   }
@@ -534,7 +538,7 @@ cudaError_t launch_pack(const uint32_t* codes, uint64_t n, uint32_t bits, uint64
   if (n == 0) return cudaSuccess;
   const uint64_t groups = (n + 31) / 32;
   const unsigned grid = (unsigned)std::min<uint64_t>((groups + 7) / 8, 148 * 16);
-  k_pack<<<grid, 256, 0, st>>>(codes, n, bits, reinterpret_cast<uint32_t*>(words), 2 * host_words(n, bits));
+  launch_k(k_pack, grid, 256, 0, st, codes, n, bits, reinterpret_cast<uint32_t*>(words), 2 * host_words(n, bits));
   note_launch();
   return cudaGetLastError();
 }
@@ -542,7 +546,7 @@ cudaError_t launch_pack(const uint32_t* codes, uint64_t n, uint32_t bits, uint64
 cudaError_t launch_unpack(const uint64_t* words, uint64_t n, uint32_t bits, uint32_t* codes, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
   const unsigned grid = (unsigned)std::min<uint64_t>((n + 255) / 256, 148 * 16);
-  k_unpack<<<grid, 256, 0, st>>>(reinterpret_cast<const uint32_t*>(words), 2 * host_words(n, bits), n, bits, codes);
+  launch_k(k_unpack, grid, 256, 0, st, reinterpret_cast<const uint32_t*>(words), 2 * host_words(n, bits), n, bits, codes);
   note_launch();
   return cudaGetLastError();
 }

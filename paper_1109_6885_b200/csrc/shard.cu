@@ -18,6 +18,7 @@ template <class KT>
 __global__ void __launch_bounds__(256) k_lower_bound(const void* __restrict__ sorted, uint64_t n,
                                                      const void* __restrict__ values, uint64_t nv,
                                                      uint64_t* __restrict__ pos) {
+  pdl_prologue();
   const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (i >= nv) return;
   const auto v = KT::load(values, i);
@@ -30,19 +31,22 @@ __global__ void __launch_bounds__(256) k_lower_bound(const void* __restrict__ so
 }
 
 __global__ void __launch_bounds__(256) k_add_u32(uint32_t* __restrict__ x, uint64_t n, uint32_t add) {
+  pdl_prologue();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
     x[i] += add;
 }
 
 // XC record word 0 = R | flag << 31: add to R, keep the flag
 __global__ void __launch_bounds__(256) k_xc_rebase(uint2* __restrict__ rec, uint64_t n, uint32_t add) {
+  pdl_prologue();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t x = rec[i].x;
     rec[i].x = (x & 0x80000000u) | ((x & 0x7fffffffu) + add);
   }
 }
 
-__global__ void k_set_delta_len(dm_header* hdr, uint64_t n) { hdr->delta_dict_len = n; }
+__global__ void k_set_delta_len(dm_header* hdr, uint64_t n) {
+  pdl_prologue(); hdr->delta_dict_len = n; }
 
 unsigned grid_for(uint64_t n) { return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, 148 * 16)); }
 
@@ -53,9 +57,9 @@ cudaError_t launch_lower_bound(int key, const void* sorted, uint64_t n, const vo
   if (nv == 0) return cudaSuccess;
   const unsigned g = (unsigned)((nv + 255) / 256);
   switch (key) {
-    case DM_KEY_U64: k_lower_bound<KeyU64><<<g, 256, 0, st>>>(sorted, n, values, nv, pos); break;
-    case DM_KEY_U32: k_lower_bound<KeyU32><<<g, 256, 0, st>>>(sorted, n, values, nv, pos); break;
-    default: k_lower_bound<KeyB16><<<g, 256, 0, st>>>(sorted, n, values, nv, pos);
+    case DM_KEY_U64: launch_k(k_lower_bound<KeyU64>, g, 256, 0, st, sorted, n, values, nv, pos); break;
+    case DM_KEY_U32: launch_k(k_lower_bound<KeyU32>, g, 256, 0, st, sorted, n, values, nv, pos); break;
+    default: launch_k(k_lower_bound<KeyB16>, g, 256, 0, st, sorted, n, values, nv, pos);
   }
   note_launch();
   return cudaGetLastError();
@@ -63,20 +67,20 @@ cudaError_t launch_lower_bound(int key, const void* sorted, uint64_t n, const vo
 
 cudaError_t launch_add_u32(uint32_t* x, uint64_t n, uint32_t add, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
-  k_add_u32<<<grid_for(n), 256, 0, st>>>(x, n, add);
+  launch_k(k_add_u32, grid_for(n), 256, 0, st, x, n, add);
   note_launch();
   return cudaGetLastError();
 }
 
 cudaError_t launch_xc_rebase(void* rec, uint64_t n, uint32_t add, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
-  k_xc_rebase<<<grid_for(n), 256, 0, st>>>(static_cast<uint2*>(rec), n, add);
+  launch_k(k_xc_rebase, grid_for(n), 256, 0, st, static_cast<uint2*>(rec), n, add);
   note_launch();
   return cudaGetLastError();
 }
 
 cudaError_t launch_set_delta_len(dm_header* hdr, uint64_t n, cudaStream_t st) {
-  k_set_delta_len<<<1, 1, 0, st>>>(hdr, n);
+  launch_k(k_set_delta_len, 1, 1, 0, st, hdr, n);
   note_launch();
   return cudaGetLastError();
 }
