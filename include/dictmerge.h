@@ -239,10 +239,14 @@ dm_status dm_pack_codes(const uint32_t* codes, uint64_t n, uint32_t bits, uint64
 dm_status dm_unpack_codes(const uint64_t* words, uint64_t n, uint32_t bits, uint32_t* codes, void* cuda_stream);
 
 /* Host-buffer entry point (end-to-end use).  `in` and `out` hold HOST pointers
- * (pinned memory gives full PCIe bandwidth); the context owns device staging
- * buffers, grows them on demand and reuses them across calls.  Copies the
- * inputs to the device, merges, copies U', M' (and any requested X_M / X_D /
- * U_D / r) back, synchronises and fills the result fields. */
+ * (pinned memory gives full PCIe bandwidth and copy/compute overlap); the
+ * context owns device staging buffers, grows them on demand and reuses them
+ * across calls.  Pipelined over three streams: U_M and D are uploaded first and
+ * Steps 1(a)-2(a) start while M is still uploading in row chunks; Step 2(b)
+ * runs chunk by chunk as M arrives (rows are independent, Eq 11) and each M'
+ * chunk is downloaded while later chunks upload; U' (and any requested X_M /
+ * X_D / U_D / r) download during the M upload.  Synchronises and fills the
+ * result fields. */
 typedef struct dm_ctx dm_ctx;
 dm_ctx* dm_ctx_create(int device);
 void dm_ctx_destroy(dm_ctx* ctx);

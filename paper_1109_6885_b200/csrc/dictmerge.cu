@@ -328,7 +328,18 @@ static StreamPool& stream_pool() {
 
 struct dm_ctx_impl {
   int device = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;    // compute
+  cudaStream_t s_in = nullptr;      // host -> device copies
+  cudaStream_t s_out = nullptr;     // device -> host copies
+  std::vector<cudaEvent_t> events;  // pipeline events, grown on demand
+  cudaEvent_t event(size_t i) {
+    while (events.size() <= i) {
+      cudaEvent_t e = nullptr;
+      cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+      events.push_back(e);
+    }
+    return events[i];
+  }
   std::vector<std::pair<void*, size_t>> bufs;  // device buffers, grown on demand
   dm_header* host_hdr = nullptr;                // pinned
   void* get(int slot, size_t bytes) {
@@ -633,6 +644,8 @@ dm_ctx* dm_ctx_create(int device) {
   dm_ctx* c = new dm_ctx();
   c->impl.device = device;
   if (cudaStreamCreateWithFlags(&c->impl.stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->impl.s_in, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->impl.s_out, cudaStreamNonBlocking) != cudaSuccess ||
       cudaMallocHost(&c->impl.host_hdr, sizeof(dm_header)) != cudaSuccess) {
     delete c;
     return nullptr;
@@ -647,14 +660,26 @@ void dm_ctx_destroy(dm_ctx* c) {
     if (b.first) cudaFree(b.first);
   if (c->impl.host_hdr) cudaFreeHost(c->impl.host_hdr);
   if (c->impl.stream) cudaStreamDestroy(c->impl.stream);
+  if (c->impl.s_in) cudaStreamDestroy(c->impl.s_in);
+  if (c->impl.s_out) cudaStreamDestroy(c->impl.s_out);
+  for (cudaEvent_t ev : c->impl.events) cudaEventDestroy(ev);
   delete c;
 }
 
 dm_status dm_merge_column_host(dm_ctx* c, const dm_column_in* hin, dm_column_out* hout) {
+  // A three-stream pipeline (copy-in, compute, copy-out; B200 has separate copy
+  // engines per direction, PCIe is full duplex):
+  //   in:      U_M, D  |  M chunk 0 | M chunk 1 | ...
+  //   compute:           Steps 1(a)-2(a) | Step 2(b) chunk 0 | chunk 1 | ...
+  //   out:                               U' (X_M ...) | M' chunk 0 | chunk 1 | ...
+  // Step 2(b) of a row chunk needs only its M words and the translation tables
+  // (Eq 11, P:272 is row-local; the paper splits N' over threads the same way,
+  // P:324), so the main-code upload overlaps Step 1 and the M' download
+  // overlaps the remaining uploads.  One host wait: for b' after Step 2(a).
   if (!c || !hin || !hout) return DM_E_INVALID;
   cudaSetDevice(c->impl.device);
   auto& I = c->impl;
-  cudaStream_t st = I.stream;
+  cudaStream_t st = I.stream, sin = I.s_in, sout = I.s_out;
   const size_t E = key_bytes(hin->key);
   dm_column_in din = *hin;
   dm_column_out dout = *hout;
@@ -668,45 +693,109 @@ dm_status dm_merge_column_host(dm_ctx* c, const dm_column_in* hin, dm_column_out
   dout.merged_dict_cap = hin->dict_len + hin->n_delta;
   dout.merged_codes = static_cast<uint64_t*>(I.get(B_MOUT, cap_words * 8));
   dout.merged_codes_cap_words = cap_words;
-  dout.x_main = hout->x_main ? static_cast<uint32_t*>(I.get(B_XM, hin->dict_len * 4)) : nullptr;
-  dout.x_delta = hout->x_delta ? static_cast<uint32_t*>(I.get(B_XD, hin->n_delta * 4)) : nullptr;
+  // the tables always live on the device (Step 2(b) runs per chunk from them)
+  uint32_t* xm = static_cast<uint32_t*>(I.get(B_XM, std::max<uint64_t>(hin->dict_len, 1) * 4));
+  uint32_t* xd = static_cast<uint32_t*>(I.get(B_XD, std::max<uint64_t>(hin->n_delta, 1) * 4));
+  uint32_t* rk = static_cast<uint32_t*>(I.get(B_R, std::max<uint64_t>(hin->n_delta, 1) * 4));
+  dout.x_main = xm;
+  dout.x_delta = xd;
+  dout.delta_rank = rk;
   dout.delta_dict = hout->delta_dict ? I.get(B_UD, hin->n_delta * E) : nullptr;
-  dout.delta_rank = hout->delta_rank ? static_cast<uint32_t*>(I.get(B_R, hin->n_delta * 4)) : nullptr;
   const size_t wsb = dm_workspace_bytes(hin);
   void* ws = I.get(B_WS, wsb);
-  if (!ws || !dout.merged_dict || !dout.merged_codes) return cuda_fail(cudaErrorMemoryAllocation);
+  if (!ws || !dout.merged_dict || !dout.merged_codes || !xm || !xd || !rk) return cuda_fail(cudaErrorMemoryAllocation);
+  if (in_words && !hin->main_codes) return DM_E_INVALID;
   cudaError_t e = cudaSuccess;
   auto h2d = [&](const void* d, const void* h, size_t n) {
-    if (n && e == cudaSuccess) e = cudaMemcpyAsync(const_cast<void*>(d), h, n, cudaMemcpyHostToDevice, st);
+    if (n && e == cudaSuccess) e = cudaMemcpyAsync(const_cast<void*>(d), h, n, cudaMemcpyHostToDevice, sin);
   };
+  auto d2h = [&](void* hp, const void* dp, size_t n) {
+    if (hp && n && e == cudaSuccess) e = cudaMemcpyAsync(hp, dp, n, cudaMemcpyDeviceToHost, sout);
+  };
+  auto rec = [&](size_t i, cudaStream_t s) {
+    if (e == cudaSuccess) e = cudaEventRecord(I.event(i), s);
+  };
+  auto wait = [&](cudaStream_t s, size_t i) {
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, I.event(i), 0);
+  };
+  // row chunks of N' at multiples of 4096 rows (word-aligned at b and b'), >= 4M rows each, <= 32
+  const uint64_t n_total = hin->n_main + hin->n_delta;
+  const uint64_t K = n_total ? std::max<uint64_t>(1, std::min<uint64_t>(32, n_total >> 22)) : 0;
+  std::vector<uint64_t> cut(K + 1, 0);
+  for (uint64_t k = 1; k < K; ++k) cut[k] = std::max(cut[k - 1], (n_total * k / K) / 4096 * 4096);
+  if (K) cut[K] = n_total;
+  enum { EV_DICT = 0, EV_S1 = 1, EV_IN0 = 2 };  // then EV_IN0 + k (M chunk k in), EV_IN0 + K + k (M' chunk k out)
+  // 1. uploads: U_M and D first, then the main codes chunk by chunk
   h2d(din.main_dict, hin->main_dict, hin->dict_len * E);
-  h2d(din.main_codes, hin->main_codes, in_words * 8);
   h2d(din.delta, hin->delta, hin->n_delta * E);
+  rec(EV_DICT, sin);
+  for (uint64_t k = 0; k < K; ++k) {
+    const uint64_t m0 = std::min(cut[k], hin->n_main), m1 = std::min(cut[k + 1], hin->n_main);
+    if (m1 > m0) {
+      const uint64_t w0 = m0 * hin->main_bits / 64, w1 = host_words(m1, hin->main_bits);
+      h2d(din.main_codes + w0, hin->main_codes + w0, (w1 - w0) * 8);
+    }
+    rec(EV_IN0 + k, sin);
+  }
   if (e != cudaSuccess) return cuda_fail(e);
+  // 2. Steps 1(a)-2(a) as soon as U_M and D are in
   const WsLayout L = ws_layout(hin);
   dm_header* d_hdr = reinterpret_cast<dm_header*>(static_cast<char*>(ws) + L.hdr);
-  dm_status s = merge_async(&din, &dout, ws, wsb, d_hdr, st, false);
-  if (s != DM_OK) return s;
-  e = cudaMemcpyAsync(I.host_hdr, d_hdr, sizeof(dm_header), cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  wait(st, EV_DICT);
   if (e != cudaSuccess) return cuda_fail(e);
-  const dm_header h = *I.host_hdr;
-  if (h.status != DM_OK) return (dm_status)h.status;
-  auto d2h = [&](void* hp, const void* dp, size_t n) {
-    if (hp && n && e == cudaSuccess) e = cudaMemcpyAsync(hp, dp, n, cudaMemcpyDeviceToHost, st);
-  };
+  dm_status s = merge_async(&din, &dout, ws, wsb, d_hdr, st, false, nullptr, MM_DICT);
+  if (s != DM_OK) {
+    cudaStreamSynchronize(sin);
+    return s;
+  }
+  rec(EV_S1, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(I.host_hdr, d_hdr, sizeof(dm_header), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // the one host wait: |U'|, b'
+  if (e != cudaSuccess) return cuda_fail(e);
+  dm_header h = *I.host_hdr;
+  if (h.status != DM_OK) {
+    cudaStreamSynchronize(sin);
+    return (dm_status)h.status;
+  }
+  const uint32_t nb = h.merged_bits;
+  // 3. U' and the requested tables go out while M is still coming in
+  wait(sout, EV_S1);
   d2h(hout->merged_dict, dout.merged_dict, h.merged_dict_len * E);
-  d2h(hout->merged_codes, dout.merged_codes, host_words(hin->n_main + hin->n_delta, h.merged_bits) * 8);
-  d2h(hout->x_main, dout.x_main, hin->dict_len * 4);
-  d2h(hout->x_delta, dout.x_delta, h.delta_dict_len * 4);
+  d2h(hout->x_main, xm, hin->dict_len * 4);
+  d2h(hout->x_delta, xd, h.delta_dict_len * 4);
   d2h(hout->delta_dict, dout.delta_dict, h.delta_dict_len * E);
-  d2h(hout->delta_rank, dout.delta_rank, hin->n_delta * 4);
+  d2h(hout->delta_rank, rk, hin->n_delta * 4);
+  // 4. Step 2(b) chunk by chunk, each M' chunk downloaded as soon as it is written
+  for (uint64_t k = 0; k < K && e == cudaSuccess; ++k) {
+    const uint64_t r0 = cut[k], r1 = cut[k + 1];
+    const uint64_t m0 = std::min(r0, hin->n_main), m1 = std::min(r1, hin->n_main);
+    const uint64_t d0 = std::max(r0, hin->n_main) - hin->n_main, d1 = std::max(r1, hin->n_main) - hin->n_main;
+    wait(st, EV_IN0 + k);
+    dm_column_in cin{};
+    cin.key = hin->key;
+    cin.dict_len = hin->dict_len;
+    cin.main_codes = m1 > m0 ? din.main_codes + m0 * hin->main_bits / 64 : nullptr;
+    cin.n_main = m1 - m0;
+    cin.main_bits = hin->main_bits;
+    cin.n_delta = d1 - d0;
+    dm_column_out cout{};
+    cout.merged_codes = dout.merged_codes + r0 * nb / 64;
+    cout.merged_codes_cap_words = host_words(r1, nb) - r0 * nb / 64;
+    if (e == cudaSuccess) e = launch_recompress(&cin, &cout, xm, xd, rk + d0, d_hdr, st, nb);
+    rec(EV_IN0 + K + k, st);
+    wait(sout, EV_IN0 + K + k);
+    d2h(hout->merged_codes + r0 * nb / 64, cout.merged_codes, cout.merged_codes_cap_words * 8);
+  }
+  if (e == cudaSuccess) e = cudaMemcpyAsync(I.host_hdr, d_hdr, sizeof(dm_header), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(sout);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(sin);
   if (e != cudaSuccess) return cuda_fail(e);
+  h = *I.host_hdr;
   hout->merged_dict_len = h.merged_dict_len;
   hout->delta_dict_len = h.delta_dict_len;
   hout->merged_bits = h.merged_bits;
-  return DM_OK;
+  return (dm_status)h.status;
 }
 
 uint64_t dm_launch_count(void) { return g_launches.load(); }

@@ -393,6 +393,17 @@ static int xc_raw_warps() {
   return v;
 }
 
+// Share of the SM slots a recompress launch may take (DM_REC_GRID_PCT, 1..100;
+// experiments: a smaller share lets concurrent columns' Step 1 kernels co-run).
+static int rec_grid_percent() {
+  static const int v = [] {
+    const char* e = std::getenv("DM_REC_GRID_PCT");
+    const int x = e ? std::atoi(e) : 100;
+    return (x >= 1 && x <= 100) ? x : 100;
+  }();
+  return v;
+}
+
 // Shared-memory bytes left for XC next to a kRecStagesXc-deep ring.
 static uint32_t xc_smem_budget(uint32_t in_stage) {
   static int optin = [] {
@@ -416,7 +427,8 @@ cudaError_t launch_nb(const dm_column_in* in, const dm_column_out* out, const ui
   auto go = [&](auto kern, size_t smem, uint32_t budget, int threads = kRecThreads, int groups = kRecGroups) {
     const uint64_t nchunks = (n_total + 32ull * groups - 1) / (32ull * groups);
     const int occ = occupancy((const void*)kern, threads, smem);
-    const unsigned grid = (unsigned)std::min<uint64_t>(nchunks, (uint64_t)sms * occ);
+    const unsigned grid = (unsigned)std::max<uint64_t>(
+        1, std::min<uint64_t>(nchunks, (uint64_t)sms * occ * rec_grid_percent() / 100));
     launch_k(kern, grid, threads, smem, st, in->main_codes, in->n_main, in->main_bits, in->dict_len, xm, xd, rank,
                                           in->n_delta, out->merged_codes, hdr,
                                           groups == kRecGroups ? in_stage : in_stage_xc, fixed_bits, xrec, xoffs,

@@ -285,3 +285,35 @@ def test_cfg5_reduced_scale_width_growth():
     M, r = run_gpu(col)
     ref = compare(col, M, r)
     assert r.merged_len == col.dict_len + col.n_delta
+
+
+@pytest.mark.parametrize("key,n_main,dict_len,n_delta,p_new", [
+    ("u64", 13_000_003, 300_000, 200_001, 0.2),    # 3 chunks, ragged
+    ("b16", 4_000_000, 50_000, 9_000_001, 0.6),    # delta rows span chunks
+    ("u32", 9_000_000, 2_000, 1, 1.0),
+])
+def test_host_entry_point_pipelined(key, n_main, dict_len, n_delta, p_new):
+    """dm_merge_column_host over several row chunks (copy-in / compute / copy-out
+    pipeline): U', M' and the requested tables bit-exact; pinned and pageable."""
+    import paper_1109_6885_b200 as dm
+    col = datagen.make_random_case(5 + n_delta, n_main, dict_len, n_delta, p_new, key=key)
+    ref = oracle.merge(col)
+    E = col.key_bytes
+    host = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int64 if E == 8 else np.int32 if E == 4
+                                                                    else np.uint8).copy())
+    UM, D = host(col.main_dict), host(col.delta)
+    if E == 16:
+        UM, D = UM.reshape(-1, 16), D.reshape(-1, 16)
+    Mw = torch.from_numpy(oracle.pack(col.main_codes, col.main_bits).view(np.int64).copy())
+    for pinned in (True, False):
+        ctx = dm.HostContext(0)
+        args = [t.pin_memory() if pinned else t for t in (UM, Mw, D)]
+        Uo = torch.empty((col.dict_len + col.n_delta,) + tuple(UM.shape[1:]), dtype=UM.dtype)
+        Mo = torch.empty(dm.words(col.n_main + col.n_delta, 32), dtype=torch.int64)
+        if pinned:
+            Uo, Mo = Uo.pin_memory(), Mo.pin_memory()
+        n, bits, nud = ctx.merge(args[0], args[1], col.n_main, col.main_bits, args[2], Uo, Mo)
+        assert n == ref.merged_len and bits == ref.merged_bits and nud == ref.delta_dict.shape[0]
+        assert np.array_equal(keys_np(Uo[:n], col.key), ref.merged_dict)
+        assert np.array_equal(Mo[: ref.merged_words.size].numpy().view(np.uint64), ref.merged_words)
+        ctx.close()
