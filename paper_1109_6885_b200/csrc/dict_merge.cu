@@ -659,7 +659,7 @@ cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, const void*
   }
   const uint64_t nt = L.ntiles_merge;
   uint64_t* part = reinterpret_cast<uint64_t*>(ws + L.part);
-  const bool xc = xc_wanted(in->dict_len) || (force_xc && in->dict_len > 0);
+  const bool xc = xc_wanted(in) || (force_xc && in->dict_len > 0);
   uint32_t* rblk = xc ? reinterpret_cast<uint32_t*>(ws + L.xc_rblk) : nullptr;
   uint8_t* offs = xc ? reinterpret_cast<uint8_t*>(ws + L.xc_offs) : nullptr;
   const uint32_t xs = xc_shift(in);

@@ -276,7 +276,7 @@ static dm_status merge_async(const dm_column_in* in, const dm_column_out* out, v
   if ((e = dbg("step 1(b)")) != cudaSuccess) return cuda_fail(e);
   mark(2);
   // Step 2(b): M' (Eq 11).
-  const bool xc = xc_wanted(in->dict_len);
+  const bool xc = xc_wanted(in);
   if (with_step2 && tuning(3) == 1) {
     if ((e = launch_naive_step2(in, out, d_header, st)) != cudaSuccess) return cuda_fail(e);
   } else if (with_step2 && (e = launch_recompress(in, out, xm, xd, rank, d_header, st, 0,

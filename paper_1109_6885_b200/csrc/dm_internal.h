@@ -52,10 +52,21 @@ enum XMode { XM_RAW_GLOBAL = 0, XM_RAW_SMEM = 1, XM_XC_SMEM = 2, XM_XC_GLOBAL = 
 int tuning(int knob);
 // Whether a merge builds XC at all: only when the plain X_M is too big for smem.
 inline bool xc_enabled(uint64_t dict_len) { return dict_len * 4 > kRecSmemXBytes; }
-// Whether this merge builds XC: auto only when the plain X_M exceeds kXcGlobalMinBytes.
-inline bool xc_wanted(uint64_t dict_len) {
+// Auto mode, plain X_M between kRecSmemXBytes and kXcGlobalMinBytes: build XC
+// with 256-code blocks when its records leave room in shared memory for the
+// lists; Step 2(b) then decodes it from shared memory if the lists turn out
+// short (decided on the device from |U'|), else gathers the plain X_M from L2.
+constexpr uint64_t kXcSmemRecMax = 112 * 1024;
+inline bool xc_smem_candidate(const dm_column_in* in) {
+  return tuning(0) == 0 && in->dict_len * 4 > kRecSmemXBytes && in->dict_len * 4 <= kXcGlobalMinBytes &&
+         xc_nsb(in->dict_len, 8) * kXcRecBytes <= kXcSmemRecMax;
+}
+// Whether this merge builds XC: auto when the plain X_M exceeds kXcGlobalMinBytes
+// or XC may fit in shared memory.
+inline bool xc_wanted(const dm_column_in* in) {
   const int k = tuning(0);
-  return k == 1 ? false : k == 0 ? dict_len * 4 > kXcGlobalMinBytes : xc_enabled(dict_len);
+  return k == 1 ? false : k == 0 ? in->dict_len * 4 > kXcGlobalMinBytes || xc_smem_candidate(in)
+                                 : xc_enabled(in->dict_len);
 }
 // Step 1(a) dedup front end (NEXT1): knob 2 = 0 auto (16-byte keys with
 // N_D >= 2^16: 16 radix passes make repeats expensive), 1 off, 2 on.
@@ -69,7 +80,7 @@ inline bool dedup_wanted(const dm_column_in* in) {
 int xc_shift_override();  // knob 4 / DM_XC_SHIFT: 7 or 8, 0 = none
 inline uint32_t xc_shift(const dm_column_in* in) {
   if (const int o = xc_shift_override()) return (uint32_t)o;
-  if (tuning(0) == 2) return 8;
+  if (tuning(0) == 2 || xc_smem_candidate(in)) return 8;
   return in->n_delta * 256 <= 6 * in->dict_len ? 8u : 7u;
 }
 

@@ -85,6 +85,47 @@ __device__ __forceinline__ uint32_t count_lt(uint32_t w, uint32_t ob, int i, uin
   const uint32_t m = shl32(0xffffffffu, 8 * a) & (z >= 4 ? 0xffffffffu : shl32(1u, 8 * z) - 1u);
   return __popc(__vcmpltu4(w, ob) & m);
 }
+// Per-byte x < y over four packed bytes, as the byte's most significant bit
+// (no cross-byte borrow: each byte of (x | 0x80) - (y & 0x7f) stays >= 1).
+__device__ __forceinline__ uint32_t bytes_lt_msb(uint32_t x, uint32_t y, uint32_t y7) {
+  const uint32_t z = (x | 0x80808080u) - y7;  // byte msb = (x & 0x7f) >= (y & 0x7f)
+  // borrow out of x - y: (~x & y) | (~(x ^ y) & ~z), per byte msb
+  return ((~x & y) | (~(x ^ y) & ~z)) & 0x80808080u;
+}
+
+// Lean shared-memory lookup (blocks of 256 codes, xs = 8): one 8-byte record,
+// an 8-byte window of the list read as two (a third, predicated, when the list
+// starts late in a word) conflict-prone shared loads, and a SIMD byte compare.
+// Lists longer than 8 and flagged superblocks take a rare slow path.  Counts
+// are those of xc_lookup; only the instruction and shared-load budget differ
+// (the kernel is bound by both).
+__device__ __forceinline__ uint32_t xc_lookup_smem8(uint32_t code, const uint2* __restrict__ rec,
+                                                    const uint32_t* __restrict__ offs32,
+                                                    const uint32_t* __restrict__ XM) {
+  const uint2 r = rec[code >> 10];
+  const uint32_t ry = (int)r.x < 0 ? 0u : r.y;  // flagged: empty list at R (keeps the window in bounds)
+  const uint32_t t8 = (code >> 5) & 24u;
+  const uint32_t s_rel = ((ry << 8) >> t8) & 255u, e_rel = (ry >> t8) & 255u;
+  const uint32_t start = (r.x & 0x7fffffffu) + s_rel;
+  const uint32_t n = e_rel - s_rel;
+  const uint32_t s3 = start & 3u, sh = 8u * s3;
+  const uint32_t* w = offs32 + (start >> 2);
+  const uint32_t w0 = w[0], w1 = w[1];
+  const uint32_t w2 = n + s3 > 8u ? w[2] : 0u;
+  const uint32_t a = __funnelshift_r(w0, w1, sh), b = __funnelshift_r(w1, w2, sh);  // bytes [start, start + 8)
+  const uint32_t y = (code & 255u) * 0x01010101u, y7 = y & 0x7f7f7f7fu;
+  const uint32_t k8 = 8u * umin32(n, 8u);
+  const uint32_t ma = ~shl32(0xffffffffu, k8), mb = shr32(0xffffffffu, 64u - k8);
+  uint32_t cnt = __popc(bytes_lt_msb(a, y, y7) & ma) + __popc(bytes_lt_msb(b, y, y7) & mb);
+  if (__builtin_expect(n > 8u || (int)r.x < 0, 0)) {
+    if ((int)r.x < 0) return __ldg(XM + code);  // flagged superblock: plain X_M
+    const uint32_t o = code & 255u;
+    for (uint32_t q = start + 8; q < start + n; ++q) cnt += ((offs32[q >> 2] >> (8 * (q & 3u))) & 255u) < o ? 1u : 0u;
+  }
+  return code + start + cnt;
+}
+
+// xs: block shift (blocks of 2^xs codes, superblocks of 4 blocks).
 // xs: block shift (blocks of 2^xs codes, superblocks of 4 blocks).
 template <bool SM>
 __device__ __forceinline__ uint32_t xc_lookup(uint32_t code, uint32_t xs, const uint2* __restrict__ rec,
@@ -147,7 +188,7 @@ __global__ void __launch_bounds__(rec_threads<XMODE>(), XMODE == XM_XC_SMEM ? 1 
                                                             uint32_t in_stage_bytes, uint32_t fixed_bits,
                                                             const uint2* __restrict__ xrec,
                                                             const uint8_t* __restrict__ xoffs, uint32_t xc_budget,
-                                                            int raw_warps, uint32_t xs) {
+                                                            uint32_t xc_dens, uint32_t xs) {
   pdl_prologue();
   constexpr int G = rec_groups<XMODE>();
   constexpr int S = XMODE == XM_XC_SMEM ? kRecStagesXc : kRecStages;
@@ -164,7 +205,10 @@ __global__ void __launch_bounds__(rec_threads<XMODE>(), XMODE == XM_XC_SMEM ? 1 
     const uint64_t n_new = hdr->merged_dict_len - dict_len;
     xc_offs_bytes = (n_new + 15) & ~15ull;
     // + 16: the two-word read may touch up to 8 bytes past the last entry
-    const bool fits = ((nsb * kXcRecBytes + 15) & ~15ull) + xc_offs_bytes + 16 <= xc_budget;
+    // xc_dens (auto mode): also require n_new * 2^xc_dens <= |U_M|, i.e. short
+    // lists (cfg2: 2.6 entries per 256-code block), else the L2 companion runs
+    const bool fits = ((nsb * kXcRecBytes + 15) & ~15ull) + xc_offs_bytes + 16 <= xc_budget &&
+                      (xc_dens == 0 || (n_new << xc_dens) <= dict_len);
     if ((XMODE == XM_XC_SMEM) != fits) return;
   }
 
@@ -233,11 +277,8 @@ __global__ void __launch_bounds__(rec_threads<XMODE>(), XMODE == XM_XC_SMEM ? 1 
   const uint32_t umask = b == 32 ? 0xffffffffu : ((1u << b) - 1);
   const uint32_t pr0 = (32 * lane) / nb, pop = 32 * lane - pr0 * nb;
   uint32_t* out32 = reinterpret_cast<uint32_t*>(Mout);
+  const uint32_t dict_len32 = (uint32_t)dict_len;  // < 2^32 (validated by the ABI)
   bool bad = false;
-  // XM_XC_SMEM: the first raw_warps consumer warps gather the plain X_M through
-  // L2 (bound by the L1 request pipeline), the others decode XC from shared
-  // memory (bound by instruction issue) -- two different limits run in parallel.
-  const bool raw_warp = (int)warp < raw_warps;
 
   for (uint64_t k = 0;; ++k) {
     const uint64_t c = blockIdx.x + k * gridDim.x;
@@ -248,14 +289,14 @@ __global__ void __launch_bounds__(rec_threads<XMODE>(), XMODE == XM_XC_SMEM ? 1 
     const uint64_t row_base = c * R;
     uint32_t v[U];
     auto translate = [&](uint32_t code) -> uint32_t {
-      if (code >= dict_len) {
+      if (code >= dict_len32) {
         bad = true;
         code = 0;
       }
       if constexpr (XMODE == XM_RAW_SMEM)
         return sx[code];
       else if constexpr (XMODE == XM_XC_SMEM)
-        return raw_warp ? ld_gather_u32(XM + code, pol_x) : xc_lookup<true>(code, xs, srec, soffs, XM, pol_x);
+        return xc_lookup_smem8(code, srec, soffs, XM);
       else if constexpr (XMODE == XM_XC_GLOBAL)
         return xc_lookup<false>(code, xs, xrec, reinterpret_cast<const uint32_t*>(xoffs), XM, pol_x);
       else
@@ -381,18 +422,6 @@ __global__ void __launch_bounds__(256) k_unpack(const uint32_t* __restrict__ wor
   }
 }
 
-// Consumer warps of the XC shared-memory kernel that gather the plain X_M
-// instead (DM_XC_RAW_WARPS, experiments).  Default 0: with XC holding ~220 KB
-// of shared memory the L1 is too small for L2 gathers (cfg2: 8 raw warps
-// 0.50 ms, 28 raw warps 0.79 ms, 0 raw warps 0.433 ms).
-static int xc_raw_warps() {
-  static const int v = [] {
-    const char* e = std::getenv("DM_XC_RAW_WARPS");
-    return e ? std::atoi(e) : 0;
-  }();
-  return v;
-}
-
 // Share of the SM slots a recompress launch may take (DM_REC_GRID_PCT, 1..100;
 // experiments: a smaller share lets concurrent columns' Step 1 kernels co-run).
 static int rec_grid_percent() {
@@ -424,6 +453,7 @@ cudaError_t launch_nb(const dm_column_in* in, const dm_column_out* out, const ui
   const uint32_t in_stage_xc = rec_groups<XM_XC_SMEM>() * in->main_bits * 4 + 16;
   const int sms = device_sms();
   const uint64_t n_total = in->n_main + in->n_delta;
+  uint32_t dens = 0;
   auto go = [&](auto kern, size_t smem, uint32_t budget, int threads = kRecThreads, int groups = kRecGroups) {
     const uint64_t nchunks = (n_total + 32ull * groups - 1) / (32ull * groups);
     const int occ = occupancy((const void*)kern, threads, smem);
@@ -432,7 +462,7 @@ cudaError_t launch_nb(const dm_column_in* in, const dm_column_out* out, const ui
     launch_k(kern, grid, threads, smem, st, in->main_codes, in->n_main, in->main_bits, in->dict_len, xm, xd, rank,
                                           in->n_delta, out->merged_codes, hdr,
                                           groups == kRecGroups ? in_stage : in_stage_xc, fixed_bits, xrec, xoffs,
-                                          budget, xc_raw_warps(), xs);
+                                          budget, dens, xs);
     note_launch();
   };
   const size_t ring = 128 + (size_t)kRecStages * in_stage;
@@ -447,8 +477,10 @@ cudaError_t launch_nb(const dm_column_in* in, const dm_column_out* out, const ui
   }
   // compact table available: the smem variant (if its records can fit at all)
   // plus an L2 companion; which one runs is decided on the device from |U'|
-  const bool want_smem = knob == 2;  // measured slower than the L2 gather on cfg2: opt-in
-  if (knob == 0 && in->dict_len * 4 <= kXcGlobalMinBytes) {
+  const bool auto_smem = knob == 0 && xc_smem_candidate(in);
+  const bool want_smem = (knob == 2 || auto_smem) && xs == 8;
+  if (auto_smem) dens = 6;  // <= 4 entries per 256-code block on average
+  if (knob == 0 && !auto_smem && in->dict_len * 4 <= kXcGlobalMinBytes) {
     go(k_recompress<NB, XM_RAW_GLOBAL>, ring, 0);
     return cudaGetLastError();
   }
@@ -469,7 +501,7 @@ cudaError_t launch_nb(const dm_column_in* in, const dm_column_out* out, const ui
 
 using XcKernel = void (*)(const uint64_t*, uint64_t, uint32_t, uint64_t, const uint32_t*, const uint32_t*,
                          const uint32_t*, uint64_t, uint64_t*, dm_header*, uint32_t, uint32_t, const uint2*,
-                         const uint8_t*, uint32_t, int, uint32_t);
+                         const uint8_t*, uint32_t, uint32_t, uint32_t);
 template <int... I>
 constexpr auto make_xc_table(std::integer_sequence<int, I...>) {
   return std::array<XcKernel, sizeof...(I)>{&k_recompress<I, XM_XC_GLOBAL>...};
