@@ -275,8 +275,14 @@ dm_status dm_merge_column_host(dm_ctx* ctx, const dm_column_in* in, dm_column_ou
  *   every tuple's value binary-searched in U' -- a measured baseline only.
  * knob 4 = XC block shift: 0 (default) per column from N_D / |U_M|; 7 or 8
  *   fixed (the sharded Step 1(b) needs one shift for all value ranges).
- * The process starts with knobs 0..4 = $DM_XMODE / $DM_MERGE / $DM_DEDUP /
- * $DM_STEP2 / $DM_XC_SHIFT when set (experiments), else 0.
+ * knob 5 = Step 1(a) sort: 0 (default) auto -- the bucket path for
+ *   2^11 <= N_D <= 2^23 (one counting pass into ~N_D/4 buckets by the top bits
+ *   below the keys' common prefix, then each key ranked among its bucket mates),
+ *   else the LSD radix passes; 1 LSD passes only; 2 bucket path for any N_D.  A
+ *   skewed key set (a bucket above 256 keys) falls back to the LSD passes on the
+ *   device.  Same U_D and r either way.  Changes the workspace size.
+ * The process starts with knobs 0..5 = $DM_XMODE / $DM_MERGE / $DM_DEDUP /
+ * $DM_STEP2 / $DM_XC_SHIFT / $DM_SORT1A when set (experiments), else 0.
  * Returns DM_OK, or DM_E_INVALID for an unknown knob or value.  Affects calls
  * made after it returns (a captured CUDA graph keeps the kernels it recorded). */
 int dm_set_tuning(int knob, int value);

@@ -81,8 +81,9 @@ template <class KT>
 __global__ void __launch_bounds__(256) k_hist(const void* __restrict__ D, uint64_t n_host,
                                               const unsigned long long* __restrict__ n_dev,
                                               uint32_t* __restrict__ hist, uint32_t* done,
-                                              SortPlan* __restrict__ plan) {
+                                              SortPlan* __restrict__ plan, const BucketState* __restrict__ gate) {
   pdl_prologue();
+  if (gate && !gate->overflow) return;  // the bucket path sorted D (its plan stands)
   constexpr int P = KT::kPasses;
   const uint64_t n = n_dev ? (uint64_t)*n_dev : n_host;
   __shared__ uint32_t s_h[P][256];
@@ -358,6 +359,203 @@ __global__ void __launch_bounds__(kUniqThreads) k_unique(const void* __restrict_
   }
 }
 
+// ------------------------------------------------------------ bucket path
+// Step 1(a) for N_D <= 2^23 without LSD passes.  Each LSD pass over ~10^6 keys is
+// a latency-bound kernel of ~16 us (look-back chain, one tile per SM), and a
+// 48-bit key needs six of them.  Instead, one counting pass places every key in
+// one of B ~ N_D / 4 buckets by the top log2 B bits below the prefix shared by
+// all keys (so bucket order = key order), and each key then finds its final
+// position inside its (small) bucket by comparing with its bucket mates:
+//   k_bk_range    OR of (k ^ k0) over D -> the highest differing bit h; digit =
+//                 bits [h + 1 - log2 B, h]; zeroes the counts
+//   k_bk_count    counts per bucket (global atomics)
+//   k_bk_scan     exclusive offsets (single pass, decoupled look-back); a bucket
+//                 above kBkMaxBucket raises the overflow flag
+//   k_bk_scatter  key -> its bucket (slot from an atomic cursor: unordered)
+//   k_bk_local    rank among the bucket mates by (key, index) -> sorted order
+// then k_unique as after the LSD passes.  Skewed key sets (a dense cluster, an
+// outlier, heavy repeats without the dedup front end) overflow a bucket: the
+// bucket kernels stop and the LSD passes, launched behind them and gated on
+// the flag, sort instead.
+template <class KT>
+struct Bits128;
+template <>
+struct Bits128<KeyU64> {
+  __device__ __forceinline__ static void get(uint64_t k, uint64_t& hi, uint64_t& lo) { hi = 0; lo = k; }
+};
+template <>
+struct Bits128<KeyU32> {
+  __device__ __forceinline__ static void get(uint32_t k, uint64_t& hi, uint64_t& lo) { hi = 0; lo = k; }
+};
+template <>
+struct Bits128<KeyB16> {
+  __device__ __forceinline__ static void get(K128 k, uint64_t& hi, uint64_t& lo) { hi = k.hi; lo = k.lo; }
+};
+template <class KT>
+__device__ __forceinline__ uint32_t bk_digit(typename KT::K k, uint32_t s, uint32_t mask) {
+  uint64_t hi, lo;
+  Bits128<KT>::get(k, hi, lo);
+  const uint64_t v = s >= 64 ? hi >> (s - 64) : s == 0 ? lo : (lo >> s) | (hi << (64 - s));
+  return (uint32_t)v & mask;
+}
+
+template <class KT>
+__global__ void __launch_bounds__(256) k_bk_range(const void* __restrict__ D, uint64_t n_host,
+                                                  const unsigned long long* __restrict__ n_dev,
+                                                  BucketState* st, uint32_t* __restrict__ cnt, uint32_t bits,
+                                                  SortPlan* __restrict__ plan) {  // cnt: the counts to zero
+  pdl_prologue();
+  const uint64_t n = n_dev ? (uint64_t)*n_dev : n_host;
+  const uint64_t nb = 1ull << bits;
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, nthr = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = tid; i < nb; i += nthr) cnt[i] = 0;
+  uint64_t h0 = 0, l0 = 0, dh = 0, dl = 0;
+  if (n) Bits128<KT>::get(KT::load(D, 0), h0, l0);
+  for (uint64_t i = tid; i < n; i += nthr) {
+    uint64_t h, l;
+    Bits128<KT>::get(KT::load(D, i), h, l);
+    dh |= h ^ h0;
+    dl |= l ^ l0;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    dh |= __shfl_xor_sync(FULL, dh, o);
+    dl |= __shfl_xor_sync(FULL, dl, o);
+  }
+  __shared__ unsigned long long s_h, s_l;
+  __shared__ bool s_last;
+  if (threadIdx.x == 0) s_h = s_l = 0;
+  __syncthreads();
+  if (lane_id() == 0) {
+    atomicOr(&s_h, (unsigned long long)dh);
+    atomicOr(&s_l, (unsigned long long)dl);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // one global atomic per block and word
+    if (s_h) atomicOr(&st->diff_hi, s_h);
+    if (s_l) atomicOr(&st->diff_lo, s_l);
+    __threadfence();
+    s_last = atomicAdd(&st->done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last || threadIdx.x != 0) return;
+  __threadfence();
+  const uint64_t H = __ldcg(&st->diff_hi), Lo = __ldcg(&st->diff_lo);
+  const int h = H ? 127 - __clzll((long long)H) : Lo ? 63 - __clzll((long long)Lo) : -1;
+  st->shift = h + 1 > (int)bits ? (uint32_t)(h + 1 - (int)bits) : 0u;
+  // the LSD passes stay idle unless a bucket overflows (k_hist then rebuilds
+  // this plan and k_unique runs)
+  for (int p = 0; p < 16; ++p) plan->active[p] = 0;
+  plan->final_sel = SEL_BUF0;
+  plan->n_active = 0;
+}
+
+template <class KT>
+__global__ void __launch_bounds__(256) k_bk_count(const void* __restrict__ D, uint64_t n_host,
+                                                  const unsigned long long* __restrict__ n_dev,
+                                                  const BucketState* __restrict__ st, uint32_t* __restrict__ off,
+                                                  uint32_t bits) {
+  pdl_prologue();
+  const uint64_t n = n_dev ? (uint64_t)*n_dev : n_host;
+  const uint32_t s = st->shift, mask = (uint32_t)((1ull << bits) - 1);
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    atomicAdd(off + bk_digit<KT>(KT::load(D, i), s, mask), 1u);
+}
+
+// In place: off[d] = #keys in buckets < d (off[B] = n), cur[d] = off[d]; a
+// bucket above kBkMaxBucket keys raises the overflow flag.
+__global__ void __launch_bounds__(256) k_bk_scan(uint32_t* __restrict__ off, uint32_t* __restrict__ cur,
+                                                 uint64_t nb, uint64_t* status, uint32_t* counter,
+                                                 BucketState* st) {
+  pdl_prologue();
+  constexpr int ITEMS = kBkScanItems, TILE = 256 * ITEMS;
+  __shared__ uint32_t s_warp[9];
+  __shared__ uint64_t s_excl;
+  __shared__ uint32_t s_tile;
+  if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
+  __syncthreads();
+  const uint64_t tile = s_tile;
+  const uint64_t p0 = tile * TILE + threadIdx.x * ITEMS;  // nb is a multiple of TILE
+  uint32_t v[ITEMS], sum = 0, mx = 0;
+#pragma unroll
+  for (int i = 0; i < ITEMS; i += 4) {
+    const uint4 q = *reinterpret_cast<const uint4*>(off + p0 + i);
+    v[i] = q.x, v[i + 1] = q.y, v[i + 2] = q.z, v[i + 3] = q.w;
+  }
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    sum += v[i];
+    mx = v[i] > mx ? v[i] : mx;
+  }
+  if (__any_sync(FULL, mx > kBkMaxBucket) && lane_id() == 0) atomicOr(&st->overflow, 1u);
+  uint32_t tile_sum;
+  const uint32_t texcl = block_exclusive_scan<256>(sum, s_warp, tile_sum);
+  if (threadIdx.x < 32) {
+    const uint64_t e = lookback_exclusive(status, tile, tile_sum);
+    if (threadIdx.x == 0) s_excl = e;
+  }
+  __syncthreads();
+  uint32_t run = (uint32_t)(s_excl + texcl);
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const uint32_t x = v[i];
+    v[i] = run;
+    run += x;
+  }
+#pragma unroll
+  for (int i = 0; i < ITEMS; i += 4) {
+    *reinterpret_cast<uint4*>(off + p0 + i) = make_uint4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+    *reinterpret_cast<uint4*>(cur + p0 + i) = make_uint4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+  }
+  if ((tile + 1) * TILE >= nb && threadIdx.x == 255) off[nb] = run;
+}
+
+template <class KT>
+__global__ void __launch_bounds__(256) k_bk_scatter(const void* __restrict__ D, uint64_t n_host,
+                                                    const unsigned long long* __restrict__ n_dev,
+                                                    const BucketState* __restrict__ st, uint32_t* __restrict__ cur,
+                                                    uint32_t bits, void* __restrict__ kout,
+                                                    uint32_t* __restrict__ vout) {
+  pdl_prologue();
+  if (st->overflow) return;
+  const uint64_t n = n_dev ? (uint64_t)*n_dev : n_host;
+  const uint32_t s = st->shift, mask = (uint32_t)((1ull << bits) - 1);
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const typename KT::K k = KT::load(D, i);
+    const uint32_t pos = atomicAdd(cur + bk_digit<KT>(k, s, mask), 1u);
+    NumStore<KT>::st(kout, pos, k);
+    vout[pos] = (uint32_t)i;
+  }
+}
+
+// Final position of each key: its bucket's offset + #{bucket mates ordered
+// before it by (key, original index)} -- a permutation, sorted by key.
+template <class KT>
+__global__ void __launch_bounds__(256) k_bk_local(const void* __restrict__ kin, const uint32_t* __restrict__ vin,
+                                                  uint64_t n_host, const unsigned long long* __restrict__ n_dev,
+                                                  const BucketState* __restrict__ st,
+                                                  const uint32_t* __restrict__ off, uint32_t bits,
+                                                  void* __restrict__ kout, uint32_t* __restrict__ vout) {
+  pdl_prologue();
+  if (st->overflow) return;
+  using K = typename KT::K;
+  const uint64_t n = n_dev ? (uint64_t)*n_dev : n_host;
+  const uint32_t s = st->shift, mask = (uint32_t)((1ull << bits) - 1);
+  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n; p += (uint64_t)gridDim.x * blockDim.x) {
+    const K k = NumStore<KT>::ld(kin, p);
+    const uint32_t id = vin[p];
+    const uint32_t d = bk_digit<KT>(k, s, mask);
+    const uint32_t lo = off[d], hi = off[d + 1];
+    uint32_t r = lo;
+    for (uint32_t q = lo; q < hi; ++q) {
+      const K kq = NumStore<KT>::ld(kin, q);
+      r += KT::lt(kq, k) ? 1u : (KT::eq(kq, k) && vin[q] < id) ? 1u : 0u;
+    }
+    NumStore<KT>::st(kout, r, k);
+    vout[r] = id;
+  }
+}
+
 // ------------------------------------------------------------ dedup front end
 // NEXT1: the paper gets U_D by "extracting the unique values"
 // from a tree it maintained at insert time; a delta with many
@@ -476,8 +674,30 @@ cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, void* udict
     n_dev = n_dist;
     sort_rank = reinterpret_cast<uint32_t*>(ws + L.dd_rank);
   }
+  const BucketState* gate = nullptr;
+  if (L.bucket) {
+    BucketState* bst = reinterpret_cast<BucketState*>(ws + L.bk_state);
+    uint32_t* off = reinterpret_cast<uint32_t*>(ws + L.bk_off);
+    uint32_t* cur = reinterpret_cast<uint32_t*>(ws + L.bk_cur);
+    const uint64_t nb = 1ull << L.bk_bits;
+    const int sms = device_sms();
+    const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, (uint64_t)sms * 8));
+    const unsigned g_range = (unsigned)std::max<uint64_t>(
+        1, std::min<uint64_t>((std::max<uint64_t>(n, nb) + 255) / 256, (uint64_t)sms * 8));
+    launch_k(k_bk_range<KT>, g_range, 256, 0, st, D, n, n_dev, bst, off, L.bk_bits, plan);
+    launch_k(k_bk_count<KT>, g, 256, 0, st, D, n, n_dev, (const BucketState*)bst, off, L.bk_bits);
+    launch_k(k_bk_scan, (unsigned)(nb / (256 * kBkScanItems)), 256, 0, st, off, cur, nb,
+             reinterpret_cast<uint64_t*>(ws + L.bk_status), counters + CNT_BKSCAN, bst);
+    launch_k(k_bk_scatter<KT>, g, 256, 0, st, D, n, n_dev, (const BucketState*)bst, cur, L.bk_bits,
+             (void*)(ws + L.keys1), reinterpret_cast<uint32_t*>(ws + L.vals1));
+    launch_k(k_bk_local<KT>, g, 256, 0, st, (const void*)(ws + L.keys1),
+             reinterpret_cast<const uint32_t*>(ws + L.vals1), n, n_dev, (const BucketState*)bst,
+             (const uint32_t*)off, L.bk_bits, (void*)(ws + L.keys0), reinterpret_cast<uint32_t*>(ws + L.vals0));
+    note_launch(5);
+    gate = bst;
+  }
   const int hist_blocks = (int)std::min<uint64_t>((n + 4095) / 4096, 148 * 4);
-  launch_k(k_hist<KT>, hist_blocks, 256, 0, st, D, n, n_dev, hist, counters + CNT_HIST, plan);
+  launch_k(k_hist<KT>, hist_blocks, 256, 0, st, D, n, n_dev, hist, counters + CNT_HIST, plan, gate);
   note_launch();
   constexpr bool U64 = KT::kBytes <= 8;  // tile shape: 8-byte and 4-byte keys alike
   switch (sort_variant()) {  // must match sort_tile_keys() (workspace layout)

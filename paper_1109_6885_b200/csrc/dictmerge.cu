@@ -105,9 +105,9 @@ static int env_knob(const char* name, int hi) {
   const int v = s ? std::atoi(s) : 0;
   return (v >= 0 && v <= hi) ? v : 0;
 }
-static std::atomic<int> g_tuning[5] = {env_knob("DM_XMODE", 3), env_knob("DM_MERGE", 2), env_knob("DM_DEDUP", 2),
-                                       env_knob("DM_STEP2", 1), env_knob("DM_XC_SHIFT", 8)};
-int tuning(int knob) { return (knob >= 0 && knob < 5) ? g_tuning[knob].load(std::memory_order_relaxed) : 0; }
+static std::atomic<int> g_tuning[6] = {env_knob("DM_XMODE", 3), env_knob("DM_MERGE", 2), env_knob("DM_DEDUP", 2),
+                                       env_knob("DM_STEP2", 1), env_knob("DM_XC_SHIFT", 8), env_knob("DM_SORT1A", 2)};
+int tuning(int knob) { return (knob >= 0 && knob < 6) ? g_tuning[knob].load(std::memory_order_relaxed) : 0; }
 
 int xc_shift_override() {
   const int x = tuning(4);  // knob 4 (DM_XC_SHIFT): the sharded Step 1(b) fixes one shift for all ranges
@@ -151,6 +151,12 @@ WsLayout ws_layout(const dm_column_in* in) {
   L.status_sort = take((size_t)L.npass * L.ntiles_sort * 256 * sizeof(uint32_t));
   L.status_unique = take(L.ntiles_unique * sizeof(uint64_t));
   L.status_merge = take((L.ntiles_merge + 1) * sizeof(uint64_t));  // per tile (single-pass look-back)
+  L.bucket = bucket_wanted(in);
+  L.bk_bits = L.bucket ? bucket_bits(nD) : 0;
+  if (L.bucket) {
+    L.bk_state = take(sizeof(BucketState));
+    L.bk_status = take(((1ull << L.bk_bits) / (256 * kBkScanItems) + 1) * sizeof(uint64_t));
+  }
   L.zero_bytes = o;
   L.plan = take(sizeof(SortPlan));
   L.keys0 = take(nD * E);
@@ -167,6 +173,10 @@ WsLayout ws_layout(const dm_column_in* in) {
   L.xc_rblk = take((xc_nblk(in->dict_len, kXcMinShift) + 1) * 4);  // sized for the smallest blocks
   L.xc_rec = take(xc_nsb(in->dict_len, kXcMinShift) * kXcRecBytes);
   L.xc_offs = take(nD + 16);
+  if (L.bucket) {
+    L.bk_off = take(((1ull << L.bk_bits) + 1) * 4);
+    L.bk_cur = take((1ull << L.bk_bits) * 4);
+  }
   L.dedup = dedup_wanted(in);
   if (L.dedup) {
     uint64_t cap = 1024;
@@ -367,8 +377,8 @@ struct dm_ctx {
 extern "C" {
 
 int dm_set_tuning(int knob, int value) {
-  static const int hi[5] = {3, 2, 2, 1, 8};
-  if (knob < 0 || knob > 4 || value < 0 || value > hi[knob]) return DM_E_INVALID;
+  static const int hi[6] = {3, 2, 2, 1, 8, 2};
+  if (knob < 0 || knob > 5 || value < 0 || value > hi[knob]) return DM_E_INVALID;
   if (knob == 4 && value != 0 && value != 7 && value != 8) return DM_E_INVALID;
   g_tuning[knob].store(value);
   return DM_OK;

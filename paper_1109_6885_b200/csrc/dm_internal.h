@@ -70,10 +70,30 @@ inline bool xc_wanted(const dm_column_in* in) {
 }
 // Step 1(a) dedup front end (NEXT1): knob 2 = 0 auto (16-byte keys with
 // N_D >= 2^16: 16 radix passes make repeats expensive), 1 off, 2 on.
+// Step 1(a) sort (knob 5): 0 auto = the bucket path (below) for 2^11 <= N_D <=
+// 2^23, else the LSD passes; 1 LSD only; 2 bucket path for any N_D >= 1.
+constexpr uint64_t kBkMinN = 1ull << 11, kBkMaxN = 1ull << 23;
+constexpr uint32_t kBkMaxBucket = 256;  // a larger bucket sends the merge to the LSD passes
+constexpr int kBkScanItems = 16;        // counts per thread in k_bk_scan (tile = 4096 buckets)
+inline bool bucket_wanted(const dm_column_in* in) {
+  const int k = tuning(5);
+  if (in->n_delta == 0 || k == 1) return false;
+  return k == 2 || (in->n_delta >= kBkMinN && in->n_delta <= kBkMaxN);
+}
+// log2 of the bucket count: about four keys per bucket
+inline uint32_t bucket_bits(uint64_t n) {
+  uint32_t b = 0;
+  while ((1ull << b) < n) ++b;
+  return b < 14 ? 12u : b > 26 ? 24u : b - 2;  // >= one k_bk_scan tile
+}
 inline bool dedup_wanted(const dm_column_in* in) {
   const int k = tuning(2);
   if (in->n_delta == 0 || k == 1) return false;
-  return k == 2 || (in->key == DM_KEY_B16 && in->n_delta >= (1u << 16));
+  // 16-byte keys with many tuples (16 radix passes), or -- for the bucket path,
+  // whose buckets must stay small -- a delta that must repeat values heavily
+  // (at most |U_M| of its distinct values can be old ones)
+  return k == 2 || (in->key == DM_KEY_B16 && in->n_delta >= (1u << 16)) ||
+         (bucket_wanted(in) && in->dict_len * 4 < in->n_delta);
 }
 // Block shift: 256-code blocks when N_D / |U_M| promises <= 6 entries per block
 // (and always for the shared-memory variant, knob 2), else 128-code blocks.
@@ -99,6 +119,13 @@ struct SortPlan {
   int32_t n_active;
   int32_t pad[2];
   uint32_t digit_base[16][256];
+};
+// Bucket path state (zeroed per call): OR of (key ^ key[0]) over all keys, the
+// grid-done counter, the overflow flag (a bucket > kBkMaxBucket keys: the LSD passes
+// run instead) and the digit shift.
+struct BucketState {
+  unsigned long long diff_hi, diff_lo;
+  uint32_t done, overflow, shift, pad;
 };
 
 // Workspace layout (byte offsets).  [0, zero_bytes) is memset to 0 per call.
@@ -130,12 +157,18 @@ struct WsLayout {
   size_t dd_rank;        // dedup: u32[n_delta] rank of each distinct id
   uint64_t dd_cap;       // dedup: table slots (power of two >= 2 n_delta), 0 = no dedup
   bool dedup;
+  bool bucket;           // Step 1(a) bucket path
+  uint32_t bk_bits;      // log2 bucket count
+  size_t bk_state;       // BucketState (zeroed region)
+  size_t bk_status;      // u64[scan tiles + 1] look-back (zeroed region)
+  size_t bk_off;         // u32[B + 1]: counts, then exclusive offsets
+  size_t bk_cur;         // u32[B]: scatter cursors
   size_t total;
   uint64_t ntiles_sort, ntiles_unique, ntiles_merge;
   int npass;
 };
 
-enum { CNT_SORT = 0, CNT_UNIQUE = 16, CNT_MERGE = 17, CNT_HIST = 18, CNT_DEDUP = 20 /* u64, 2 slots */ };
+enum { CNT_SORT = 0, CNT_UNIQUE = 16, CNT_MERGE = 17, CNT_HIST = 18, CNT_DEDUP = 20 /* u64, 2 slots */, CNT_BKSCAN = 22 };
 
 WsLayout ws_layout(const dm_column_in* in);
 inline size_t key_bytes(int key) { return key == DM_KEY_U64 ? 8 : key == DM_KEY_U32 ? 4 : 16; }
