@@ -412,9 +412,42 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge(const void* __restrict_
       if (k < na + nb) sk[1 + k] = v[r];
     }
   }
+  const bool small_b = nb <= na;
+  if constexpr (MODE == 1) {
+    // count pass: only the tile's duplicate count (each U_D value matches at
+    // most one U_M value) -- no slot arrays, so the launch takes the key
+    // staging only and more tiles are resident per SM
+    __syncthreads();
+    uint32_t c = 0;
+    if (small_b) {
+      for (uint32_t j = threadIdx.x; j < nb; j += NT) {
+        const K v = B_(j);
+        uint32_t lo = 0, hi = na;
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (KT::le(A_(mid), v)) lo = mid + 1; else hi = mid;
+        }
+        c += (lo > 0 ? KT::eq(A_(lo - 1), v) : (has_prev && KT::eq(sk[0], v))) ? 1u : 0u;
+      }
+    } else {
+      for (uint32_t a = threadIdx.x; a < na; a += NT) {
+        const K v = A_(a);
+        uint32_t lo = 0, hi = nb;
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (KT::lt(B_(mid), v)) lo = mid + 1; else hi = mid;
+        }
+        c += (lo < nb && KT::eq(B_(lo), v)) ? 1u : 0u;
+      }
+      if (threadIdx.x == 0 && has_prev && nb > 0 && KT::eq(B_(0), sk[0])) ++c;
+    }
+    uint32_t tot;
+    block_exclusive_scan<NT>(c, s_warp, tot);
+    if (threadIdx.x == 0) cnt[tile] = tot;
+    return;
+  }
   for (uint32_t k = threadIdx.x; k <= nb; k += NT) se[k] = 0;
   __syncthreads();
-  const bool small_b = nb <= na;
   if (small_b) {
     for (uint32_t j = threadIdx.x; j < nb; j += NT) {
       const K v = B_(j);
@@ -460,10 +493,6 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge(const void* __restrict_
   }
   __syncthreads();
   const uint32_t dups = se[nb];
-  if constexpr (MODE == 1) {
-    if (threadIdx.x == 0) cnt[tile] = dups;
-    return;
-  }
   if (MODE == 0 && warp == 0) {
     const uint64_t e = lookback_exclusive(status, tile, dups);
     if (lane == 0) s_D0 = e;
@@ -672,19 +701,19 @@ cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, const void*
     launch_k(k_partition<KT>, (unsigned)((nt + 1 + 7) / 8), 256, 0, st, in->main_dict, in->dict_len, udict, hdr, nt + 1,
                                                                      part);
     const size_t smem = sizeof(K) * (kMergeTile + 1) + sizeof(uint32_t) * (3 * kMergeTile + 1);
-    auto go = [&](auto kern) {
+    auto go = [&](auto kern, size_t sm) {
       ensure_smem((const void*)kern, true);
-      launch_k(kern, (unsigned)nt, kMergeThreads, smem, st, in->main_dict, in->dict_len, udict, part, nt, status, counter,
+      launch_k(kern, (unsigned)nt, kMergeThreads, sm, st, in->main_dict, in->dict_len, udict, part, nt, status, counter,
                                                       cnt, excl, U, xm, xd, hdr, rblk, offs, xs);
     };
     if (variant == 2) {
-      go(k_merge<KT, 0>);
+      go(k_merge<KT, 0>, smem);
       note_launch(2);
     } else {
-      go(k_merge<KT, 1>);
+      go(k_merge<KT, 1>, sizeof(K) * (kMergeTile + 1));  // count pass: key staging only
       launch_k(k_scan_counts, (unsigned)((nt + 2047) / 2048), 256, 0, st, cnt, nt, excl, status, counter, in->dict_len,
                                                                     hdr);
-      go(k_merge<KT, 2>);
+      go(k_merge<KT, 2>, smem);
       note_launch(4);
     }
   } else {
