@@ -584,43 +584,7 @@ __device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// Global table: insert value k, return its distinct id.
 // Slot tag: 0 empty; (h & ~3) | 1 claimed; | 3 ready (id and key published).
-template <class KT>
-__device__ __forceinline__ uint32_t dd_global_insert(typename KT::K k, uint32_t* __restrict__ tags,
-                                                     uint32_t* __restrict__ ids, uint64_t mask,
-                                                     void* __restrict__ dkeys, unsigned long long* n_dist) {
-  const uint64_t h = dd_hash(k);
-  uint64_t slot = (h >> 32) & mask;
-  const uint32_t tg = ((uint32_t)h & ~3u) | 1u;
-  for (;;) {
-    uint32_t t = ld_acquire_u32(tags + slot);
-    if (t == 0) {
-      t = atomicCAS(tags + slot, 0u, tg);
-      if (t == 0) {  // claimed: publish the value, then the id, then "ready"
-        const uint32_t id = (uint32_t)atomicAdd(n_dist, 1ull);
-        KT::store(dkeys, id, k);
-        ids[slot] = id;
-        __threadfence();
-        st_release_u32(tags + slot, tg | 2u);
-        return id;
-      }
-    }
-    if ((t | 2u) == (tg | 2u)) {  // same hash tag: wait until ready, compare the value
-      while (!(t & 2u)) t = ld_acquire_u32(tags + slot);
-      const uint32_t cid = __ldcg(ids + slot);
-      if (KT::eq(KT::load_cg(dkeys, cid), k)) return cid;
-    }
-    slot = (slot + 1) & mask;
-  }
-}
-
-// Two levels: a block first collapses the repeats inside its tile of
-// kDdTile tuples in a shared-memory table (slot owner = the first tuple of the
-// value, compared against the input itself, so nothing needs publishing), and
-// only the owners go to the global table.  A Zipf-reused delta (cfg3) sends
-// most tuples of a hot value to one global slot -- one L2 slice serialising
-// them -- without this.
 template <class KT>
 __global__ void __launch_bounds__(256) k_dedup_insert(const void* __restrict__ D, uint64_t n,
                                                       uint32_t* __restrict__ tags, uint32_t* __restrict__ ids,
@@ -628,49 +592,36 @@ __global__ void __launch_bounds__(256) k_dedup_insert(const void* __restrict__ D
                                                       uint32_t* __restrict__ tid, unsigned long long* n_dist) {
   pdl_prologue();
   using K = typename KT::K;
-  constexpr uint32_t IT = kDdTile / 256, SLOTS = 2 * kDdTile, EMPTY = 0xffffffffu;
-  __shared__ uint32_t s_own[SLOTS];  // local index of the slot's first tuple
-  __shared__ uint32_t s_gid[SLOTS];  // its global distinct id
-  for (uint64_t base = (uint64_t)blockIdx.x * kDdTile; base < n; base += (uint64_t)gridDim.x * kDdTile) {
-    for (uint32_t i = threadIdx.x; i < SLOTS; i += 256) s_own[i] = EMPTY;
-    __syncthreads();
-    K k[IT];
-    uint32_t slot[IT];
-    bool owner[IT];
-#pragma unroll
-    for (uint32_t r = 0; r < IT; ++r) {
-      const uint32_t li = threadIdx.x + r * 256;
-      const uint64_t gi = base + li;
-      owner[r] = false;
-      slot[r] = 0;
-      if (gi >= n) continue;
-      k[r] = KT::load(D, gi);
-      uint32_t sl = (uint32_t)(dd_hash(k[r]) & (SLOTS - 1));
-      for (;;) {
-        uint32_t o = s_own[sl];
-        if (o == EMPTY) {
-          o = atomicCAS(&s_own[sl], EMPTY, li);
-          if (o == EMPTY) {
-            owner[r] = true;
-            break;
-          }
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const K k = KT::load(D, i);
+    const uint64_t h = dd_hash(k);
+    uint64_t slot = (h >> 32) & mask;
+    const uint32_t tg = ((uint32_t)h & ~3u) | 1u;
+    uint32_t id = 0;
+    for (;;) {
+      uint32_t t = ld_acquire_u32(tags + slot);
+      if (t == 0) {
+        t = atomicCAS(tags + slot, 0u, tg);
+        if (t == 0) {  // claimed: publish the value, then the id, then "ready"
+          id = (uint32_t)atomicAdd(n_dist, 1ull);
+          KT::store(dkeys, id, k);
+          ids[slot] = id;
+          __threadfence();
+          st_release_u32(tags + slot, tg | 2u);
+          break;
         }
-        if (KT::eq(KT::load(D, base + o), k[r])) break;
-        sl = (sl + 1) & (SLOTS - 1);
       }
-      slot[r] = sl;
+      if ((t | 2u) == (tg | 2u)) {  // same hash tag: wait until ready, compare the value
+        while (!(t & 2u)) t = ld_acquire_u32(tags + slot);
+        const uint32_t cid = __ldcg(ids + slot);
+        if (KT::eq(KT::load_cg(dkeys, cid), k)) {
+          id = cid;
+          break;
+        }
+      }
+      slot = (slot + 1) & mask;
     }
-    __syncthreads();
-#pragma unroll
-    for (uint32_t r = 0; r < IT; ++r)
-      if (owner[r]) s_gid[slot[r]] = dd_global_insert<KT>(k[r], tags, ids, mask, dkeys, n_dist);
-    __syncthreads();
-#pragma unroll
-    for (uint32_t r = 0; r < IT; ++r) {
-      const uint64_t gi = base + threadIdx.x + r * 256;
-      if (gi < n) tid[gi] = s_gid[slot[r]];
-    }
-    __syncthreads();
+    tid[i] = id;
   }
 }
 
@@ -715,7 +666,7 @@ cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, void* udict
   if (L.dedup) {
     unsigned long long* n_dist = reinterpret_cast<unsigned long long*>(counters + CNT_DEDUP);
     const int sms = device_sms();
-    launch_k(k_dedup_insert<KT>, (unsigned)std::min<uint64_t>((n + kDdTile - 1) / kDdTile, (uint64_t)sms * 4), 256, 0, st, 
+    launch_k(k_dedup_insert<KT>, (unsigned)std::min<uint64_t>((n + 255) / 256, (uint64_t)sms * 8), 256, 0, st, 
         in->delta, n, reinterpret_cast<uint32_t*>(ws + L.dd_tags), reinterpret_cast<uint32_t*>(ws + L.dd_ids),
         L.dd_cap - 1, ws + L.dd_keys, reinterpret_cast<uint32_t*>(ws + L.dd_tid), n_dist);
     note_launch();

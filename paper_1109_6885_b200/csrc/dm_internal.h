@@ -74,7 +74,6 @@ inline bool xc_wanted(const dm_column_in* in) {
 // 2^23, else the LSD passes; 1 LSD only; 2 bucket path for any N_D >= 1.
 constexpr uint64_t kBkMinN = 1ull << 11, kBkMaxN = 1ull << 23;
 constexpr uint32_t kBkMaxBucket = 256;  // a larger bucket sends the merge to the LSD passes
-constexpr uint32_t kDdTile = 2048;      // tuples per block-local dedup table (k_dedup_insert)
 constexpr int kBkScanItems = 16;        // counts per thread in k_bk_scan (tile = 4096 buckets)
 inline bool bucket_wanted(const dm_column_in* in) {
   const int k = tuning(5);
