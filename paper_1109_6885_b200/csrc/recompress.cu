@@ -277,8 +277,10 @@ __global__ void __launch_bounds__(rec_threads<XMODE>(), XMODE == XM_XC_SMEM ? 1 
   const uint32_t umask = b == 32 ? 0xffffffffu : ((1u << b) - 1);
   const uint32_t pr0 = (32 * lane) / nb, pop = 32 * lane - pr0 * nb;
   uint32_t* out32 = reinterpret_cast<uint32_t*>(Mout);
-  const uint32_t dict_len32 = (uint32_t)dict_len;  // < 2^32 (validated by the ABI)
-  bool bad = false;
+  // codes >= |U_M| are clamped (reads stay in the table) and reported once at
+  // the end through the running maximum: two ALU ops per row
+  const uint32_t dict_last = (uint32_t)dict_len - 1u;  // |U_M| >= 1 when N_M > 0 (validated by the ABI)
+  uint32_t code_max = 0;
 
   for (uint64_t k = 0;; ++k) {
     const uint64_t c = blockIdx.x + k * gridDim.x;
@@ -289,10 +291,8 @@ __global__ void __launch_bounds__(rec_threads<XMODE>(), XMODE == XM_XC_SMEM ? 1 
     const uint64_t row_base = c * R;
     uint32_t v[U];
     auto translate = [&](uint32_t code) -> uint32_t {
-      if (code >= dict_len32) {
-        bad = true;
-        code = 0;
-      }
+      code_max = umax32(code_max, code);
+      code = umin32(code, dict_last);
       if constexpr (XMODE == XM_RAW_SMEM)
         return sx[code];
       else if constexpr (XMODE == XM_XC_SMEM)
@@ -327,14 +327,25 @@ __global__ void __launch_bounds__(rec_threads<XMODE>(), XMODE == XM_XC_SMEM ? 1 
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);  // stage s fully read by this warp
+    // output: group g of chunk c is words [(c G + g) b', +b'); lane k < b' writes word k
+    uint32_t* outc = out32 + (c * G + warp) * (uint64_t)nb + lane;
+    if ((c + 1) * G * (uint64_t)nb <= nw32) {  // the whole chunk is inside M' (all but the last)
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int g = warp + CW * u;
-      const uint32_t word = warp_pack<NB>(v[u], nb, pr0, pop);
-      const uint64_t ow = (c * G + g) * nb + lane;
-      if (lane < nb && ow < nw32) __stcs(out32 + ow, word);
+      for (int u = 0; u < U; ++u) {
+        const uint32_t word = warp_pack<NB>(v[u], nb, pr0, pop);
+        if (lane < nb) __stcs(outc + (size_t)CW * u * nb, word);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int g = warp + CW * u;
+        const uint32_t word = warp_pack<NB>(v[u], nb, pr0, pop);
+        const uint64_t ow = (c * G + g) * nb + lane;
+        if (lane < nb && ow < nw32) __stcs(out32 + ow, word);
+      }
     }
   }
+  const bool bad = n_main > 0 && code_max > dict_last;
   if (__any_sync(FULL, bad) && lane == 0) atomicMin(&hdr->status, (int)DM_E_CODE_RANGE);
 }
 
@@ -525,7 +536,10 @@ cudaError_t launch_recompress(const dm_column_in* in, const dm_column_out* out, 
   const uint64_t lo_len = std::max<uint64_t>(in->dict_len, in->n_delta ? 1 : 0);
   const uint32_t nb_lo = host_width(lo_len), nb_hi = host_width(in->dict_len + in->n_delta);
   if (nb_hi > 32) return cudaErrorInvalidValue;  // caller checks DM_E_TOO_WIDE first
-  if (nb_hi - nb_lo <= 2) {
+  // b' is only known on the device: launch every width-specialised kernel |U'|'s
+  // bounds allow (the others exit at once, ~2 us each) while that is cheaper
+  // than the runtime-width kernel (its shuffle-pack loop and spills)
+  if (nb_hi - nb_lo <= 3) {
     for (uint32_t nb = nb_lo; nb <= nb_hi; ++nb) {
       cudaError_t e = table[nb](in, out, xm, xd, rank, hdr, st, 0, xc_rec, xc_offs, xc_shift);
       if (e != cudaSuccess) return e;
