@@ -534,36 +534,49 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge(const void* __restrict_
             (unsigned long long)D0, (unsigned long long)j0, dups, nb);
   const unsigned lt = lanemask_lt();
   bool unsorted = false;
+  // 32-bit per-element index math from tile-base pointers (U', X_M) and
+  // per-tile constants (the write pass is issue-bound); sk[g] is the element
+  // before A_(g) (sk[0] = A[i0 - 1]), so the sortedness check needs no select
+  void* const Ub = static_cast<char*>(U) + base * (uint64_t)KT::kBytes;  // U' from the tile's first slot
+  uint32_t* const XMt = XM + i0;
+  const uint32_t bmask = (1u << xs) - 1, i0lo = (uint32_t)i0, ub32 = (uint32_t)base;
+  const uint32_t dU = (uint32_t)(base - i0);  // U' index - U_M index of the tile's first A slot
+  const uint32_t glast = nA > i0 && nA <= i1 ? (uint32_t)(nA - 1 - i0) : 0xffffffffu;
+  const uint32_t hp = has_prev ? 1u : 0u;
+  auto sample = [&](uint32_t a, uint32_t r32) {  // XC block samples R(g) = X_M[256 g] - 256 g
+    if (((i0lo + a) & bmask) == 0) rblk[(i0 + a) >> xs] = r32;
+    if (a == glast) rblk[(nA + bmask) >> xs] = r32;
+  };
   // fill: slot p not taken by S holds the (p - #S slots before p)-th G element
+  if (small_b) {
 #pragma unroll
-  for (int r = 0; r < IT; ++r) {
-    const uint32_t p = r * NT + threadIdx.x;
-    if (p >= nU) break;
-    const uint32_t bits = s_bm[p >> 5];
-    if ((bits >> lane) & 1u) continue;
-    const uint32_t before = s_wpre[p >> 5] + __popc(bits & lt);  // S slots before p
-    const uint32_t g = p - before;
-    const uint64_t u = base + p;
-    DM_ASSERT(small_b ? g < na : g < nb - dups, "fill tile %llu p %u g %u na %u nb %u dups %u small %d",
-              (unsigned long long)tile, p, g, na, nb, dups, (int)small_b);
-    if (small_b) {
-      const K v = A_(g);
-      const uint64_t i = i0 + g;
-      KT::store(U, u, v);
-      XM[i] = (uint32_t)u;
-      if (rblk) {
-        if ((i & ((1u << xs) - 1)) == 0) rblk[i >> xs] = (uint32_t)(u - i);
-        if (i == nA - 1) rblk[(nA + (1u << xs) - 1) >> xs] = (uint32_t)(u - i);
-      }
-      if ((g > 0 || has_prev) && !KT::lt(g > 0 ? A_(g - 1) : sk[0], v)) unsorted = true;
-    } else {
+    for (int r = 0; r < IT; ++r) {
+      const uint32_t p = r * NT + threadIdx.x;
+      if (p >= nU) break;
+      const uint32_t bits = s_bm[p >> 5];
+      if ((bits >> lane) & 1u) continue;
+      const uint32_t g = p - (s_wpre[p >> 5] + __popc(bits & lt));  // minus the S slots before p
+      DM_ASSERT(g < na, "fill tile %llu p %u g %u na %u", (unsigned long long)tile, p, g, na);
+      const K v = sk[1 + g];
+      KT::store(Ub, p, v);
+      XMt[g] = ub32 + p;
+      if (rblk) sample(g, dU + p - g);
+      if ((g | hp) && !KT::lt(sk[g], v)) unsorted = true;
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < IT; ++r) {
+      const uint32_t p = r * NT + threadIdx.x;
+      if (p >= nU) break;
+      const uint32_t bits = s_bm[p >> 5];
+      if ((bits >> lane) & 1u) continue;
+      const uint32_t before = s_wpre[p >> 5] + __popc(bits & lt);  // S slots before p
+      const uint32_t g = p - before;
+      DM_ASSERT(g < nb - dups, "fill tile %llu p %u g %u nb %u dups %u", (unsigned long long)tile, p, g, nb, dups);
       const uint32_t j = snd[g];
-      KT::store(U, u, B_(j));
-      XD[j0 + j] = (uint32_t)u;
-      if (offs) {
-        const uint64_t P = i0 + before;  // U_M entries below this new value
-        offs[u - P] = (uint8_t)((P - 1) & ((1u << xs) - 1));
-      }
+      KT::store(Ub, p, B_(j));
+      XD[j0 + j] = ub32 + p;
+      if (offs) offs[(uint64_t)(dU + p - before)] = (uint8_t)((i0lo + before - 1) & bmask);  // P = i0 + before
     }
   }
   // the small side
@@ -586,16 +599,12 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge(const void* __restrict_
   } else {
     for (uint32_t a = threadIdx.x; a < na; a += NT) {
       const uint32_t l = sq[a], slot = a + l - se[l];
-      const uint64_t u = base + slot, i = i0 + a;
-      const K v = A_(a);
-      KT::store(U, u, v);
-      XM[i] = (uint32_t)u;
-      if (l < nb && se[l + 1] != se[l] && KT::eq(B_(l), v)) XD[j0 + l] = (uint32_t)u;
-      if (rblk) {
-        if ((i & ((1u << xs) - 1)) == 0) rblk[i >> xs] = (uint32_t)(u - i);
-        if (i == nA - 1) rblk[(nA + (1u << xs) - 1) >> xs] = (uint32_t)(u - i);
-      }
-      if ((a > 0 || has_prev) && !KT::lt(a > 0 ? A_(a - 1) : sk[0], v)) unsorted = true;
+      const K v = sk[1 + a];
+      KT::store(Ub, slot, v);
+      XMt[a] = ub32 + slot;
+      if (l < nb && se[l + 1] != se[l] && KT::eq(B_(l), v)) XD[j0 + l] = ub32 + slot;
+      if (rblk) sample(a, dU + slot - a);
+      if ((a | hp) && !KT::lt(sk[a], v)) unsorted = true;
     }
     if (threadIdx.x == 0 && has_prev && nb > 0 && KT::eq(B_(0), sk[0])) XD[j0] = (uint32_t)(base - 1);
   }
