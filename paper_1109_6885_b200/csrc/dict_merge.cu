@@ -538,7 +538,7 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge(const void* __restrict_
   // per-tile constants (the write pass is issue-bound); sk[g] is the element
   // before A_(g) (sk[0] = A[i0 - 1]), so the sortedness check needs no select
   void* const Ub = static_cast<char*>(U) + base * (uint64_t)KT::kBytes;  // U' from the tile's first slot
-  uint32_t* const XMt = XM + i0;
+  uint32_t* const XMt = XM + i0;  // XM == nullptr: X_M is not materialised (see launch_dictionary_merge)
   const uint32_t bmask = (1u << xs) - 1, i0lo = (uint32_t)i0, ub32 = (uint32_t)base;
   const uint32_t dU = (uint32_t)(base - i0);  // U' index - U_M index of the tile's first A slot
   const uint32_t glast = nA > i0 && nA <= i1 ? (uint32_t)(nA - 1 - i0) : 0xffffffffu;
@@ -559,7 +559,7 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge(const void* __restrict_
       DM_ASSERT(g < na, "fill tile %llu p %u g %u na %u", (unsigned long long)tile, p, g, na);
       const K v = sk[1 + g];
       KT::store(Ub, p, v);
-      XMt[g] = ub32 + p;
+      if (XM) XMt[g] = ub32 + p;
       if (rblk) sample(g, dU + p - g);
       if ((g | hp) && !KT::lt(sk[g], v)) unsorted = true;
     }
@@ -601,7 +601,7 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge(const void* __restrict_
       const uint32_t l = sq[a], slot = a + l - se[l];
       const K v = sk[1 + a];
       KT::store(Ub, slot, v);
-      XMt[a] = ub32 + slot;
+      if (XM) XMt[a] = ub32 + slot;
       if (l < nb && se[l + 1] != se[l] && KT::eq(B_(l), v)) XD[j0 + l] = ub32 + slot;
       if (rblk) sample(a, dU + slot - a);
       if ((a | hp) && !KT::lt(sk[a], v)) unsorted = true;
@@ -639,6 +639,36 @@ __global__ void __launch_bounds__(256) k_xc_records(const uint32_t* __restrict__
     prev = c;
   }
   rec[sb] = make_uint2(R0 | (flag << 31), cum);
+}
+
+// X_M for the flagged superblocks only, when the merge does not materialise X_M
+// (nobody asked for it and Step 2(b) reads XC from L2, which falls back to
+// X_M on flagged superblocks alone): X_M[c] = c + R(g) + #{entries of block g
+// below c mod 2^xs} with g = c's block -- the closed form XC encodes,
+// the list binary-searched (sorted: new values in order).  One warp per superblock.
+__global__ void __launch_bounds__(256) k_xm_flagged(const uint2* __restrict__ rec, uint64_t nsb, uint32_t xs,
+                                                    uint64_t dict_len, const uint32_t* __restrict__ rblk,
+                                                    uint64_t nblk, const uint8_t* __restrict__ offs,
+                                                    uint32_t* __restrict__ xm) {
+  pdl_prologue();
+  const unsigned lane = lane_id();
+  const uint64_t warp0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint32_t bmask = (1u << xs) - 1;
+  for (uint64_t sb = warp0; sb < nsb; sb += nwarps) {
+    if (!(rec[sb].x >> 31)) continue;
+    const uint64_t c0 = sb << (xs + 2), c1 = umin64(c0 + (4ull << xs), dict_len);
+    for (uint64_t c = c0 + lane; c < c1; c += 32) {
+      const uint64_t g = c >> xs;
+      const uint32_t lo = rblk[g], hi = rblk[umin64(g + 1, nblk)], o = (uint32_t)c & bmask;
+      uint32_t a = lo, b = hi;  // first entry >= o
+      while (a < b) {
+        const uint32_t m = (a + b) >> 1;
+        if (offs[m] < o) a = m + 1; else b = m;
+      }
+      xm[c] = (uint32_t)c + a;  // c + R(g) + (a - lo), R(g) = lo
+    }
+  }
 }
 
 // XC exception list (row-sharded Step 2): one warp per superblock; a flagged
@@ -688,7 +718,7 @@ __global__ void k_empty_header(dm_header* hdr) {
 
 template <class KT>
 cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, const void* udict, void* U, uint32_t* xm,
-                uint32_t* xd, dm_header* hdr, cudaStream_t st, bool force_xc) {
+                uint32_t* xd, dm_header* hdr, cudaStream_t st, bool force_xc, bool xm_requested) {
   using K = typename KT::K;
   if (in->dict_len + in->n_delta == 0) {
     launch_k(k_empty_header, 1, 1, 0, st, hdr);
@@ -706,6 +736,13 @@ cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, const void*
   uint64_t* status = reinterpret_cast<uint64_t*>(ws + L.status_merge);
   uint32_t* counter = reinterpret_cast<uint32_t*>(ws + L.counters) + CNT_MERGE;
   const int variant = tuning(1);
+  // X_M need not be materialised when nobody asked for it and Step 2(b) will
+  // read XC from L2 (that kernel falls back to X_M on flagged superblocks only,
+  // filled by k_xm_flagged): cfg5 skips 4.3 GB of writes
+  const int xknob = tuning(0);
+  const bool skip_xm = xc && !force_xc && !xm_requested && (variant == 0 || variant == 2) &&
+                       (xknob == 2 || xknob == 3 || (xknob == 0 && in->dict_len * 4 > kXcGlobalMinBytes));
+  uint32_t* xm_w = skip_xm ? nullptr : xm;
   if (variant == 0 || variant == 2) {  // lean tiles: two passes (default) or single pass
     launch_k(k_partition<KT>, (unsigned)((nt + 1 + 7) / 8), 256, 0, st, in->main_dict, in->dict_len, udict, hdr, nt + 1,
                                                                      part);
@@ -713,7 +750,7 @@ cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, const void*
     auto go = [&](auto kern, size_t sm) {
       ensure_smem((const void*)kern, true);
       launch_k(kern, (unsigned)nt, kMergeThreads, sm, st, in->main_dict, in->dict_len, udict, part, nt, status, counter,
-                                                      cnt, excl, U, xm, xd, hdr, rblk, offs, xs);
+                                                      cnt, excl, U, xm_w, xd, hdr, rblk, offs, xs);
     };
     if (variant == 2) {
       go(k_merge<KT, 0>, smem);
@@ -748,6 +785,12 @@ cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, const void*
     launch_k(k_xc_records, (unsigned)((nsb + 255) / 256), 256, 0, st, rblk, xc_nblk(in->dict_len, xs), nsb,
                                                                 reinterpret_cast<uint2*>(ws + L.xc_rec));
     note_launch();
+    if (skip_xm) {
+      const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nsb + 7) / 8, (uint64_t)device_sms() * 8));
+      launch_k(k_xm_flagged, g, 256, 0, st, reinterpret_cast<const uint2*>(ws + L.xc_rec), nsb, xs, in->dict_len,
+               (const uint32_t*)rblk, xc_nblk(in->dict_len, xs), (const uint8_t*)offs, xm);
+      note_launch();
+    }
   }
   return cudaGetLastError();
 }
@@ -769,9 +812,9 @@ cudaError_t launch_dictionary_merge(const dm_column_in* in, const dm_column_out*
                                     const void* udict, uint32_t* xm, uint32_t* xd, dm_header* hdr, cudaStream_t st,
                                     bool force_xc) {
   switch (in->key) {
-    case DM_KEY_U64: return run<KeyU64>(in, ws, L, udict, out->merged_dict, xm, xd, hdr, st, force_xc);
-    case DM_KEY_U32: return run<KeyU32>(in, ws, L, udict, out->merged_dict, xm, xd, hdr, st, force_xc);
-    default: return run<KeyB16>(in, ws, L, udict, out->merged_dict, xm, xd, hdr, st, force_xc);
+    case DM_KEY_U64: return run<KeyU64>(in, ws, L, udict, out->merged_dict, xm, xd, hdr, st, force_xc, out->x_main != nullptr);
+    case DM_KEY_U32: return run<KeyU32>(in, ws, L, udict, out->merged_dict, xm, xd, hdr, st, force_xc, out->x_main != nullptr);
+    default: return run<KeyB16>(in, ws, L, udict, out->merged_dict, xm, xd, hdr, st, force_xc, out->x_main != nullptr);
   }
 }
 

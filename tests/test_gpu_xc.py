@@ -3,8 +3,9 @@
 XC replaces the Step 2(b) gather X_M[c] by c + #{new dictionary values inserted
 at or before main position c} (the closed form of X_M; DESIGN.md
 §7).  It must never change a result, so every case runs under each placement
-knob (auto / plain X_M / XC with shared-memory preference / XC from L2) and is
-compared element by element with the oracle.  The cases aim at the format's
+knob (auto / plain X_M / XC with shared-memory preference / XC from L2), with
+and without the translation tables requested, and is compared element by
+element with the oracle.  The cases aim at the format's
 edges: insertions before the first and after the last main entry, at 256- and
 1024-code boundaries, blocks with exactly kXcMaxBlock (32) and 33 insertions
 (flagged), list lengths 0..12 against the two-word read window, dictionary
@@ -63,12 +64,20 @@ def _column(n_dict, n_main, insert_at, n_reuse, seed, key="u64"):
 
 
 def _run_all_knobs(col):
+    """Every placement knob, with X_M / X_D returned (compared too) and without:
+    then a merge that reads XC from L2 does not materialise X_M at all and fills
+    only the flagged superblocks' entries (k_xm_flagged), so M' checks them."""
     import paper_1109_6885_b200 as dm
+    from tests.parity import to_device
     ref = None
     for k in KNOBS:
         dm.set_tuning(0, k)
         M, r = run_gpu(col)
         ref = compare(col, M, r, ref=ref)
+        UM, M, D = to_device(col)
+        r = dm.merge_column(UM, M, col.n_main, col.main_bits, D)
+        torch.cuda.synchronize()
+        compare(col, M, r, ref=ref, check_tables=False)
 
 
 def _spread(n_dict, n_new, seed):
