@@ -37,14 +37,16 @@ namespace {
 
 __device__ __forceinline__ uint64_t dwords(uint64_t n, uint32_t bits) { return (n * bits + 63) >> 6; }
 
+// NB > 0: b' = NB at compile time.  NB <= 0: b' at run time, with at most -NB
+// codes per output word (NB = 0: any width, up to 32).
 template <int NB>
 __device__ __forceinline__ uint32_t warp_pack(uint32_t v, uint32_t nb, uint32_t r0, uint32_t op) {
-  constexpr int TMAX = NB ? (2 * NB + 30) / NB : 32;
-  const int tmax = NB ? TMAX : (int)((2 * nb + 30) / nb);
+  constexpr int TMAX = NB > 0 ? (2 * NB + 30) / NB : NB < 0 ? -NB : 32;
+  const int tmax = NB > 0 ? TMAX : (int)((2 * nb + 30) / nb);
   uint32_t word = 0;
 #pragma unroll
   for (int t = 0; t < TMAX; ++t) {
-    if (!NB && t >= tmax) break;
+    if (NB <= 0 && t >= tmax) break;
     const uint32_t c = __shfl_sync(FULL, v, (r0 + t) & 31);
     word |= (t == 0) ? shr32(c, op) : shl32(c, t * nb - op);
   }
@@ -197,8 +199,8 @@ __global__ void __launch_bounds__(rec_threads<XMODE>(), XMODE == XM_XC_SMEM ? 1 
   constexpr bool XS = XMODE == XM_RAW_SMEM;
   static_assert(G % CW == 0, "groups must split evenly over consumer warps");
   const uint32_t hb = fixed_bits ? fixed_bits : hdr->merged_bits;
-  if (NB && hb != (uint32_t)NB) return;
-  const uint32_t nb = NB ? (uint32_t)NB : hb;
+  if (NB > 0 && hb != (uint32_t)NB) return;
+  const uint32_t nb = NB > 0 ? (uint32_t)NB : hb;
   const uint64_t nsb = (dict_len + (4ull << xs) - 1) >> (xs + 2);
   uint64_t xc_offs_bytes = 0;
   if (xc_budget) {
@@ -482,6 +484,12 @@ cudaError_t launch_nb(const dm_column_in* in, const dm_column_out* out, const ui
     return cudaGetLastError();
   }
   const int knob = tuning(0);
+  if constexpr (NB < 0) {  // bounded runtime-width kernels exist for the plain-X_M modes only
+    if (xrec && knob != 1)
+      return launch_nb<0>(in, out, xm, xd, rank, hdr, st, fixed_bits, xrec, xoffs, xs);
+    go(k_recompress<NB, XM_RAW_GLOBAL>, ring, 0);
+    return cudaGetLastError();
+  } else {
   if (!xrec || knob == 1) {
     go(k_recompress<NB, XM_RAW_GLOBAL>, ring, 0);
     return cudaGetLastError();
@@ -508,6 +516,7 @@ cudaError_t launch_nb(const dm_column_in* in, const dm_column_out* out, const ui
   else
     go(k_recompress<NB, XM_RAW_GLOBAL>, ring, budget);
   return cudaGetLastError();
+  }
 }
 
 using XcKernel = void (*)(const uint64_t*, uint64_t, uint32_t, uint64_t, const uint32_t*, const uint32_t*,
@@ -546,6 +555,16 @@ cudaError_t launch_recompress(const dm_column_in* in, const dm_column_out* out, 
     }
     return cudaSuccess;
   }
+  // wider ranges: a runtime-width kernel whose pack loop is bounded by the
+  // narrowest candidate (codes per output word = 2 + 30 / b', non-increasing in
+  // b'), so small-dictionary columns with large deltas keep a short, unspilled loop
+  static const LaunchFn classes[] = {&launch_nb<-2>, &launch_nb<-3>, &launch_nb<-4>, &launch_nb<-5>,
+                                     &launch_nb<-6>, &launch_nb<-7>, &launch_nb<-8>, &launch_nb<-9>,
+                                     &launch_nb<-12>, &launch_nb<-17>};
+  static const int bound[] = {2, 3, 4, 5, 6, 7, 8, 9, 12, 17};
+  const int tm = (int)((2 * nb_lo + 30) / nb_lo);
+  for (int c = 0; c < 10; ++c)
+    if (tm <= bound[c]) return classes[c](in, out, xm, xd, rank, hdr, st, 0, xc_rec, xc_offs, xc_shift);
   return table[0](in, out, xm, xd, rank, hdr, st, 0, xc_rec, xc_offs, xc_shift);
 }
 
