@@ -523,6 +523,7 @@ __global__ void __launch_bounds__(256) k_bk_scatter(const void* __restrict__ D, 
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const typename KT::K k = KT::load(D, i);
     const uint32_t pos = atomicAdd(cur + bk_digit<KT>(k, s, mask), 1u);
+    DM_ASSERT(pos < n, "bucket scatter pos %u n %llu", pos, (unsigned long long)n);
     NumStore<KT>::st(kout, pos, k);
     vout[pos] = (uint32_t)i;
   }
@@ -546,6 +547,8 @@ __global__ void __launch_bounds__(256) k_bk_local(const void* __restrict__ kin, 
     const uint32_t id = vin[p];
     const uint32_t d = bk_digit<KT>(k, s, mask);
     const uint32_t lo = off[d], hi = off[d + 1];
+    DM_ASSERT(lo <= p && p < hi && hi <= n, "bucket local p %llu lo %u hi %u n %llu", (unsigned long long)p, lo, hi,
+              (unsigned long long)n);
     uint32_t r = lo;
     for (uint32_t q = lo; q < hi; ++q) {
       const K kq = NumStore<KT>::ld(kin, q);

@@ -112,6 +112,7 @@ __device__ __forceinline__ uint32_t xc_lookup_smem8(uint32_t code, const uint2* 
   const uint32_t n = e_rel - s_rel;
   const uint32_t s3 = start & 3u, sh = 8u * s3;
   const uint32_t* w = offs32 + (start >> 2);
+  DM_ASSERT(n <= kXcMaxBlock || (int)r.x < 0, "xc smem list n %u", n);
   const uint32_t w0 = w[0], w1 = w[1];
   const uint32_t w2 = n + s3 > 8u ? w[2] : 0u;
   const uint32_t a = __funnelshift_r(w0, w1, sh), b = __funnelshift_r(w1, w2, sh);  // bytes [start, start + 8)
