@@ -98,21 +98,25 @@ __device__ __forceinline__ uint32_t bytes_lt_msb(uint32_t x, uint32_t y, uint32_
 // Lean shared-memory lookup (blocks of 256 codes, xs = 8): one 8-byte record,
 // an 8-byte window of the list read as two (a third, predicated, when the list
 // starts late in a word) conflict-prone shared loads, and a SIMD byte compare.
-// Lists longer than 8 and flagged superblocks take a rare slow path.  Counts
-// are those of xc_lookup; only the instruction and shared-load budget differ
-// (the kernel is bound by both).
+// Lists longer than 8 and flagged superblocks take a rare branch: the staging
+// copy rewrites a flagged record as {R, kXcFlagY}, whose byte pattern gives
+// every block a "length" above 8 (no valid record has it: cumulative counts
+// never decrease), so the fast path carries no flag test.  Counts are those of
+// xc_lookup; only the instruction and shared-load budget differ (the kernel is
+// bound by both).
+constexpr uint32_t kXcFlagY = 0x00ff00ffu;
+constexpr uint32_t kXcSmemSlack = 272;  // window reads up to R + 255 + 12 for a rewritten flagged record
 __device__ __forceinline__ uint32_t xc_lookup_smem8(uint32_t code, const uint2* __restrict__ rec,
                                                     const uint32_t* __restrict__ offs32,
                                                     const uint32_t* __restrict__ XM) {
   const uint2 r = rec[code >> 10];
-  const uint32_t ry = (int)r.x < 0 ? 0u : r.y;  // flagged: empty list at R (keeps the window in bounds)
   const uint32_t t8 = (code >> 5) & 24u;
-  const uint32_t s_rel = ((ry << 8) >> t8) & 255u, e_rel = (ry >> t8) & 255u;
-  const uint32_t start = (r.x & 0x7fffffffu) + s_rel;
+  const uint32_t s_rel = ((r.y << 8) >> t8) & 255u, e_rel = (r.y >> t8) & 255u;
+  const uint32_t start = r.x + s_rel;
   const uint32_t n = e_rel - s_rel;
   const uint32_t s3 = start & 3u, sh = 8u * s3;
   const uint32_t* w = offs32 + (start >> 2);
-  DM_ASSERT(n <= kXcMaxBlock || (int)r.x < 0, "xc smem list n %u", n);
+  DM_ASSERT(n <= kXcMaxBlock || r.y == kXcFlagY, "xc smem list n %u", n);
   const uint32_t w0 = w[0], w1 = w[1];
   const uint32_t w2 = n + s3 > 8u ? w[2] : 0u;
   const uint32_t a = __funnelshift_r(w0, w1, sh), b = __funnelshift_r(w1, w2, sh);  // bytes [start, start + 8)
@@ -120,8 +124,8 @@ __device__ __forceinline__ uint32_t xc_lookup_smem8(uint32_t code, const uint2* 
   const uint32_t k8 = 8u * umin32(n, 8u);
   const uint32_t ma = ~shl32(0xffffffffu, k8), mb = shr32(0xffffffffu, 64u - k8);
   uint32_t cnt = __popc(bytes_lt_msb(a, y, y7) & ma) + __popc(bytes_lt_msb(b, y, y7) & mb);
-  if (__builtin_expect(n > 8u || (int)r.x < 0, 0)) {
-    if ((int)r.x < 0) return __ldg(XM + code);  // flagged superblock: plain X_M
+  if (__builtin_expect(n > 8u, 0)) {
+    if (r.y == kXcFlagY) return __ldg(XM + code);  // flagged superblock: plain X_M
     const uint32_t o = code & 255u;
     for (uint32_t q = start + 8; q < start + n; ++q) cnt += ((offs32[q >> 2] >> (8 * (q & 3u))) & 255u) < o ? 1u : 0u;
   }
@@ -207,10 +211,10 @@ __global__ void __launch_bounds__(rec_threads<XMODE>(), XMODE == XM_XC_SMEM ? 1 
   if (xc_budget) {
     const uint64_t n_new = hdr->merged_dict_len - dict_len;
     xc_offs_bytes = (n_new + 15) & ~15ull;
-    // + 16: the two-word read may touch up to 8 bytes past the last entry
+    // + slack: the window reads past the last entry (kXcSmemSlack)
     // xc_dens (auto mode): also require n_new * 2^xc_dens <= |U_M|, i.e. short
     // lists (cfg2: 2.6 entries per 256-code block), else the L2 companion runs
-    const bool fits = ((nsb * kXcRecBytes + 15) & ~15ull) + xc_offs_bytes + 16 <= xc_budget &&
+    const bool fits = ((nsb * kXcRecBytes + 15) & ~15ull) + xc_offs_bytes + kXcSmemSlack <= xc_budget &&
                       (xc_dens == 0 || (n_new << xc_dens) <= dict_len);
     if ((XMODE == XM_XC_SMEM) != fits) return;
   }
@@ -245,7 +249,12 @@ __global__ void __launch_bounds__(rec_threads<XMODE>(), XMODE == XM_XC_SMEM ? 1 
   if (XMODE == XM_XC_SMEM) {
     const uint4* src = reinterpret_cast<const uint4*>(xrec);  // records, then the offsets
     uint4* dst = reinterpret_cast<uint4*>(sx);
-    for (uint64_t i = threadIdx.x; i < rec_pad / 16; i += blockDim.x) dst[i] = __ldg(src + i);
+    for (uint64_t i = threadIdx.x; i < rec_pad / 16; i += blockDim.x) {
+      uint4 v = __ldg(src + i);  // two records; flagged ones become {R, kXcFlagY}
+      if ((int)v.x < 0) v.x &= 0x7fffffffu, v.y = kXcFlagY;
+      if ((int)v.z < 0) v.z &= 0x7fffffffu, v.w = kXcFlagY;
+      dst[i] = v;
+    }
     const uint4* go = reinterpret_cast<const uint4*>(xoffs);
     uint4* so = dst + rec_pad / 16;
     for (uint64_t i = threadIdx.x; i < xc_offs_bytes / 16; i += blockDim.x) so[i] = __ldg(go + i);
