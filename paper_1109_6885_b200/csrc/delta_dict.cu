@@ -587,12 +587,31 @@ __device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// Slot tag: 0 empty; (h & ~3) | 1 claimed; | 3 ready (id and key published).
+// One 8-byte slot per entry: low word = tag (0 empty; (h & ~3) | 1 claimed;
+// | 3 ready), high word = the distinct id once ready, so a probe reads tag and id
+// in one access.  Probes and the spin read relaxed (no L1 invalidation); one
+// acquire load once a matching tag is ready orders the value read after it.
+// The claimant's release store orders its value write before (id, ready)
+// (measured: a __threadfence there and acquire probes took ~60% of the
+// kernel's stall samples on cfg3).
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_acquire_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 template <class KT>
 __global__ void __launch_bounds__(256) k_dedup_insert(const void* __restrict__ D, uint64_t n,
-                                                      uint32_t* __restrict__ tags, uint32_t* __restrict__ ids,
-                                                      uint64_t mask, void* __restrict__ dkeys,
-                                                      uint32_t* __restrict__ tid, unsigned long long* n_dist) {
+                                                      uint64_t* __restrict__ slots, uint64_t mask,
+                                                      void* __restrict__ dkeys, uint32_t* __restrict__ tid,
+                                                      unsigned long long* n_dist) {
   pdl_prologue();
   using K = typename KT::K;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
@@ -601,27 +620,21 @@ __global__ void __launch_bounds__(256) k_dedup_insert(const void* __restrict__ D
     uint64_t slot = (h >> 32) & mask;
     const uint32_t tg = ((uint32_t)h & ~3u) | 1u;
     uint32_t id = 0;
-    // Probes and the spin read the tag relaxed (no L1 invalidation); one acquire
-    // load once a matching tag is ready orders the id / value reads after it.
-    // The claimant's release store orders its value and id writes before
-    // "ready" (measured: an extra __threadfence there and acquire probes took
-    // ~60% of the kernel's stall samples on cfg3).
     for (;;) {
-      uint32_t t = ld_volatile_u32(tags + slot);
-      if (t == 0) {
-        t = atomicCAS(tags + slot, 0u, tg);
-        if (t == 0) {  // claimed: publish the value, then the id, then "ready"
+      uint64_t sv = ld_relaxed_u64(slots + slot);
+      if ((uint32_t)sv == 0) {
+        sv = atomicCAS(reinterpret_cast<unsigned long long*>(slots + slot), 0ull, (unsigned long long)tg);
+        if (sv == 0) {  // claimed: publish the value, then (id, ready)
           id = (uint32_t)atomicAdd(n_dist, 1ull);
           KT::store(dkeys, id, k);
-          ids[slot] = id;
-          st_release_u32(tags + slot, tg | 2u);
+          st_release_u64(slots + slot, ((uint64_t)id << 32) | tg | 2u);
           break;
         }
       }
-      if ((t | 2u) == (tg | 2u)) {  // same hash tag: wait until ready, compare the value
-        while (!(t & 2u)) t = ld_volatile_u32(tags + slot);
-        (void)ld_acquire_u32(tags + slot);
-        const uint32_t cid = __ldcg(ids + slot);
+      if (((uint32_t)sv | 2u) == (tg | 2u)) {  // same hash tag: wait until ready, compare the value
+        while (!((uint32_t)sv & 2u)) sv = ld_relaxed_u64(slots + slot);
+        sv = ld_acquire_u64(slots + slot);
+        const uint32_t cid = (uint32_t)(sv >> 32);
         if (KT::eq(KT::load_cg(dkeys, cid), k)) {
           id = cid;
           break;
@@ -675,8 +688,8 @@ cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, void* udict
     unsigned long long* n_dist = reinterpret_cast<unsigned long long*>(counters + CNT_DEDUP);
     const int sms = device_sms();
     launch_k(k_dedup_insert<KT>, (unsigned)std::min<uint64_t>((n + 255) / 256, (uint64_t)sms * 8), 256, 0, st, 
-        in->delta, n, reinterpret_cast<uint32_t*>(ws + L.dd_tags), reinterpret_cast<uint32_t*>(ws + L.dd_ids),
-        L.dd_cap - 1, ws + L.dd_keys, reinterpret_cast<uint32_t*>(ws + L.dd_tid), n_dist);
+        in->delta, n, reinterpret_cast<uint64_t*>(ws + L.dd_slots), L.dd_cap - 1, ws + L.dd_keys,
+        reinterpret_cast<uint32_t*>(ws + L.dd_tid), n_dist);
     note_launch();
     D = ws + L.dd_keys;
     n_dev = n_dist;

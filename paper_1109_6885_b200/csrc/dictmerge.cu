@@ -182,8 +182,7 @@ WsLayout ws_layout(const dm_column_in* in) {
     uint64_t cap = 1024;
     while (cap < 2 * nD) cap <<= 1;
     L.dd_cap = cap;
-    L.dd_tags = take(cap * 4);
-    L.dd_ids = take(cap * 4);
+    L.dd_slots = take(cap * 8);
     L.dd_keys = take(nD * E);
     L.dd_tid = take(nD * 4);
     L.dd_rank = take(nD * 4);
@@ -253,7 +252,7 @@ static dm_status merge_async(const dm_column_in* in, const dm_column_out* out, v
   };
   mark(0);
   cudaError_t e = cudaMemsetAsync(w, 0, L.zero_bytes, st);
-  if (e == cudaSuccess && L.dedup) e = cudaMemsetAsync(w + L.dd_tags, 0, L.dd_cap * 4, st);
+  if (e == cudaSuccess && L.dedup) e = cudaMemsetAsync(w + L.dd_slots, 0, L.dd_cap * 8, st);
   if (e == cudaSuccess && zero_header) e = cudaMemsetAsync(d_header, 0, sizeof(dm_header), st);
   if (e != cudaSuccess) return cuda_fail(e);
   void* udict = out->delta_dict ? out->delta_dict : (void*)(w + L.udict);

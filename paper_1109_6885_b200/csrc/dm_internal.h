@@ -150,8 +150,7 @@ struct WsLayout {
   size_t xc_rblk;        // XC: u32[nblk + 1], new values inserted before each 256-block
   size_t xc_rec;         // XC: uint2[nsb] superblock records
   size_t xc_offs;        // XC: u8[n_delta] insertion position mod 256 per new value
-  size_t dd_tags;        // dedup (NEXT1): u32[dd_cap] slot tags (memset per call)
-  size_t dd_ids;         // dedup: u32[dd_cap] distinct id per slot
+  size_t dd_slots;       // dedup (NEXT1): u64[dd_cap] (tag | id << 32) slots (memset per call)
   size_t dd_keys;        // dedup: distinct values, raw layout, n_delta capacity
   size_t dd_tid;         // dedup: u32[n_delta] distinct id per tuple
   size_t dd_rank;        // dedup: u32[n_delta] rank of each distinct id
