@@ -8,6 +8,11 @@
 // raw insertion-order array (BASELINE.json north_star), so the sort happens at
 // merge time:
 //
+// Two sorting paths with the same result (U_D sorted and distinct, r[k] =
+// rank of tuple k's value): for 2^11 <= N_D <= 2^23 the bucket path (k_bk_*,
+// below: one counting pass into ~N_D/4 buckets by the keys' top varying bits,
+// then a rank among the bucket mates) and otherwise, or when a bucket
+// overflows (skewed keys; decided on the device), the LSD radix passes:
 //   k_hist       one read of D: all digit histograms (8 or 16 byte passes) at
 //                once; the last block to finish turns them into the pass plan:
 //                exclusive digit offsets, and passes whose byte is constant over

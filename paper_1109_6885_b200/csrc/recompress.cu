@@ -10,21 +10,26 @@
 // (P:324); its time is the stream of the packed vectors plus the X gathers,
 // which hit the cache when X fits on die.
 //
-// GPU form: a persistent kernel, one CTA per SM slot.  The output rows are cut
-// into 4096-row chunks; a 32-row group is exactly b input u32 words and b'
-// output u32 words for every width, so chunks are word-aligned at both widths.
-//   * the main words of each chunk arrive by bulk TMA (cp.async.bulk, L2
-//     evict-first) into a 4-stage shared-memory ring guarded by mbarriers;
-//   * each warp handles whole 32-row groups: lane l unpacks row l with two
-//     conflict-free shared loads and a funnel shift, gathers X_M[code] through
-//     the read-only path with an L2 evict-last hint (X_M stays L2-resident
-//     while the streams flow past it), delta rows gather X_D[r[k]];
+// GPU form: a persistent, warp-specialised kernel, one CTA per SM slot.  The
+// output rows are cut into chunks of 32-row groups; a group is exactly b input
+// u32 words and b' output u32 words for every width, so chunks are
+// word-aligned at both widths.
+//   * one producer warp brings the main words of each chunk by bulk TMA
+//     (cp.async.bulk, L2 evict-first) into a 4-stage shared-memory ring guarded
+//     by mbarriers (full / empty per stage);
+//   * each consumer warp handles whole 32-row groups: lane l unpacks row l with
+//     two conflict-free shared loads and a funnel shift and translates it --
+//     plain X_M staged in shared memory (<= 96 KB), the compact table XC in
+//     shared memory (lean lookup below), plain X_M gathered through L2
+//     (evict-last: it stays resident while the streams flow past), or XC
+//     through L2; delta rows gather X_D[r[k]];
 //   * lane k builds output word k of the group from the <= ceil((b'+31)/b')
 //     codes that overlap it, fetched by warp shuffles (funnel packing across
-//     word boundaries), into a shared staging buffer;
-//   * the staged chunk leaves by bulk TMA store (L2 evict-first).
+//     word boundaries), and writes it with a streaming store (coalesced per
+//     group).
 // b' is only known on the device (no host sync): the host launches the width
-// specialisations that |U'|'s bounds allow and each exits unless it matches.
+// specialisations that |U'|'s bounds allow and each exits unless it matches
+// (wide ranges: one runtime-width kernel, see launch_recompress).
 #include <algorithm>
 #include <array>
 #include <cstdlib>
