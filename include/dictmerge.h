@@ -255,18 +255,22 @@ dm_status dm_merge_column_host(dm_ctx* ctx, const dm_column_in* in, dm_column_ou
 /* Process-wide tuning knobs (they never change results, only which kernels
  * run).  knob 0 = placement of the main translation table in Step 2(b):
  *   0 auto (default): plain X_M in shared memory when it fits (<= 96 KB);
- *     else, when the plain X_M exceeds 64 MB (it would not stay L2-resident),
- *     the compact table XC (per 2048 codes a 16-byte record,
- *     per new dictionary value one byte; X_M[c] = c + #{new values inserted at
- *     or before main position c}, P:224-230 restated) read through L2; else
- *     the plain X_M through L2;
+ *     else the compact table XC (per 4 blocks of 128 or 256
+ *     codes an 8-byte record, per new dictionary value one byte; X_M[c] = c +
+ *     #{new values inserted at or before main position c}
+ *     restated): staged in shared memory when X_M is at most 64 MB, its
+ *     records fit and the device finds few new values per block, read through
+ *     L2 when X_M exceeds 64 MB (it would not stay L2-resident); else the plain
+ *     X_M through L2.  When XC is read through L2 and X_M was not requested
+ *     (out->x_main NULL), X_M is only filled for the superblocks XC flags;
  *   1 plain X_M only;  2 XC, staged in shared memory when it fits, else L2;
  *   3 XC through L2.
  * knob 1 = Step 1(b) variant: 0 (default) bitmap-slot tiles in two passes
  *   (count, prefix sum, write: P:302-314); 1 the first GPU form (rank tiles,
  *   three kernels); 2 bitmap-slot tiles in one pass with decoupled look-back.
  * knob 2 = Step 1(a) front end: 0 (default) auto -- hash
- *   deduplication of D before the sort for 16-byte keys with N_D >= 65536;
+ *   deduplication of D before the sort for 16-byte keys with N_D >= 65536, and
+ *   for bucket-path deltas with N_D > 4 |U_M| (they must repeat values);
  *   1 never; 2 always.  Insert every tuple into a device hash table, sort only
  *   the distinct values, map each tuple to its value's rank (same U_D and r).
  *   Changes the workspace size: call dm_workspace_bytes after setting it.
