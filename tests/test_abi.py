@@ -90,3 +90,42 @@ def test_product_and_oracle_are_separate():
         if p.endswith((".py", ".cpp", ".h")):
             txt = open(p).read()
             assert not re.search(r"import paper_1109_6885_b200|from paper_1109_6885_b200|#include.*dictmerge\.h", txt), p
+
+
+def test_tuning_knobs_validated_on_the_host():
+    """dm_set_tuning (include/dictmerge.h): knobs 0..5 with their value ranges;
+    anything else is DM_E_INVALID.  Pure host logic (no GPU needed)."""
+    import paper_1109_6885_b200 as dm
+    L = dm._lib()
+    hi = {0: 3, 1: 2, 2: 2, 3: 1, 5: 2}
+    try:
+        for k, h in hi.items():
+            for v in range(h + 1):
+                assert L.dm_set_tuning(k, v) == dm.Status.OK, (k, v)
+            assert L.dm_set_tuning(k, h + 1) == dm.Status.E_INVALID, k
+            assert L.dm_set_tuning(k, -1) == dm.Status.E_INVALID, k
+        for v in (0, 7, 8):
+            assert L.dm_set_tuning(4, v) == dm.Status.OK
+        for v in (1, 6, 9):
+            assert L.dm_set_tuning(4, v) == dm.Status.E_INVALID
+        assert L.dm_set_tuning(6, 0) == dm.Status.E_INVALID
+    finally:
+        for k in range(6):
+            L.dm_set_tuning(k, 0)
+
+
+def test_bucket_path_workspace():
+    """The Step 1(a) bucket path (knob 5) sizes its own workspace: ~N_D/4 bucket
+    offsets; forcing the LSD passes (knob 5 = 1) drops them."""
+    import paper_1109_6885_b200 as dm
+    L = dm._lib()
+    cin = dm._In(0, 16, 1000, 16, 5000, 10, 16, 1_000_000)
+    try:
+        L.dm_set_tuning(5, 0)
+        auto = dm.workspace_bytes(cin)
+        L.dm_set_tuning(5, 1)
+        lsd = dm.workspace_bytes(cin)
+        assert auto > lsd
+        assert auto - lsd >= 4 * (1_000_000 // 8)  # bucket offsets (u32, >= N_D / 8 buckets)
+    finally:
+        L.dm_set_tuning(5, 0)
