@@ -529,8 +529,13 @@ __global__ void __launch_bounds__(256) k_bk_scatter(const void* __restrict__ D, 
     const typename KT::K k = KT::load(D, i);
     const uint32_t pos = atomicAdd(cur + bk_digit<KT>(k, s, mask), 1u);
     DM_ASSERT(pos < n, "bucket scatter pos %u n %llu", pos, (unsigned long long)n);
-    NumStore<KT>::st(kout, pos, k);
-    vout[pos] = (uint32_t)i;
+    if constexpr (KT::kBytes <= 8) {  // one 16-byte (key, index) record: one scattered store
+      const uint64_t k64 = (uint64_t)k;
+      static_cast<uint4*>(kout)[pos] = make_uint4((uint32_t)k64, (uint32_t)(k64 >> 32), (uint32_t)i, 0u);
+    } else {
+      NumStore<KT>::st(kout, pos, k);
+      vout[pos] = (uint32_t)i;
+    }
   }
 }
 
@@ -547,17 +552,32 @@ __global__ void __launch_bounds__(256) k_bk_local(const void* __restrict__ kin, 
   using K = typename KT::K;
   const uint64_t n = n_dev ? (uint64_t)*n_dev : n_host;
   const uint32_t s = st->shift, mask = (uint32_t)((1ull << bits) - 1);
+  // 4/8-byte keys arrive as 16-byte (key, index) records (k_bk_scatter)
   for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n; p += (uint64_t)gridDim.x * blockDim.x) {
-    const K k = NumStore<KT>::ld(kin, p);
-    const uint32_t id = vin[p];
+    K k;
+    uint32_t id;
+    if constexpr (KT::kBytes <= 8) {
+      const uint4 v = static_cast<const uint4*>(kin)[p];
+      k = (K)(((uint64_t)v.y << 32) | v.x);
+      id = v.z;
+    } else {
+      k = NumStore<KT>::ld(kin, p);
+      id = vin[p];
+    }
     const uint32_t d = bk_digit<KT>(k, s, mask);
     const uint32_t lo = off[d], hi = off[d + 1];
     DM_ASSERT(lo <= p && p < hi && hi <= n, "bucket local p %llu lo %u hi %u n %llu", (unsigned long long)p, lo, hi,
               (unsigned long long)n);
     uint32_t r = lo;
     for (uint32_t q = lo; q < hi; ++q) {
-      const K kq = NumStore<KT>::ld(kin, q);
-      r += KT::lt(kq, k) ? 1u : (KT::eq(kq, k) && vin[q] < id) ? 1u : 0u;
+      if constexpr (KT::kBytes <= 8) {
+        const uint4 v = static_cast<const uint4*>(kin)[q];
+        const K kq = (K)(((uint64_t)v.y << 32) | v.x);
+        r += KT::lt(kq, k) ? 1u : (KT::eq(kq, k) && v.z < id) ? 1u : 0u;
+      } else {
+        const K kq = NumStore<KT>::ld(kin, q);
+        r += KT::lt(kq, k) ? 1u : (KT::eq(kq, k) && vin[q] < id) ? 1u : 0u;
+      }
     }
     NumStore<KT>::st(kout, r, k);
     vout[r] = id;
@@ -714,9 +734,10 @@ cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, void* udict
     launch_k(k_bk_count<KT>, g, 256, 0, st, D, n, n_dev, (const BucketState*)bst, off, L.bk_bits);
     launch_k(k_bk_scan, (unsigned)(nb / (256 * kBkScanItems)), 256, 0, st, off, cur, nb,
              reinterpret_cast<uint64_t*>(ws + L.bk_status), counters + CNT_BKSCAN, bst);
+    void* const scat = KT::kBytes <= 8 ? (void*)(ws + L.bk_pairs) : (void*)(ws + L.keys1);
     launch_k(k_bk_scatter<KT>, g, 256, 0, st, D, n, n_dev, (const BucketState*)bst, cur, L.bk_bits,
-             (void*)(ws + L.keys1), reinterpret_cast<uint32_t*>(ws + L.vals1));
-    launch_k(k_bk_local<KT>, g, 256, 0, st, (const void*)(ws + L.keys1),
+             scat, reinterpret_cast<uint32_t*>(ws + L.vals1));
+    launch_k(k_bk_local<KT>, g, 256, 0, st, (const void*)scat,
              reinterpret_cast<const uint32_t*>(ws + L.vals1), n, n_dev, (const BucketState*)bst,
              (const uint32_t*)off, L.bk_bits, (void*)(ws + L.keys0), reinterpret_cast<uint32_t*>(ws + L.vals0));
     note_launch(5);

@@ -175,6 +175,7 @@ WsLayout ws_layout(const dm_column_in* in) {
   L.xc_offs = take(nD + 16);
   if (L.bucket) {
     L.bk_off = take(((1ull << L.bk_bits) + 1) * 4);
+    if (E <= 8) L.bk_pairs = take(nD * 16);
     L.bk_cur = take((1ull << L.bk_bits) * 4);
   }
   L.dedup = dedup_wanted(in);

@@ -161,6 +161,7 @@ struct WsLayout {
   size_t bk_state;       // BucketState (zeroed region)
   size_t bk_status;      // u64[scan tiles + 1] look-back (zeroed region)
   size_t bk_off;         // u32[B + 1]: counts, then exclusive offsets
+  size_t bk_pairs;       // 4/8-byte keys: 16-byte (key, index) records, n_delta
   size_t bk_cur;         // u32[B]: scatter cursors
   size_t total;
   uint64_t ntiles_sort, ntiles_unique, ntiles_merge;
