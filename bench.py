@@ -10,10 +10,13 @@ region starts, L2 flushed (512 MB write) before every timed step.
 
 Default workload: BASELINE.json configs[1] ("cfg2": N_M = 1e8 rows at 24 bits over
 a 1e7-entry u64 dictionary, N_D = 1e6, 10% new) -- the config the metric is quoted
-on.  N > 1 (torchrun, one rank per GPU): whole columns are independent units
-(P:184), so each rank merges its own column (cfg1/2/3/5) or its LPT share of
-the 300 columns (cfg4): no collective on the data path, weak scaling, step time =
-max over ranks.  Prints ONE JSON line (rank 0).  Keys: DESIGN.md "Measurement".
+on.  N > 1 (torchrun, one rank per GPU), strong scaling (the workload is the same
+at every N): a single column (cfg1/2/2e4/3/5) is split by output rows through the
+library's dm_merge_column_sharded (root Steps 1(a)-2(a), XC broadcast over NCCL,
+Step 2(b) per row range: the paper's tuple split of Step 2); the 300-column
+table (cfg4) is split by whole columns, LPT, no collective.  Step
+time = max over ranks.  Prints ONE JSON line (rank 0).  Keys: DESIGN.md
+"Measurement".
 """
 from __future__ import annotations
 
@@ -222,6 +225,110 @@ def reference_arm(args, rank, world):
     return 0
 
 
+# ----------------------------------------------------------- N > 1: one column row-sharded
+def sharded_inputs(workload: str, rank: int, world: int, dev):
+    """(UM, D on the root else None, this rank's packed main-code shard, n_main,
+    main_bits, dict_len, n_delta, key): the row plan is the library's
+    (dm_plan_row_shards); the shard is packed from bit 0 (its first row is a
+    multiple of 4096, so these are exactly the words of the full packing)."""
+    import torch
+    import paper_1109_6885_b200 as dm
+    cfg = cfg_number(workload)
+    UM = D = None
+    if cfg == 5:
+        from datagen import torch_gen
+        UM, codes, bits, D = torch_gen.make_cfg5(seed=datagen.BASE_SEED, device=dev)
+        n_main, dict_len, n_delta, key = codes.numel(), UM.shape[0], D.shape[0], "u64"
+    else:
+        col = datagen.make_config_e4() if workload.endswith("e4") else datagen.make_config(cfg)
+        codes = torch.from_numpy(col.main_codes.view(np.int32))
+        n_main, bits, dict_len, n_delta, key = col.n_main, col.main_bits, col.dict_len, col.n_delta, col.key
+        if rank == 0:
+            if col.key in ("u64", "u32"):
+                it = np.int64 if col.key == "u64" else np.int32
+                UM = torch.from_numpy(col.main_dict.view(it)).to(dev)
+                D = torch.from_numpy(col.delta.view(it)).to(dev)
+            else:
+                UM = torch.from_numpy(np.ascontiguousarray(col.main_dict)).to(dev)
+                D = torch.from_numpy(np.ascontiguousarray(col.delta)).to(dev)
+        del col
+    cuts = dm.plan_row_shards(n_main, n_delta, world)
+    m0, m1 = min(cuts[rank], n_main), min(cuts[rank + 1], n_main)
+    shard = dm.pack_codes(codes[m0:m1].to(dev), bits) if m1 > m0 else torch.zeros(2, dtype=torch.int64, device=dev)
+    del codes
+    if rank != 0:
+        UM = D = None
+    return UM, D, shard, n_main, bits, dict_len, n_delta, key, cuts
+
+
+def run_sharded(args, rank, world, local, dev, backend):
+    """One column's merge split by output rows over the ranks (the
+    paper's tuple split of Step 2) through dm_merge_column_sharded: strong
+    scaling (the column is fixed, every rank does 1/N of Step 2 after the root's
+    Step 1 and the table broadcasts)."""
+    import torch
+    import torch.distributed as dist
+    import paper_1109_6885_b200 as dm
+    UM, D, shard, n_main, bits, dict_len, n_delta, key, cuts = sharded_inputs(args.workload, rank, world, dev)
+    comm = dm.Comm.nccl() if backend == "nccl" else dm.Comm.callbacks()
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    def step():
+        return dm.merge_column_sharded(comm, shard, n_main, bits, dict_len, n_delta, main_dict=UM, delta=D, key=key)
+
+    for _ in range(max(args.warmup, 0)):
+        r = step()
+    torch.cuda.synchronize()
+    launches0 = dm.launch_count()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            dist.barrier()
+            ev[k][0].record()
+            r = step()
+            ev[k][1].record()
+        torch.cuda.synchronize()
+    dist.barrier()
+    launches = dm.launch_count() - launches0
+    total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    red_dev = dev if backend == "nccl" else torch.device("cpu")
+    t = torch.tensor([total_ms], dtype=torch.float64, device=red_dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_per_step = float(t.item()) / args.steps
+    n_tuples = n_main + n_delta
+    value = n_tuples / (ms_per_step / 1e3)
+    comm.close()
+    if rank == 0:
+        pk = peaks()
+        peak_hbm = pk["hbm_gbs"] if pk else 6650.0
+        kb = 8 if key == "u64" else 4 if key == "u32" else 16
+        sb = strict_bytes(n_main, bits, n_delta, kb, dict_len, r.merged_len, r.merged_bits)
+        achieved = sb / (ms_per_step / 1e3) / 1e9
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": key_dtype(args.workload),
+            "data": f"synthetic (datagen, seeded; BASELINE configs[{cfg_number(args.workload) - 1}])",
+            "config": {"workload": WORKLOADS[args.workload],
+                       "parallelism": f"row-sharded x{world}: root Steps 1(a)-2(a), XC broadcast, "
+                                      f"Step 2(b) by output rows (dm_merge_column_sharded, "
+                                      f"{'NCCL' if backend == 'nccl' else 'host callbacks over ' + backend})",
+                       "row_cuts": cuts, "l2": "flushed (512 MB write) before every timed step",
+                       "timing": "CUDA events around the collective call on each rank, max over ranks"},
+            "roofline": {"kernel": "whole sharded merge (strict bytes of the column / step time, all GPUs)",
+                         "bound": "hbm", "achieved": achieved, "peak": peak_hbm * world, "unit": "GB/s",
+                         "frac": achieved / (peak_hbm * world), "traffic": None,
+                         "algorithmic_bytes_per_launch": sb},
+            "cpu_baseline": None,
+            "e2e": None,
+            "gpu_launches": int(launches), "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    return 0
+
+
 # ------------------------------------------------------------------------- main
 def main():
     ap = argparse.ArgumentParser()
@@ -263,6 +370,10 @@ def main():
     red_dev = dev if backend == "nccl" else torch.device("cpu")
 
     cfg = cfg_number(args.workload)
+    if world > 1 and cfg != 4:  # one column, split by rows over the ranks (strong scaling)
+        rc = run_sharded(args, rank, world, local, dev, backend)
+        dist.destroy_process_group()
+        return rc
     table = cfg == 4
     # ---- inputs, resident in HBM
     if cfg == 5:
@@ -374,6 +485,7 @@ def main():
     # ---- optional: the paper's unoptimized Step 2 on the same merge (NEXT4)
     naive = None
     if args.naive_step2 and not table:
+        prev_step2 = dm.get_tuning(dm.KNOB_STEP2)
         dm.set_tuning(dm.KNOB_STEP2, 1)
         nm = dm.ColumnMerger(*dev_cols[0])
         nm.run_async()
@@ -387,7 +499,7 @@ def main():
             flush.zero_()
             nm.run_async_timed(nev[k])
         torch.cuda.synchronize()
-        dm.set_tuning(dm.KNOB_STEP2, 0)
+        dm.set_tuning(dm.KNOB_STEP2, prev_step2)
         nr = nm.result()
         same = bool(torch.equal(nr.merged_codes, results[0].merged_codes))
         n2 = statistics.mean(nev[k][2].elapsed_time(nev[k][3]) for k in range(args.steps))
@@ -436,7 +548,8 @@ def main():
     if rank == 0:
         r0 = results[0]
         cfgd = {"workload": WORKLOADS[args.workload], "columns_per_rank": len(dev_cols),
-                "parallelism": f"column-sharded x{world} (independent columns, no collective)",
+                "parallelism": (f"column-sharded x{world}: LPT share of the 300 independent columns per rank "
+                                f"(P:184, P:296), no collective" if table else "single GPU"),
                 "l2": "flushed (512 MB write) before every timed step",
                 "timing": "CUDA-graph replay of the whole merge, CUDA events on the launching stream"}
         if not table:
@@ -446,7 +559,7 @@ def main():
         line = {
             "metric": METRIC if not table else "merged column-tuples/sec (sum over columns of N_M+N_D)",
             "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": key_dtype(args.workload),
             "data": f"synthetic (datagen, seeded; BASELINE configs[{cfg - 1}])", "config": cfgd,
             "hbm_fraction_strict": sb / (ms_per_step / 1e3) / 1e9 / peak_hbm,

@@ -364,3 +364,25 @@ def make_random_case(seed: int, n_main: int, dict_len: int, n_delta: int, p_new:
         return u32_column(_u64_column(seed, n_main, dict_len, n_delta, p_new, min(value_bits, 32),
                                       main_bits=main_bits, name=f"rand{seed}"))
     return _b16_column(seed, n_main, dict_len, n_delta, p_new, main_bits=main_bits, name=f"rand{seed}")
+
+
+def make_clustered_case(seed: int, n_main: int, dict_len: int, n_delta: int, key: str = "u64") -> Column:
+    """A column whose new delta values cluster: U_M[i] = 1000 (i + 1), and about half
+    of the new values land in a few gaps of U_M (dozens per gap), the rest spread
+    uniformly; 30% of the tuples reuse main values.  Exercises dense insertion
+    runs (many new values between two neighbouring main values)."""
+    SP = 1000
+    UM = (np.arange(dict_len, dtype=np.uint64) + np.uint64(1)) * np.uint64(SP)
+    n_new = int(n_delta * 0.7)
+    n_hot = max(1, n_new // 60)  # gaps receiving ~30 new values each
+    hot = uniform_below(seed, 1, np.arange(n_hot, dtype=np.uint64), dict_len + 1)
+    gap = np.concatenate([np.repeat(hot, 30), uniform_below(seed, 2, np.arange(max(n_new - 30 * n_hot, 0),
+                                                                                dtype=np.uint64), dict_len + 1)])
+    off = uniform_below(seed, 3, np.arange(gap.size, dtype=np.uint64), SP - 1) + np.uint64(1)
+    new = np.unique(gap.astype(np.uint64) * np.uint64(SP) + off)
+    reuse = UM[uniform_below(seed, 4, np.arange(n_delta - min(new.size, n_delta), dtype=np.uint64), dict_len)]
+    D = np.concatenate([new[:n_delta], reuse])
+    D = D[np.argsort(rnd(seed, 5, np.arange(D.size, dtype=np.uint64)), kind="stable")]
+    codes = uniform_below(seed, 6, np.arange(n_main, dtype=np.uint64), dict_len).astype(np.uint32)
+    col = Column("u64", UM, codes, width_hint(dict_len), D.astype(np.uint64), f"clustered{seed}")
+    return u32_column(col) if key == "u32" else col

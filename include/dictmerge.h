@@ -185,7 +185,8 @@ dm_status dm_xc_rebase_async(void* records, uint64_t n_records, uint32_t add, vo
  * for k < n_delta, packed at new_bits (1..32) into dm_words(n_main + n_delta,
  * new_bits) words of out_codes (capacity out_cap_words).  Every table value must
  * be < 2^new_bits.  main_codes at main_bits (1..32), codes < dict_len (else
- * DM_E_CODE_RANGE, reported after a stream synchronisation).  Device pointers,
+ * DM_E_CODE_RANGE, reported after a stream synchronisation).  With n_main > 0,
+ * 1 <= dict_len < 2^32 and main_bits >= dm_width(dict_len), else DM_E_INVALID.  Device pointers,
  * 16-byte aligned.  Synchronous. */
 dm_status dm_recompress(const uint64_t* main_codes, uint64_t n_main, uint32_t main_bits, uint64_t dict_len,
                         const uint32_t* x_main, const uint32_t* x_delta, const uint32_t* delta_rank,
@@ -216,8 +217,9 @@ typedef struct {
 dm_status dm_xc_export(const dm_column_in* in, const void* ws, size_t ws_bytes, dm_xc* xc);
 /* Gather the X_M slices of flagged superblocks: for each, ids[slot] = its
  * record index and slices[slot * 4 << shift ...] = its X_M entries; *d_count
- * (device u64) = number of slots.  Capacities: ids n_records, slices
- * n_records * (4 << shift).  Stream-ordered. */
+ * (device u64) = number of slots.  Capacities: ids >= count, slices >=
+ * count * (4 << shift).  ids = slices = NULL: count only (x_main may be NULL);
+ * a caller sizes the buffers from that count first.  Stream-ordered. */
 dm_status dm_xc_exceptions_gather(const dm_xc* xc, uint64_t dict_len, const uint32_t* x_main, uint32_t* ids,
                                   uint32_t* slices, uint64_t* d_count, void* cuda_stream);
 /* The inverse on a receiving rank: write the `count` slices into x_main (a
@@ -232,6 +234,95 @@ dm_status dm_recompress_xc(const uint64_t* main_codes, uint64_t n_main, uint32_t
                            const uint32_t* delta_rank, uint64_t n_delta, uint32_t new_bits, uint64_t* out_codes,
                            uint64_t out_cap_words, void* cuda_stream);
 
+/* ---------------------------------------------------------------- sharded merge
+ * One column's merge spread over the ranks of a communicator, one GPU per rank
+ * (SURVEY §8e).  The paper splits Step 2 over threads by tuples, "the N' tuples
+ * are evenly split between the threads", every thread translating its
+ * own range through the shared tables (Eq 11); here the threads are GPUs
+ * and the tables cross NVLink once.  Output rows [0, N') are cut into one
+ * contiguous range per rank (dm_plan_row_shards); rank g holds the packed main
+ * codes of its range's main rows and writes its range's M' words.
+ *
+ * Transport: dm_comm, either NCCL (dm_comm_init_nccl; the library resolves
+ * ncclBroadcast / ncclAllGather / ncclSend / ncclRecv at run time from the
+ * process's libnccl.so.2) or caller-supplied callbacks over HOST buffers
+ * (dm_comm_init_callbacks: any process-group library; the library stages device
+ * data through pinned host memory and synchronises around each call).  Every
+ * rank calls the collectives in the same order; callbacks return 0 on success. */
+typedef struct dm_comm dm_comm;
+typedef struct {
+  /* buf: `bytes` host bytes; on `root` the data, elsewhere filled in */
+  int (*broadcast)(void* buf, uint64_t bytes, int root, void* user);
+  /* recv: nranks * bytes host bytes, rank g's `send` at offset g * bytes */
+  int (*allgather)(const void* send, void* recv, uint64_t bytes, void* user);
+  /* is_send = 1: send `bytes` of buf to `peer`; 0: receive them from `peer` into buf */
+  int (*sendrecv)(void* buf, uint64_t bytes, int peer, int is_send, void* user);
+  void* user;
+} dm_comm_callbacks;
+/* 128 bytes: a fresh NCCL unique id for rank 0 to hand to every rank (host).
+ * DM_E_NCCL when no NCCL library can be loaded. */
+dm_status dm_comm_nccl_unique_id(void* id_out);
+/* Collective over the nranks processes; `device` becomes the current device.
+ * NULL on failure. */
+dm_comm* dm_comm_init_nccl(const void* id, int nranks, int rank, int device);
+/* The callbacks struct is copied; it must stay valid (its `user`) for the comm's life. */
+dm_comm* dm_comm_init_callbacks(const dm_comm_callbacks* cb, int nranks, int rank);
+void dm_comm_destroy(dm_comm* comm);
+int dm_comm_rank(const dm_comm* comm);
+int dm_comm_size(const dm_comm* comm);
+/* Host-only self-test of a callback transport (no GPU): broadcast from every
+ * root, an all-gather in rank order and a rank 0 -> last rank transfer.
+ * Collective.  DM_OK, or DM_E_NCCL if any byte arrived wrong. */
+dm_status dm_comm_selftest_host(dm_comm* comm);
+
+/* cuts[0..nranks]: rank g owns output rows [cuts[g], cuts[g+1]) of the
+ * N' = n_main + n_delta rows (main rows first, then delta rows);
+ * every cut but the last is a multiple of 4096, so every range starts on a u64
+ * word at both widths.  Host, pure. */
+void dm_plan_row_shards(uint64_t n_main, uint64_t n_delta, int nranks, uint64_t* cuts);
+/* u64 words rank `rank`'s M' range can need: its rows at the widest possible
+ * b' = width(dict_len + n_delta).  Host, pure. */
+uint64_t dm_sharded_codes_cap_words(uint64_t dict_len, uint64_t n_main, uint64_t n_delta, int nranks, int rank);
+
+enum { DM_TABLES_XC = 0, DM_TABLES_PLAIN = 1 };
+typedef struct {
+  int32_t key;                 /* dm_key, the same on every rank                         */
+  int32_t tables;              /* DM_TABLES_XC: broadcast the compact table XC (NEXT3)   *
+                                * (+ the X_M slices of flagged superblocks); PLAIN: the  *
+                                * literal X_M (SURVEY §8e's control design)              */
+  int32_t root;                /* rank that holds U_M and D and runs Steps 1(a)-2(a)     */
+  const void* main_dict;       /* root: U_M (device), strictly increasing; others ignored */
+  uint64_t dict_len;           /* |U_M| (every rank)                                     */
+  const void* delta;           /* root: D (device), insertion order; others ignored      */
+  uint64_t n_delta;            /* N_D (every rank)                                       */
+  const uint64_t* main_codes;  /* this rank's main rows [min(cuts[g], N_M),              *
+                                * min(cuts[g+1], N_M)) packed at main_bits from bit 0    *
+                                * (device, 16-byte aligned)                              */
+  uint64_t n_main;             /* N_M, the whole column (every rank)                     */
+  uint32_t main_bits;          /* b (every rank)                                         */
+} dm_sharded_in;
+typedef struct {
+  void* merged_dict;               /* root: U' (device), capacity merged_dict_cap keys   */
+  uint64_t merged_dict_cap;        /* root: >= dict_len + n_delta                        */
+  uint64_t* merged_codes;          /* this rank's M' words: rows [cuts[g], cuts[g+1])    *
+                                    * at b' from bit 0 (device, 16-byte aligned)         */
+  uint64_t merged_codes_cap_words; /* >= dm_sharded_codes_cap_words(...)                 */
+  uint64_t merged_dict_len;        /* out (every rank): |U'|                            */
+  uint32_t merged_bits;            /* out (every rank): b'                              */
+} dm_sharded_out;
+/* Collective, synchronous.  1. every rank's descriptor (key, tables, root,
+ * |U_M|, N_M, N_D, b) must agree (all-gather; else DM_E_INVALID everywhere);
+ * 2. root: Steps 1(a)-2(a); 3. broadcast of the result
+ * header; 4. broadcast of XC (or X_M); 5. root computes the delta rows' codes
+ * X_D[r[k]] and sends each owner its slice; 6. every rank:
+ * Step 2(b) of its rows (Eq 11).  Concatenating the ranks' M' words in
+ * rank order gives the merged code vector of dm_merge_column, bit for bit.
+ * Temporaries come from the device's stream-ordered memory pool and are
+ * released before return (a non-root rank holding flagged-superblock slices
+ * allocates a sparse |U_M|-entry X_M).  Returns the worst status of all ranks;
+ * DM_E_NCCL for a failed transport call. */
+dm_status dm_merge_column_sharded(dm_comm* comm, const dm_sharded_in* in, dm_sharded_out* out, void* cuda_stream);
+
 /* Pack n u32 codes (each < 2^bits) into dm_words(n, bits) words at `bits`
  * (device pointers; words need not be zeroed).  Stream-ordered. */
 dm_status dm_pack_codes(const uint32_t* codes, uint64_t n, uint32_t bits, uint64_t* words, void* cuda_stream);
@@ -239,6 +330,11 @@ dm_status dm_pack_codes(const uint32_t* codes, uint64_t n, uint32_t bits, uint64
 dm_status dm_unpack_codes(const uint64_t* words, uint64_t n, uint32_t bits, uint32_t* codes, void* cuda_stream);
 
 /* Host-buffer entry point (end-to-end use).  `in` and `out` hold HOST pointers
+ * (checked before any copy: a NULL input with a non-zero length or a NULL
+ * merged_dict / merged_codes gives DM_E_INVALID; merged_dict_cap < dict_len +
+ * n_delta or merged_codes_cap_words < dm_merged_codes_cap_words(in) gives
+ * DM_E_CAPACITY; the optional x_main / x_delta / delta_dict / delta_rank
+ * buffers must hold dict_len / n_delta entries)
  * (pinned memory gives full PCIe bandwidth and copy/compute overlap); the
  * context owns device staging buffers, grows them on demand and reuses them
  * across calls.  Pipelined over three streams: U_M and D are uploaded first and
@@ -265,9 +361,12 @@ dm_status dm_merge_column_host(dm_ctx* ctx, const dm_column_in* in, dm_column_ou
  *     (out->x_main NULL), X_M is only filled for the superblocks XC flags;
  *   1 plain X_M only;  2 XC, staged in shared memory when it fits, else L2;
  *   3 XC through L2.
- * knob 1 = Step 1(b) variant: 0 (default) bitmap-slot tiles in two passes
- *   (count, prefix sum, write: P:302-314); 1 the first GPU form (rank tiles,
- *   three kernels); 2 bitmap-slot tiles in one pass with decoupled look-back.
+ * knob 1 = Step 1(b) variant: 0 (default) auto -- sparse-delta tiles when
+ *   N_D <= |U_M| / 8, else bitmap-slot tiles in two passes (count, prefix sum,
+ *   write: P:302-314); 1 the first GPU form (rank tiles, three kernels); 2
+ *   bitmap-slot tiles in one pass with decoupled look-back; 3 sparse-delta
+ *   tiles always (|U_M| > 0): U_M tiles of 2048 with the U_D values that fall
+ *   into them, one pass (copy U_M with gaps, insert the new values).
  * knob 2 = Step 1(a) front end: 0 (default) auto -- hash
  *   deduplication of D before the sort for 16-byte keys with N_D >= 65536, and
  *   for bucket-path deltas with N_D > 4 |U_M| (they must repeat values);
@@ -290,6 +389,9 @@ dm_status dm_merge_column_host(dm_ctx* ctx, const dm_column_in* in, dm_column_ou
  * Returns DM_OK, or DM_E_INVALID for an unknown knob or value.  Affects calls
  * made after it returns (a captured CUDA graph keeps the kernels it recorded). */
 int dm_set_tuning(int knob, int value);
+/* Current value of a knob (>= 0), or DM_E_INVALID for an unknown knob.  Lets a
+ * caller that changes a knob restore it afterwards. */
+int dm_get_tuning(int knob);
 
 /* Number of library kernels launched by this process so far (monotone). */
 uint64_t dm_launch_count(void);

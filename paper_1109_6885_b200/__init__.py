@@ -29,7 +29,8 @@ __all__ = [
     "KEY_U64", "KEY_B16", "Status", "DictMergeError", "width", "words", "merged_codes_cap_words",
     "workspace_bytes", "merge_column", "merge_column_async", "merge_table", "pack_codes", "unpack_codes",
     "ColumnMerger", "HostContext", "launch_count", "lib_path", "set_tuning", "XcTables", "recompress_xc",
-    "xc_exceptions_gather", "xc_exceptions_scatter", "lower_bound", "rebase", "DictionaryMerger",
+    "xc_exceptions_gather", "xc_exceptions_scatter", "lower_bound", "rebase", "DictionaryMerger", "get_tuning",
+    "tuning", "Comm", "plan_row_shards", "merge_column_sharded", "ShardedResult", "sharded_codes_cap_words",
 ]
 
 KEY_U64, KEY_B16, KEY_U32 = 0, 1, 2
@@ -66,6 +67,30 @@ class _Out(ctypes.Structure):
 class _Xc(ctypes.Structure):
     _fields_ = [("records", ctypes.c_void_p), ("n_records", ctypes.c_uint64), ("offsets", ctypes.c_void_p),
                 ("offsets_cap", ctypes.c_uint64), ("shift", ctypes.c_uint32), ("built", ctypes.c_int32)]
+
+
+class _ShIn(ctypes.Structure):
+    _fields_ = [("key", ctypes.c_int32), ("tables", ctypes.c_int32), ("root", ctypes.c_int32),
+                ("main_dict", ctypes.c_void_p), ("dict_len", ctypes.c_uint64), ("delta", ctypes.c_void_p),
+                ("n_delta", ctypes.c_uint64), ("main_codes", ctypes.c_void_p), ("n_main", ctypes.c_uint64),
+                ("main_bits", ctypes.c_uint32)]
+
+
+class _ShOut(ctypes.Structure):
+    _fields_ = [("merged_dict", ctypes.c_void_p), ("merged_dict_cap", ctypes.c_uint64),
+                ("merged_codes", ctypes.c_void_p), ("merged_codes_cap_words", ctypes.c_uint64),
+                ("merged_dict_len", ctypes.c_uint64), ("merged_bits", ctypes.c_uint32)]
+
+
+_CB_BCAST = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_void_p)
+_CB_AGATHER = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p)
+_CB_SENDRECV = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_int,
+                                ctypes.c_void_p)
+
+
+class _Cbs(ctypes.Structure):
+    _fields_ = [("broadcast", _CB_BCAST), ("allgather", _CB_AGATHER), ("sendrecv", _CB_SENDRECV),
+                ("user", ctypes.c_void_p)]
 
 
 class _Hdr(ctypes.Structure):
@@ -114,11 +139,22 @@ def _lib():
             "dm_merge_column_host": (i32, [vp, P(_In), P(_Out)]),
             "dm_launch_count": (u64, []),
             "dm_set_tuning": (i32, [i32, i32]),
+            "dm_get_tuning": (i32, [i32]),
             "dm_xc_export": (i32, [P(_In), vp, ctypes.c_size_t, P(_Xc)]),
             "dm_xc_exceptions_gather": (i32, [P(_Xc), u64, vp, vp, vp, vp, vp]),
             "dm_xc_exceptions_scatter": (i32, [P(_Xc), u64, vp, vp, u64, vp, vp]),
             "dm_recompress_xc": (i32, [vp, u64, u32, u64, P(_Xc), vp, vp, vp, u64, u32, vp, u64, vp]),
             "dm_last_cuda_error": (i32, []),
+            "dm_comm_nccl_unique_id": (i32, [vp]),
+            "dm_comm_init_nccl": (vp, [vp, i32, i32, i32]),
+            "dm_comm_init_callbacks": (vp, [P(_Cbs), i32, i32]),
+            "dm_comm_destroy": (None, [vp]),
+            "dm_comm_rank": (i32, [vp]),
+            "dm_comm_size": (i32, [vp]),
+            "dm_comm_selftest_host": (i32, [vp]),
+            "dm_plan_row_shards": (None, [u64, u64, i32, P(u64)]),
+            "dm_sharded_codes_cap_words": (u64, [u64, u64, u64, i32, i32]),
+            "dm_merge_column_sharded": (i32, [vp, P(_ShIn), P(_ShOut), vp]),
             "dm_status_str": (ctypes.c_char_p, [i32]),
         }
         for name, (res, args) in sig.items():
@@ -156,6 +192,31 @@ def set_tuning(knob: int, value: int) -> None:
     st = _lib().dm_set_tuning(knob, value)
     if st != Status.OK:
         raise DictMergeError(st, "dm_set_tuning")
+
+
+def get_tuning(knob: int) -> int:
+    """dm_get_tuning: the knob's current value."""
+    v = int(_lib().dm_get_tuning(knob))
+    if v < 0:
+        raise DictMergeError(v, "dm_get_tuning")
+    return v
+
+
+class tuning:
+    """Context manager: set a knob, restore its previous value on exit (the knobs
+    are process-wide)."""
+
+    def __init__(self, knob: int, value: int):
+        self.knob, self.value, self.old = knob, value, None
+
+    def __enter__(self):
+        self.old = get_tuning(self.knob)
+        set_tuning(self.knob, self.value)
+        return self
+
+    def __exit__(self, *exc):
+        set_tuning(self.knob, self.old)
+        return False
 
 
 def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
@@ -325,8 +386,8 @@ class TableMerger:
     through ``dm_merge_table_async``: one call launches every column on the
     library's stream pool; graph-capturable like ColumnMerger."""
 
-    def __init__(self, columns: Sequence[tuple]):
-        self.ms = [ColumnMerger(*c) for c in columns]
+    def __init__(self, columns: Sequence[tuple], *, x_tables: bool = False):
+        self.ms = [ColumnMerger(*c, x_tables=x_tables) for c in columns]
         n = len(self.ms)
         self.n = n
         self.ins = (_In * n)(*[m.cin for m in self.ms])
@@ -469,15 +530,23 @@ def xc_exceptions_gather(xc: XcTables, dict_len: int, x_main: torch.Tensor, stre
     """X_M slices of XC's flagged superblocks -> (ids int32, slices int32, count)."""
     dev = x_main.device
     sb = 4 << xc.shift
-    ids = torch.empty(max(xc.n_records, 1), dtype=torch.int32, device=dev)
-    slices = torch.empty(max(xc.n_records * sb, 1), dtype=torch.int32, device=dev)
     cnt = torch.zeros(2, dtype=torch.int64, device=dev)
-    st = _lib().dm_xc_exceptions_gather(ctypes.byref(xc.struct()), dict_len, _ptr(x_main), ids.data_ptr(),
-                                        slices.data_ptr(), cnt.data_ptr(), _stream_handle(stream))
+    # count first (ids = slices = NULL), then size the buffers by the count: the
+    # flagged superblocks are rare, a worst-case buffer would be X_M-sized
+    st = _lib().dm_xc_exceptions_gather(ctypes.byref(xc.struct()), dict_len, _ptr(x_main), None, None,
+                                        cnt.data_ptr(), _stream_handle(stream))
     if st != Status.OK:
         raise DictMergeError(st, "dm_xc_exceptions_gather")
     n = int(cnt[0].item())
-    return ids[:max(n, 1)], slices[: max(n * sb, 1)], n
+    ids = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    slices = torch.empty(max(n * sb, 1), dtype=torch.int32, device=dev)
+    if n:
+        cnt.zero_()
+        st = _lib().dm_xc_exceptions_gather(ctypes.byref(xc.struct()), dict_len, _ptr(x_main), ids.data_ptr(),
+                                            slices.data_ptr(), cnt.data_ptr(), _stream_handle(stream))
+        if st != Status.OK:
+            raise DictMergeError(st, "dm_xc_exceptions_gather")
+    return ids, slices, n
 
 
 def xc_exceptions_scatter(xc: XcTables, dict_len: int, ids: torch.Tensor, slices: torch.Tensor, count: int,
@@ -565,3 +634,141 @@ class HostContext:
         if st != Status.OK:
             raise DictMergeError(st, "dm_merge_column_host")
         return int(cout.merged_dict_len), int(cout.merged_bits), int(cout.delta_dict_len)
+
+
+# ------------------------------------------------------------------ sharded merge
+def plan_row_shards(n_main: int, n_delta: int, nranks: int) -> list:
+    """dm_plan_row_shards: output-row cuts [0, ..., N'] (every cut but the last a
+    multiple of 4096) -- rank g owns rows [cuts[g], cuts[g+1])."""
+    cuts = (ctypes.c_uint64 * (nranks + 1))()
+    _lib().dm_plan_row_shards(n_main, n_delta, nranks, cuts)
+    return [int(c) for c in cuts]
+
+
+def sharded_codes_cap_words(dict_len: int, n_main: int, n_delta: int, nranks: int, rank: int) -> int:
+    return int(_lib().dm_sharded_codes_cap_words(dict_len, n_main, n_delta, nranks, rank))
+
+
+class Comm:
+    """dm_comm: the transport of a sharded merge.  ``Comm.nccl()`` -- NCCL over
+    NVLink (the library resolves NCCL from the process; the unique id travels over
+    the torch.distributed default group); ``Comm.callbacks()`` -- host-buffer
+    callbacks over a torch.distributed process group (gloo on the CPU: the
+    multi-process tests; the library stages device data through pinned memory)."""
+
+    def __init__(self, handle, keep=None):
+        if not handle:
+            raise DictMergeError(Status.E_NCCL, "dm_comm_init")
+        self.h = handle
+        self._keep = keep
+
+    @property
+    def rank(self) -> int:
+        return int(_lib().dm_comm_rank(self.h))
+
+    @property
+    def size(self) -> int:
+        return int(_lib().dm_comm_size(self.h))
+
+    @classmethod
+    def nccl(cls, group=None, device: Optional[int] = None) -> "Comm":
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        uid = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            st = _lib().dm_comm_nccl_unique_id(uid.data_ptr())
+            if st != Status.OK:
+                raise DictMergeError(st, "dm_comm_nccl_unique_id")
+        dev = torch.cuda.current_device() if device is None else device
+        # the id over the process group (NCCL groups need a CUDA tensor)
+        t = uid.cuda(dev) if dist.get_backend(group) == "nccl" else uid
+        dist.broadcast(t, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        uid = t.cpu()
+        return cls(_lib().dm_comm_init_nccl(uid.data_ptr(), world, rank, dev))
+
+    @classmethod
+    def callbacks(cls, group=None) -> "Comm":
+        import numpy as np
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        glob = (lambda r: dist.get_global_rank(group, r)) if group is not None else (lambda r: r)
+
+        def view(ptr, n):
+            return torch.from_numpy(np.ctypeslib.as_array((ctypes.c_uint8 * n).from_address(ptr)))
+
+        def bcast(buf, n, root, _user):
+            try:
+                t = view(buf, n)
+                dist.broadcast(t, src=glob(root), group=group)
+                return 0
+            except Exception:  # noqa: BLE001 -- reported to the library as a transport failure
+                return 1
+
+        def agather(send, recv, n, _user):
+            try:
+                out = [torch.empty(n, dtype=torch.uint8) for _ in range(world)]
+                dist.all_gather(out, view(send, n).clone(), group=group)
+                view(recv, n * world).copy_(torch.cat(out))
+                return 0
+            except Exception:  # noqa: BLE001
+                return 1
+
+        def sendrecv(buf, n, peer, is_send, _user):
+            try:
+                t = view(buf, n)
+                if is_send:
+                    dist.send(t.clone(), dst=glob(peer), group=group)
+                else:
+                    dist.recv(t, src=glob(peer), group=group)
+                return 0
+            except Exception:  # noqa: BLE001
+                return 1
+
+        cbs = _Cbs(_CB_BCAST(bcast), _CB_AGATHER(agather), _CB_SENDRECV(sendrecv), None)
+        return cls(_lib().dm_comm_init_callbacks(ctypes.byref(cbs), world, rank), keep=cbs)
+
+    def selftest_host(self) -> int:
+        return int(_lib().dm_comm_selftest_host(self.h))
+
+    def close(self):
+        if self.h:
+            _lib().dm_comm_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+
+@dataclasses.dataclass
+class ShardedResult:
+    merged_codes: torch.Tensor           # this rank's M' words (rows [cuts[g], cuts[g+1]) at b')
+    merged_bits: int                     # b'
+    merged_len: int                      # |U'|
+    merged_dict: Optional[torch.Tensor]  # U' on the root, else None
+    row_begin: int
+    row_end: int
+
+
+def merge_column_sharded(comm: Comm, main_codes_shard: torch.Tensor, n_main: int, main_bits: int, dict_len: int,
+                         n_delta: int, *, main_dict: Optional[torch.Tensor] = None,
+                         delta: Optional[torch.Tensor] = None, key: str = "u64", tables: str = "xc",
+                         root: int = 0, stream=None) -> ShardedResult:
+    """dm_merge_column_sharded: this rank's part of one column's merge (collective).
+    ``main_codes_shard``: the packed main codes of this rank's main rows
+    (plan_row_shards); the root also passes U_M (``main_dict``) and D (``delta``)."""
+    nr, me = comm.size, comm.rank
+    cuts = plan_row_shards(n_main, n_delta, nr)
+    dev = main_codes_shard.device if main_codes_shard is not None else torch.device("cuda", torch.cuda.current_device())
+    cap = sharded_codes_cap_words(dict_len, n_main, n_delta, nr, me)
+    out_codes = torch.empty(max(cap, 2), dtype=torch.int64, device=dev)
+    U = _empty_keys(_KEY[key], dict_len + n_delta, dev) if me == root else None
+    cin = _ShIn(_KEY[key], 0 if tables == "xc" else 1, root, _ptr(main_dict) if me == root else None, dict_len,
+                _ptr(delta) if me == root else None, n_delta, _ptr(main_codes_shard), n_main, main_bits)
+    cout = _ShOut(_ptr(U), dict_len + n_delta if U is not None else 0, out_codes.data_ptr(), out_codes.numel(), 0, 0)
+    st = _lib().dm_merge_column_sharded(comm.h, ctypes.byref(cin), ctypes.byref(cout), _stream_handle(stream))
+    if st != Status.OK:
+        raise DictMergeError(st, "dm_merge_column_sharded")
+    nb = int(cout.merged_bits)
+    r0, r1 = cuts[me], cuts[me + 1]
+    nw = (r1 * nb + 63) // 64 - r0 * nb // 64
+    return ShardedResult(out_codes[:nw], nb, int(cout.merged_dict_len),
+                         U[: cout.merged_dict_len] if U is not None else None, r0, r1)

@@ -617,6 +617,214 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge(const void* __restrict_
   }
 }
 
+// ------------------------------------------------- sparse deltas: U_M tiles
+// When U_D is much smaller than U_M (cfg2: 1e6 vs 1e7; cfg5: 5e7 vs 1.07e9),
+// the merge is a copy of U_M with a few insertions.  Tile over U_M alone: tile
+// t = U_M[a, a + T) and the U_D values in [U_M[a], U_M[a + T)) (its "slice",
+// found by k_sp_partition; the first tile also takes the values below U_M[0],
+// the last the values above U_M[N-1]).  The paper's merge then
+// reduces, per tile, to:
+//   p_j   = #{tile U_M < B[j]} (binary search in the staged tile), found_j =
+//           U_M[a + p_j] == B[j] (a duplicate: appended once);
+//   cnt[p] = #{new j : p_j = p}, shift(i) = sum_{p <= i} cnt[p];
+//   E_t   = #{new values in earlier tiles} (decoupled look-back: the paper's
+//           counts + prefix sum, one pass);
+//   U_M[a+i] -> U'[a + E_t + i + shift(i)] = X_M[a+i];
+//   new B[j] -> U'[a + E_t + p_j + newrank_j] = X_D[j] (newrank_j = new values
+//           of the slice before j); a duplicate takes its twin's X_M.
+// One read of U_M and U_D, one write of U' (+ X_M when wanted), X_D and the XC
+// inputs -- the streaming bound -- instead of ranking both sides of every
+// merge-path tile twice.
+constexpr uint32_t kSpTile = 2048, kSpThreads = 256, kSpItems = kSpTile / kSpThreads, kSpChunk = 2048;
+
+template <class KT>
+__global__ void __launch_bounds__(256) k_sp_partition(const void* __restrict__ A, uint64_t nA,
+                                                      const void* __restrict__ B, const dm_header* __restrict__ hdr,
+                                                      uint64_t ntiles, uint64_t* __restrict__ part) {
+  pdl_prologue();
+  const uint64_t t = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const unsigned lane = lane_id();
+  if (t > ntiles) return;
+  const uint64_t nB = hdr->delta_dict_len;
+  if (t == 0 || t == ntiles) {
+    if (lane == 0) part[t] = t == 0 ? 0 : nB;
+    return;
+  }
+  const auto v = KT::load(A, t * kSpTile);
+  uint64_t lo = 0, hi = nB;  // lower bound of v in B, 32 probes per round
+  while (hi > lo) {
+    const uint64_t span = hi - lo;
+    const uint64_t ik = lo + span * lane / 32;
+    const bool cond = KT::lt(KT::load(B, ik), v);
+    const unsigned c = __popc(__ballot_sync(FULL, cond));
+    const uint64_t nlo = c ? lo + span * (c - 1) / 32 + 1 : lo;
+    const uint64_t nhi = c < 32 ? lo + span * c / 32 : hi;
+    lo = nlo;
+    hi = nhi;
+  }
+  if (lane == 0) part[t] = lo;
+}
+
+template <class KT>
+__global__ void __launch_bounds__(kSpThreads) k_sp_merge(const void* __restrict__ A, uint64_t nA,
+                                                         const void* __restrict__ B,
+                                                         const uint64_t* __restrict__ part, uint64_t ntiles,
+                                                         uint64_t* status, uint32_t* counter, void* __restrict__ U,
+                                                         uint32_t* __restrict__ XM, uint32_t* __restrict__ XD,
+                                                         dm_header* hdr, uint32_t* __restrict__ rblk,
+                                                         uint8_t* __restrict__ offs, uint32_t xs) {
+  pdl_prologue();
+  using K = typename KT::K;
+  constexpr uint32_t T = kSpTile, NT = kSpThreads, IT = kSpItems, C = kSpChunk;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  K* sk = reinterpret_cast<K*>(smem_raw);           // [0] = A[a - 1], then the tile
+  K* sv = sk + (T + 1);                             // slice chunk values
+  uint32_t* sp = reinterpret_cast<uint32_t*>(sv + C);  // p_j | found << 31
+  uint32_t* scnt = sp + C;                          // cnt[p], then inclusive shift(i); [T + 1]
+  __shared__ uint32_t s_warp[NT / 32 + 1];
+  __shared__ uint32_t s_tile;
+  __shared__ uint64_t s_E;
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);  // in launch order: look-back predecessors run first
+  __syncthreads();
+  const uint64_t t = s_tile;
+  if (t >= ntiles) return;
+  const uint64_t a = t * T;
+  const uint32_t na = (uint32_t)umin64(T, nA - a);
+  const uint64_t lo = part[t], hi = part[t + 1];
+  const uint64_t nb = hi - lo;
+  const bool has_prev = a > 0;
+  // stage the tile, zero the counts
+#pragma unroll
+  for (uint32_t r = 0; r < IT; ++r) {
+    const uint32_t i = threadIdx.x + r * NT;
+    if (i < na) sk[1 + i] = KT::load(A, a + i);
+  }
+  if (threadIdx.x == 0 && has_prev) sk[0] = KT::load(A, a - 1);
+  for (uint32_t i = threadIdx.x; i <= T; i += NT) scnt[i] = 0;
+  __syncthreads();
+  auto rank_in_tile = [&](const K& v, uint32_t& p, bool& found) {
+    uint32_t l = 0, h = na;  // #{tile A < v}
+    while (l < h) {
+      const uint32_t m = (l + h) >> 1;
+      if (KT::lt(sk[1 + m], v)) l = m + 1; else h = m;
+    }
+    p = l;
+    found = l < na && KT::eq(sk[1 + l], v);
+  };
+  // pass 1: rank the slice, count the new values per insertion position
+  const bool one_chunk = nb <= C;
+  for (uint64_t c0 = 0; c0 < nb; c0 += C) {
+    const uint32_t cn = (uint32_t)umin64(C, nb - c0);
+    for (uint32_t j = threadIdx.x; j < cn; j += NT) sv[j] = KT::load(B, lo + c0 + j);
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < cn; j += NT) {
+      uint32_t p;
+      bool f;
+      rank_in_tile(sv[j], p, f);
+      if (!f) atomicAdd(&scnt[p], 1u);
+      sp[j] = p | (f ? 0x80000000u : 0u);
+    }
+    __syncthreads();
+  }
+  // inclusive prefix over positions [0, na); n_t adds the values past the tile's end (p = na)
+  uint32_t n_t;
+  {
+    const uint32_t i0 = threadIdx.x * IT;
+    uint32_t v[IT], sum = 0;
+#pragma unroll
+    for (uint32_t r = 0; r < IT; ++r) {
+      v[r] = i0 + r < na ? scnt[i0 + r] : 0u;
+      sum += v[r];
+    }
+    const uint32_t tail = scnt[na];
+    uint32_t tot;
+    uint32_t run = block_exclusive_scan<NT>(sum, s_warp, tot);
+#pragma unroll
+    for (uint32_t r = 0; r < IT; ++r) {
+      run += v[r];
+      if (i0 + r < na) scnt[i0 + r] = run;
+    }
+    n_t = tot + tail;
+  }
+  if (warp == 0) {
+    const uint64_t e = lookback_exclusive(status, t, n_t);
+    if (lane == 0) s_E = e;
+  }
+  __syncthreads();
+  const uint64_t E = s_E;
+  const uint64_t base = a + E;  // U' index of the tile's first U_M element, before insertions
+  const uint32_t bmask = (1u << xs) - 1;
+  // U_M elements: copy with gaps
+  bool unsorted = false;
+#pragma unroll
+  for (uint32_t r = 0; r < IT; ++r) {
+    const uint32_t i = threadIdx.x + r * NT;
+    if (i >= na) break;
+    const uint32_t sh = scnt[i];
+    const uint64_t out = base + i + sh;
+    const K v = sk[1 + i];
+    KT::store(U, out, v);
+    if (XM) XM[a + i] = (uint32_t)out;
+    if (rblk) {  // XC block samples R(g) = X_M[2^xs g] - 2^xs g
+      if (((a + i) & bmask) == 0) rblk[(a + i) >> xs] = (uint32_t)(E + sh);
+      if (a + i == nA - 1) rblk[(nA + bmask) >> xs] = (uint32_t)(E + sh);
+    }
+    if ((i > 0 || has_prev) && !KT::lt(sk[i], v)) unsorted = true;
+  }
+  if (__any_sync(FULL, unsorted) && lane == 0) atomicMin(&hdr->status, (int)DM_E_UNSORTED);
+  // pass 2: the slice -- new values into their slots, X_D for all
+  uint32_t run_new = 0;
+  for (uint64_t c0 = 0; c0 < nb; c0 += C) {
+    const uint32_t cn = (uint32_t)umin64(C, nb - c0);
+    if (!one_chunk) {
+      __syncthreads();
+      for (uint32_t j = threadIdx.x; j < cn; j += NT) {
+        sv[j] = KT::load(B, lo + c0 + j);
+      }
+      __syncthreads();
+      for (uint32_t j = threadIdx.x; j < cn; j += NT) {
+        uint32_t p;
+        bool f;
+        rank_in_tile(sv[j], p, f);
+        sp[j] = p | (f ? 0x80000000u : 0u);
+      }
+      __syncthreads();
+    }
+    // blocked: thread k owns chunk entries [k IT', (k + 1) IT') for the new-rank scan
+    constexpr uint32_t JT = C / NT;
+    const uint32_t j0 = threadIdx.x * JT;
+    uint32_t cntn = 0;
+#pragma unroll
+    for (uint32_t r = 0; r < JT; ++r)
+      if (j0 + r < cn && !(sp[j0 + r] >> 31)) ++cntn;
+    uint32_t tot;
+    uint32_t nr = run_new + block_exclusive_scan<NT>(cntn, s_warp, tot);
+#pragma unroll
+    for (uint32_t r = 0; r < JT; ++r) {
+      const uint32_t j = j0 + r;
+      if (j >= cn) break;
+      const uint32_t w = sp[j], p = w & 0x7fffffffu;
+      if (w >> 31) {  // duplicate: its U_M twin's index
+        XD[lo + c0 + j] = (uint32_t)(base + p + scnt[p]);
+      } else {
+        const uint64_t u = base + p + nr;
+        KT::store(U, u, sv[j]);
+        XD[lo + c0 + j] = (uint32_t)u;
+        if (offs) offs[E + nr] = (uint8_t)((a + p - 1) & bmask);
+        ++nr;
+      }
+    }
+    run_new += tot;
+  }
+  if (t == ntiles - 1 && threadIdx.x == 0) {
+    const uint64_t m = nA + E + n_t;
+    hdr->merged_dict_len = m;
+    hdr->merged_bits = dev_width(m);
+    if (m > (1ull << 32)) atomicMin(&hdr->status, (int)DM_E_TOO_WIDE);
+  }
+}
+
 // XC superblock records (NEXT3) from the block samples R(g) = rblk[g]:
 // {R(4s) | flag << 31, cum bytes 0..3}, cum[t] = R(4s+t+1) - R(4s).  Flag = the
 // counts do not fit a byte, or one block holds more than kXcMaxBlock
@@ -690,6 +898,7 @@ __global__ void __launch_bounds__(256) k_xc_exceptions(bool gather, const uint2*
       if (!(rec[w].x >> 31)) continue;
       unsigned long long sl = 0;
       if (lane == 0) sl = atomicAdd(d_count, 1ull);
+      if (!slices) continue;  // count only (the caller sizes the slices from the count)
       slot = __shfl_sync(FULL, sl, 0);
       sb = w;
       if (lane == 0) ids[slot] = (uint32_t)sb;
@@ -735,15 +944,24 @@ cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, const void*
   uint64_t* excl = reinterpret_cast<uint64_t*>(ws + L.mexcl);
   uint64_t* status = reinterpret_cast<uint64_t*>(ws + L.status_merge);
   uint32_t* counter = reinterpret_cast<uint32_t*>(ws + L.counters) + CNT_MERGE;
-  const int variant = tuning(1);
+  const int variant = sp_wanted(in) ? 3 : tuning(1) == 3 ? 0 : tuning(1);
   // X_M need not be materialised when nobody asked for it and Step 2(b) will
   // read XC from L2 (that kernel falls back to X_M on flagged superblocks only,
   // filled by k_xm_flagged): cfg5 skips 4.3 GB of writes
   const int xknob = tuning(0);
-  const bool skip_xm = xc && !force_xc && !xm_requested && (variant == 0 || variant == 2) &&
+  const bool skip_xm = xc && !force_xc && !xm_requested && (variant == 0 || variant == 2 || variant == 3) &&
                        (xknob == 2 || xknob == 3 || (xknob == 0 && in->dict_len * 4 > kXcGlobalMinBytes));
   uint32_t* xm_w = skip_xm ? nullptr : xm;
-  if (variant == 0 || variant == 2) {  // lean tiles: two passes (default) or single pass
+  if (variant == 3) {  // sparse deltas: U_M tiles with their U_D slices, one pass (sp_wanted)
+    const uint64_t ntiles = (in->dict_len + kSpTile - 1) / kSpTile;
+    launch_k(k_sp_partition<KT>, (unsigned)((ntiles + 1 + 7) / 8), 256, 0, st, in->main_dict, in->dict_len, udict, hdr,
+                                                                        ntiles, part);
+    const size_t smem = sizeof(K) * (kSpTile + 1 + kSpChunk) + sizeof(uint32_t) * (kSpChunk + kSpTile + 1);
+    ensure_smem((const void*)k_sp_merge<KT>, true);
+    launch_k(k_sp_merge<KT>, (unsigned)ntiles, kSpThreads, smem, st, in->main_dict, in->dict_len, udict, part, ntiles,
+                                                                status, counter, U, xm_w, xd, hdr, rblk, offs, xs);
+    note_launch(2);
+  } else if (variant == 0 || variant == 2) {  // lean tiles: two passes (default) or single pass
     launch_k(k_partition<KT>, (unsigned)((nt + 1 + 7) / 8), 256, 0, st, in->main_dict, in->dict_len, udict, hdr, nt + 1,
                                                                      part);
     const size_t smem = sizeof(K) * (kMergeTile + 1) + sizeof(uint32_t) * (3 * kMergeTile + 1);

@@ -200,6 +200,12 @@ static dm_status cuda_fail(cudaError_t e) {
 }
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+// Main codes index a dictionary: with N_M > 0, 1 <= |U_M| < 2^32 and b >= width(|U_M|)
+// (the recompress kernels clamp codes to |U_M| - 1, so |U_M| = 0 must not reach them).
+static bool main_dict_len_ok(uint64_t n_main, uint64_t dict_len, uint32_t main_bits) {
+  if (n_main == 0) return dict_len < (1ull << 32);
+  return dict_len >= 1 && dict_len < (1ull << 32) && main_bits >= host_width(dict_len);
+}
 
 // What one call runs: the whole merge, Steps 1(a)-2(a), Step 1(a) alone, or
 // Steps 1(b)-2(a) on a delta that already is U_D (sorted, distinct).
@@ -300,10 +306,14 @@ static dm_status merge_async(const dm_column_in* in, const dm_column_out* out, v
 }
 
 // Per-device pool of non-blocking streams used by dm_merge_table.
+// One caller at a time forks / joins a pool (`mu`): the fork and join events
+// are shared, so two host threads (or interleaved captures) on one device must
+// not interleave their record / wait pairs.
 struct StreamPool {
   std::vector<cudaStream_t> streams;
   std::vector<cudaEvent_t> join;
   cudaEvent_t fork = nullptr;
+  std::mutex mu;
 };
 // Stream-pool size for dm_merge_table (DM_TABLE_STREAMS overrides; experiments).
 static int table_streams() {
@@ -377,12 +387,14 @@ struct dm_ctx {
 extern "C" {
 
 int dm_set_tuning(int knob, int value) {
-  static const int hi[6] = {3, 2, 2, 1, 8, 2};
+  static const int hi[6] = {3, 3, 2, 1, 8, 2};
   if (knob < 0 || knob > 5 || value < 0 || value > hi[knob]) return DM_E_INVALID;
   if (knob == 4 && value != 0 && value != 7 && value != 8) return DM_E_INVALID;
   g_tuning[knob].store(value);
   return DM_OK;
 }
+
+int dm_get_tuning(int knob) { return (knob >= 0 && knob < 6) ? tuning(knob) : DM_E_INVALID; }
 
 uint32_t dm_width(uint64_t n) { return host_width(n); }
 uint64_t dm_words(uint64_t n, uint32_t bits) { return host_words(n, bits); }
@@ -470,19 +482,24 @@ dm_status dm_merge_table_async(int ncols, const dm_column_in* in, const dm_colum
     return in[a].n_main + in[a].n_delta > in[b].n_main + in[b].n_delta;
   });
   StreamPool& pool = stream_pool();
+  std::lock_guard<std::mutex> lk(pool.mu);
   const int K = std::max(1, std::min<int>(ncols, (int)pool.streams.size()));
   cudaError_t e = cudaEventRecord(pool.fork, st);
   for (int k = 0; k < K && e == cudaSuccess; ++k) e = cudaStreamWaitEvent(pool.streams[k], pool.fork, 0);
   if (e != cudaSuccess) return cuda_fail(e);
-  for (int t = 0; t < ncols; ++t) {
+  dm_status bad = DM_OK;
+  for (int t = 0; t < ncols && bad == DM_OK; ++t) {
     const int c = order[t];
-    dm_status s = merge_async(&in[c], &out[c], ws[c], ws_bytes[c], hdrs[c], pool.streams[t % K], true);
-    if (s != DM_OK) return s;
+    bad = merge_async(&in[c], &out[c], ws[c], ws_bytes[c], hdrs[c], pool.streams[t % K], true);
   }
-  for (int k = 0; k < K && e == cudaSuccess; ++k) {
-    e = cudaEventRecord(pool.join[k], pool.streams[k]);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, pool.join[k], 0);
+  // always join every forked stream back (an active graph capture must not end
+  // with forked streams, even when a column failed to launch)
+  for (int k = 0; k < K; ++k) {
+    cudaError_t j = cudaEventRecord(pool.join[k], pool.streams[k]);
+    if (j == cudaSuccess) j = cudaStreamWaitEvent(st, pool.join[k], 0);
+    if (e == cudaSuccess) e = j;
   }
+  if (bad != DM_OK) return bad;
   return e == cudaSuccess ? DM_OK : cuda_fail(e);
 }
 
@@ -529,6 +546,7 @@ dm_status dm_recompress(const uint64_t* main_codes, uint64_t n_main, uint32_t ma
                         uint64_t n_delta, uint32_t new_bits, uint64_t* out_codes, uint64_t out_cap_words,
                         void* cuda_stream) {
   if (main_bits < 1 || main_bits > 32 || new_bits < 1 || new_bits > 32) return DM_E_INVALID;
+  if (!main_dict_len_ok(n_main, dict_len, main_bits)) return DM_E_INVALID;
   if (n_main && (!main_codes || !x_main || !aligned16(main_codes))) return DM_E_INVALID;
   if (n_delta && (!x_delta || !delta_rank)) return DM_E_INVALID;
   const uint64_t need = host_words(n_main + n_delta, new_bits);
@@ -576,7 +594,8 @@ dm_status dm_xc_export(const dm_column_in* in, const void* ws, size_t ws_bytes, 
 dm_status dm_xc_exceptions_gather(const dm_xc* xc, uint64_t dict_len, const uint32_t* x_main, uint32_t* ids,
                                   uint32_t* slices, uint64_t* d_count, void* cuda_stream) {
   if (!xc || !xc->records || (xc->shift != 7 && xc->shift != 8) || !d_count) return DM_E_INVALID;
-  if (xc->n_records && (!x_main || !ids || !slices)) return DM_E_INVALID;
+  if ((ids == nullptr) != (slices == nullptr)) return DM_E_INVALID;  // both NULL: count only
+  if (xc->n_records && slices && !x_main) return DM_E_INVALID;
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
   cudaError_t e = cudaMemsetAsync(d_count, 0, sizeof(uint64_t), st);
   if (e == cudaSuccess)
@@ -601,6 +620,7 @@ dm_status dm_recompress_xc(const uint64_t* main_codes, uint64_t n_main, uint32_t
                            const uint32_t* delta_rank, uint64_t n_delta, uint32_t new_bits, uint64_t* out_codes,
                            uint64_t out_cap_words, void* cuda_stream) {
   if (main_bits < 1 || main_bits > 32 || new_bits < 1 || new_bits > 32) return DM_E_INVALID;
+  if (!main_dict_len_ok(n_main, dict_len, main_bits)) return DM_E_INVALID;
   if (!xc || !xc->built || (xc->shift != 7 && xc->shift != 8)) return DM_E_INVALID;
   if (xc->n_records != xc_nsb(dict_len, xc->shift)) return DM_E_INVALID;
   if (n_main && (!main_codes || !x_main || !xc->records || !xc->offsets || !aligned16(main_codes) ||
@@ -676,6 +696,27 @@ void dm_ctx_destroy(dm_ctx* c) {
   delete c;
 }
 
+// dm_merge_column_host's checks of the caller's HOST buffers: the same argument
+// rules as the device entry points (validate), minus alignment, and output
+// capacities that fit every possible result.
+static dm_status validate_host(const dm_column_in* in, const dm_column_out* out) {
+  if (in->key != DM_KEY_U64 && in->key != DM_KEY_B16 && in->key != DM_KEY_U32) return DM_E_INVALID;
+  if (in->main_bits < 1 || in->main_bits > 32) return DM_E_INVALID;
+  if (in->dict_len >= (1ull << 32) || in->n_delta >= (1ull << 30)) return DM_E_INVALID;
+  if (!main_dict_len_ok(in->n_main, in->dict_len, in->main_bits)) return DM_E_INVALID;
+  if (in->dict_len && !in->main_dict) return DM_E_INVALID;
+  if (in->n_main && !in->main_codes) return DM_E_INVALID;
+  if (in->n_delta && !in->delta) return DM_E_INVALID;
+  const uint64_t dict_cap = in->dict_len + in->n_delta;
+  if (dict_cap > (1ull << 32)) return DM_E_TOO_WIDE;
+  if (dict_cap && !out->merged_dict) return DM_E_INVALID;
+  if (out->merged_dict_cap < dict_cap) return DM_E_CAPACITY;
+  const uint64_t need_words = dm_merged_codes_cap_words(in);
+  if (need_words && !out->merged_codes) return DM_E_INVALID;
+  if (out->merged_codes_cap_words < need_words) return DM_E_CAPACITY;
+  return DM_OK;
+}
+
 dm_status dm_merge_column_host(dm_ctx* c, const dm_column_in* hin, dm_column_out* hout) {
   // A three-stream pipeline (copy-in, compute, copy-out; B200 has separate copy
   // engines per direction, PCIe is full duplex):
@@ -687,6 +728,10 @@ dm_status dm_merge_column_host(dm_ctx* c, const dm_column_in* hin, dm_column_out
   // P:324), so the main-code upload overlaps Step 1 and the M' download
   // overlaps the remaining uploads.  One host wait: for b' after Step 2(a).
   if (!c || !hin || !hout) return DM_E_INVALID;
+  {  // the host buffers: inputs present, outputs present and large enough (before any copy)
+    dm_status v = validate_host(hin, hout);
+    if (v != DM_OK) return v;
+  }
   cudaSetDevice(c->impl.device);
   auto& I = c->impl;
   cudaStream_t st = I.stream, sin = I.s_in, sout = I.s_out;
@@ -768,6 +813,10 @@ dm_status dm_merge_column_host(dm_ctx* c, const dm_column_in* hin, dm_column_out
     return (dm_status)h.status;
   }
   const uint32_t nb = h.merged_bits;
+  const bool xc_on = din.dict_len > 0;  // MM_DICT builds XC whenever |U_M| > 0 (force_xc)
+  const uint2* xc_rec = xc_on ? reinterpret_cast<const uint2*>(static_cast<char*>(ws) + L.xc_rec) : nullptr;
+  const uint8_t* xc_offs = xc_on ? reinterpret_cast<const uint8_t*>(static_cast<char*>(ws) + L.xc_offs) : nullptr;
+  const uint32_t xs = xc_shift(&din);
   // 3. U' and the requested tables go out while M is still coming in
   wait(sout, EV_S1);
   d2h(hout->merged_dict, dout.merged_dict, h.merged_dict_len * E);
@@ -791,7 +840,10 @@ dm_status dm_merge_column_host(dm_ctx* c, const dm_column_in* hin, dm_column_out
     dm_column_out cout{};
     cout.merged_codes = dout.merged_codes + r0 * nb / 64;
     cout.merged_codes_cap_words = host_words(r1, nb) - r0 * nb / 64;
-    if (e == cudaSuccess) e = launch_recompress(&cin, &cout, xm, xd, rk + d0, d_hdr, st, nb);
+    // the same translation-table placement as the device entry point: the
+    // dictionary merge built XC (force_xc) whenever the plain X_M is too big
+    // for shared memory, so each chunk may read it from shared memory or L2
+    if (e == cudaSuccess) e = launch_recompress(&cin, &cout, xm, xd, rk + d0, d_hdr, st, nb, xc_rec, xc_offs, xs);
     rec(EV_IN0 + K + k, st);
     wait(sout, EV_IN0 + K + k);
     d2h(hout->merged_codes + r0 * nb / 64, cout.merged_codes, cout.merged_codes_cap_words * 8);

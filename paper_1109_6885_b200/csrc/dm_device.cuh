@@ -282,6 +282,20 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s
 
 // ------------------------------------------------------------------ TMA / mbarrier
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// Shared-memory loads by 32-bit shared address; the predicated form compiles to
+// one predicated LDS (no branch) and yields 0 when `pred` is false.  Only for
+// data that is read-only after a barrier (the address depends on loaded data,
+// so the compiler cannot hoist these above the barrier).
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u32_if(uint32_t a, bool pred) {
+  uint32_t v = 0;
+  asm("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.shared.u32 %0, [%1];\n}" : "+r"(v) : "r"(a), "r"((uint32_t)pred));
+  return v;
+}
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
@@ -307,6 +321,21 @@ __device__ __forceinline__ bool mbar_try_wait_parity(uint64_t* bar, uint32_t par
 __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait_parity(bar, parity)) {
   }
+}
+// As mbar_wait_parity, with a suspend-time hint: the thread sleeps in the
+// try_wait until the phase completes or ~`ns` elapse, instead of re-issuing
+// it (each retry costs issue slots the streaming kernels need).
+__device__ __forceinline__ void mbar_wait_parity_sleep(uint64_t* bar, uint32_t parity, uint32_t ns = 20000) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, P;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(ns)
+        : "memory");
+  } while (!ok);
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");

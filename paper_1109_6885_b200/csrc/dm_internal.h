@@ -26,6 +26,7 @@ constexpr int kRecThreads = 32 * (kRecConsumerWarps + 1);  // + one TMA producer
 constexpr int kRecGroups = 128;                          // 32-row groups per chunk (4096 rows)
 constexpr int kRecStages = 4;                            // TMA input ring depth
 constexpr uint32_t kRecSmemXBytes = 96 * 1024;           // X_M staged in shared memory up to this size
+constexpr int kRecHdrBytes = 256;                        // recompress smem head: mbarriers + XC mask table
 constexpr int kRecStagesXc = 4;                          // ring depth when the compact X_M takes the smem
 
 // Compact translation table "XC": X_M[c] = c + #{new values
@@ -102,6 +103,15 @@ inline uint32_t xc_shift(const dm_column_in* in) {
   if (const int o = xc_shift_override()) return (uint32_t)o;
   if (tuning(0) == 2 || xc_smem_candidate(in)) return 8;
   return in->n_delta * 256 <= 6 * in->dict_len ? 8u : 7u;
+}
+
+// Step 1(b) sparse-delta tiles (knob 1 = 3, auto when N_D <= |U_M| / 8): U_M
+// tiles of 2048 with the U_D values falling into them (k_sp_merge).  Needs
+// |U_M| > 0; ws status_merge / part hold >= |U_M| / 2048 + 1 entries.
+inline bool sp_wanted(const dm_column_in* in) {
+  const int k = tuning(1);
+  if (in->dict_len == 0) return false;
+  return k == 3 || (k == 0 && in->n_delta * 8 <= in->dict_len);
 }
 
 constexpr uint32_t kRadixFlagAgg = 1u << 30;
@@ -215,10 +225,13 @@ cudaError_t launch_dictionary_merge(const dm_column_in* in, const dm_column_out*
 // Step 2(b): recompress main through X_M and append delta through X_D.
 // fixed_bits != 0: b' given by the caller (dm_recompress); else read from hdr->merged_bits.
 // xc_rec / xc_offs: the compact table (NULL: plain X_M only).
+// rank NULL: delta row k takes xd[k] (the codes themselves).  xc_only: the caller
+// holds XC but not the plain X_M (beyond flagged superblocks): never pick a
+// plain-X_M kernel (requires |U_M| * 4 > kRecSmemXBytes).
 cudaError_t launch_recompress(const dm_column_in* in, const dm_column_out* out, const uint32_t* xm,
                               const uint32_t* xd, const uint32_t* rank, dm_header* hdr, cudaStream_t st,
                               uint32_t fixed_bits = 0, const uint2* xc_rec = nullptr,
-                              const uint8_t* xc_offs = nullptr, uint32_t xc_shift = 8);
+                              const uint8_t* xc_offs = nullptr, uint32_t xc_shift = 8, bool xc_only = false);
 // Step 2(b) of a row shard through XC read from L2 (dm_recompress_xc).
 cudaError_t launch_recompress_xc(const dm_column_in* in, const dm_column_out* out, const uint32_t* xm,
                                  const uint32_t* xd, const uint32_t* rank, dm_header* hdr, cudaStream_t st,

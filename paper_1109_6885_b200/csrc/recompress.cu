@@ -44,19 +44,78 @@ __device__ __forceinline__ uint64_t dwords(uint64_t n, uint32_t bits) { return (
 
 // NB > 0: b' = NB at compile time.  NB <= 0: b' at run time, with at most -NB
 // codes per output word (NB = 0: any width, up to 32).
+// Exact maximum number of b'-bit codes overlapping one 32-bit output word (the
+// pattern repeats every b' words): e.g. 2 for b' = 24, whose code offsets are
+// multiples of 8 (the generic bound (2b' + 30) / b' says 3).
+__host__ __device__ constexpr int pack_tmax(int nb) {
+  int mx = 0;
+  for (int k = 0; k < nb; ++k) {
+    int c = 0;
+    for (int j = 0; j < 32; ++j) c += (j * nb < 32 * k + 32 && (j + 1) * nb > 32 * k) ? 1 : 0;
+    mx = c > mx ? c : mx;
+  }
+  return mx;
+}
 template <int NB>
 __device__ __forceinline__ uint32_t warp_pack(uint32_t v, uint32_t nb, uint32_t r0, uint32_t op) {
-  constexpr int TMAX = NB > 0 ? (2 * NB + 30) / NB : NB < 0 ? -NB : 32;
+  constexpr int TMAX = NB > 0 ? pack_tmax(NB) : NB < 0 ? -NB : 32;
   const int tmax = NB > 0 ? TMAX : (int)((2 * nb + 30) / nb);
   uint32_t word = 0;
+  if constexpr (NB == 0) {  // any width: a rolled loop (unrolling 32 steps behind a break only spills)
+#pragma unroll 1
+    for (int t = 0; t < tmax; ++t) {
+      const uint32_t c = __shfl_sync(FULL, v, (r0 + t) & 31);
+      word |= (t == 0) ? shr32(c, op) : shl32(c, t * nb - op);
+    }
+  } else {
 #pragma unroll
-  for (int t = 0; t < TMAX; ++t) {
-    if (NB <= 0 && t >= tmax) break;
-    const uint32_t c = __shfl_sync(FULL, v, (r0 + t) & 31);
-    word |= (t == 0) ? shr32(c, op) : shl32(c, t * nb - op);
+    for (int t = 0; t < TMAX; ++t) {
+      if (NB <= 0 && t >= tmax) break;
+      const uint32_t c = __shfl_sync(FULL, v, (r0 + t) & 31);
+      word |= (t == 0) ? shr32(c, op) : shl32(c, t * nb - op);
+    }
   }
   return word;
 }
+
+// Warp packing on the FMA pipe (widths with at most 5 codes per output word):
+// the codes overlapping a word occupy disjoint bits, so the word is a SUM of
+// shifted codes, and every shift is by a per-lane constant -- a multiply by a
+// per-lane power of two.  word = hi(c_0 * 2^(32-op)) [op > 0] + c_0 [op = 0]
+// + sum_{t >= 1} c_t * 2^(t b' - op) [t b' - op < 32], all IMAD / IMAD.HI:
+// the ALU pipe, which the lookups saturate, is left alone (B300 microarch
+// notes: ALU and FMA pipes each take one warp instruction per 2 cycles).
+template <int NB>
+struct FmaPack {
+  static constexpr int T = pack_tmax(NB);
+  uint32_t src[T], mul[T], m0hi;
+  __device__ __forceinline__ FmaPack(uint32_t lane) {
+    const uint32_t r0 = (32 * lane) / NB, op = 32 * lane - r0 * NB;
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      src[t] = (r0 + t) & 31;
+      const uint32_t a = t * NB - op;  // t >= 1: shift left by a
+      mul[t] = t == 0 ? (op == 0 ? 1u : 0u) : (a < 32 ? (1u << a) : 0u);
+    }
+    m0hi = op == 0 ? 0u : (1u << (32 - op));
+  }
+  __device__ __forceinline__ uint32_t pack(uint32_t v) const {
+    uint32_t c[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) c[t] = __shfl_sync(FULL, v, src[t]);
+    uint32_t acc = 0;
+#pragma unroll
+    for (int t = 0; t < T; ++t) acc += c[t] * mul[t];
+    uint32_t w;
+    asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(w) : "r"(c[0]), "r"(m0hi), "r"(acc));
+    return w;
+  }
+};
+#ifndef DM_PACK_FMA
+#define DM_PACK_FMA 1
+#endif
+template <int NB>
+__host__ __device__ constexpr bool use_fma_pack() { return DM_PACK_FMA && NB >= 8; }
 
 // Compact X_M lookup (XC, NEXT3; layout in dm_internal.h):
 //   X_M[c] = c + start + #{entries of c's 256-block with offset < c mod 256}
@@ -100,44 +159,118 @@ __device__ __forceinline__ uint32_t bytes_lt_msb(uint32_t x, uint32_t y, uint32_
   return ((~x & y) | (~(x ^ y) & ~z)) & 0x80808080u;
 }
 
-// Lean shared-memory lookup (blocks of 256 codes, xs = 8): one 8-byte record,
-// an 8-byte window of the list read as two (a third, predicated, when the list
-// starts late in a word) conflict-prone shared loads, and a SIMD byte compare.
-// Lists longer than 8 and flagged superblocks take a rare branch: the staging
-// copy rewrites a flagged record as {R, kXcFlagY}, whose byte pattern gives
-// every block a "length" above 8 (no valid record has it: cumulative counts
-// never decrease), so the fast path carries no flag test.  Counts are those of
-// xc_lookup; only the instruction and shared-load budget differ (the kernel is
-// bound by both).
-constexpr uint32_t kXcFlagY = 0x00ff00ffu;
-constexpr uint32_t kXcSmemSlack = 272;  // window reads up to R + 255 + 12 for a rewritten flagged record
-__device__ __forceinline__ uint32_t xc_lookup_smem8(uint32_t code, const uint2* __restrict__ rec,
-                                                    const uint32_t* __restrict__ offs32,
-                                                    const uint32_t* __restrict__ XM) {
-  const uint2 r = rec[code >> 10];
-  const uint32_t t8 = (code >> 5) & 24u;
-  const uint32_t s_rel = ((r.y << 8) >> t8) & 255u, e_rel = (r.y >> t8) & 255u;
-  const uint32_t start = r.x + s_rel;
-  const uint32_t n = e_rel - s_rel;
-  const uint32_t s3 = start & 3u, sh = 8u * s3;
-  const uint32_t* w = offs32 + (start >> 2);
-  DM_ASSERT(n <= kXcMaxBlock || r.y == kXcFlagY, "xc smem list n %u", n);
-  const uint32_t w0 = w[0], w1 = w[1];
-  const uint32_t w2 = n + s3 > 8u ? w[2] : 0u;
+// Shared-memory lookup (blocks of 256 codes, xs = 8).  The staging copy turns
+// every 8-byte superblock record of the global XC into two 4-byte records, one
+// per pair of 256-code blocks (512 codes): bits [0,7) = c1 = entries of the
+// first block, [7,14) = c2 = entries of both blocks, [14,32) = R' = #new values
+// inserted at or before the pair's first code (= the list start of the pair).
+// A 4-byte random shared load costs fewer bank-conflict wavefronts than the
+// 8-byte one, and the list window is read as one word plus two words predicated
+// on the list actually reaching them (~2.6 entries per block on cfg2), so idle
+// lanes take no bank slots.  Lists longer than 8 and flagged superblocks
+// (rewritten as c1 = 127, c2 = 0: n = c2 - c1 wraps, so the fast path needs no
+// flag test) report `slow`; the caller resolves them in one rare pass after all
+// of a warp's lookups (xc4_slow), so the fast path is straight-line code whose
+// loads the compiler can overlap across rows.  Counts are those of xc_lookup.
+#ifndef DM_XC_HYB
+#define DM_XC_HYB 0  // experiments: rows per lane and chunk translated by an L2 gather of X_M instead
+#endif
+constexpr uint32_t kXc4Flag = 127u;      // c1 = 127, c2 = 0: flagged superblock
+constexpr uint32_t kXc4MaxStart = 1u << 18;
+constexpr uint32_t kXcSmemSlack = 272;  // window reads up to start + 11 with start <= n_new + 127
+__device__ __forceinline__ uint32_t xc4_fast(uint32_t code, uint32_t rec4_sa, uint32_t offs_sa, uint32_t& slow) {
+  const uint32_t w = lds_u32(rec4_sa + ((code >> 9) << 2));
+  const bool hi = (code & 256u) != 0u;
+  const uint32_t c1 = w & 127u, c2 = (w >> 7) & 127u;
+  const uint32_t s_rel = hi ? c1 : 0u, e_rel = hi ? c2 : c1;
+  const uint32_t start = (w >> 14) + s_rel;
+  const uint32_t n = e_rel - s_rel;  // wraps (huge) for a flagged record
+  const uint32_t s3 = start & 3u, ns = n + s3;
+  const uint32_t pa = offs_sa + (start & ~3u);
+  const uint32_t w0 = lds_u32(pa);
+  const uint32_t w1 = lds_u32_if(pa + 4, ns > 4u);
+  const uint32_t w2 = lds_u32_if(pa + 8, ns > 8u);
+  const uint32_t sh = 8u * s3;
   const uint32_t a = __funnelshift_r(w0, w1, sh), b = __funnelshift_r(w1, w2, sh);  // bytes [start, start + 8)
   const uint32_t y = (code & 255u) * 0x01010101u, y7 = y & 0x7f7f7f7fu;
   const uint32_t k8 = 8u * umin32(n, 8u);
   const uint32_t ma = ~shl32(0xffffffffu, k8), mb = shr32(0xffffffffu, 64u - k8);
-  uint32_t cnt = __popc(bytes_lt_msb(a, y, y7) & ma) + __popc(bytes_lt_msb(b, y, y7) & mb);
-  if (__builtin_expect(n > 8u, 0)) {
-    if (r.y == kXcFlagY) return __ldg(XM + code);  // flagged superblock: plain X_M
-    const uint32_t o = code & 255u;
-    for (uint32_t q = start + 8; q < start + n; ++q) cnt += ((offs32[q >> 2] >> (8 * (q & 3u))) & 255u) < o ? 1u : 0u;
-  }
-  return code + start + cnt;
+  slow = n > 8u;
+  return code + start + __popc(bytes_lt_msb(a, y, y7) & ma) + __popc(bytes_lt_msb(b, y, y7) & mb);
+}
+// The same lookup rebalanced for the pipes (the kernel is bound by the ALU pipe,
+// ~75% busy, while the FMA pipe idles): shifts by constants become IMAD.HI /
+// IMAD by runtime powers of two (k.m23 = 2^23, k.m18 = 2^18, kept opaque so
+// ptxas cannot turn them back into shifts), the byte masks for the list length
+// come from a 9-entry shared-memory table (one conflict-free LDS.64 instead of
+// four ALU ops), and the window start is formed with adds.
+struct Xc4Consts {
+  uint32_t rec_sa, offs_sa, lut_sa, m23, m18, kpop, four, eight;
+};
+#ifndef DM_POPC_FMA
+#define DM_POPC_FMA 0
+#endif
+__device__ __forceinline__ uint32_t mad_hi(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+__device__ __forceinline__ uint2 lds_u64(uint32_t a) {
+  uint2 v;
+  asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t xc4_fast2(uint32_t code, const Xc4Consts& k, uint32_t& slow) {
+  const uint32_t ridx = __umulhi(code, k.m23);  // code >> 9
+  const uint32_t w = lds_u32(ridx * k.four + k.rec_sa);
+  const bool hi = (code & 256u) != 0u;
+  const uint32_t c1 = w & 127u, c2 = (w >> 7) & 127u;
+  const uint32_t s_rel = hi ? c1 : 0u, e_rel = hi ? c2 : c1;
+  const uint32_t start = mad_hi(w, k.m18, s_rel);  // (w >> 14) + s_rel
+  const uint32_t n = e_rel - s_rel;  // wraps (huge) for a flagged record
+  const uint32_t s3 = start & 3u, ns = n + s3;
+  const uint32_t pa = k.offs_sa + (start - s3);
+  const uint32_t w0 = lds_u32(pa), w1 = lds_u32(pa + 4);
+  const uint32_t w2 = lds_u32_if(pa + 8, ns > 8u);
+  const uint2 m = lds_u64(umin32(n, 8u) * k.eight + k.lut_sa);  // byte-MSB masks of the first min(n, 8) bytes
+  const uint32_t sh = 8u * s3;
+  const uint32_t a = __funnelshift_r(w0, w1, sh), b = __funnelshift_r(w1, w2, sh);  // bytes [start, start + 8)
+  const uint32_t y = __byte_perm(code, 0u, 0u), y7 = y & 0x7f7f7f7fu;
+  const uint32_t za = (a | 0x80808080u) - y7, zb = (b | 0x80808080u) - y7;
+  const uint32_t lta = ((~a & y) | (~(a ^ y) & ~za)) & m.x, ltb = ((~b & y) | (~(b ^ y) & ~zb)) & m.y;
+  slow = n > 8u;
+#if DM_POPC_FMA
+  return code + start + (mad_hi(lta, k.kpop, __umulhi(ltb, k.kpop)) & 255u);
+#else
+  return code + start + __popc(lta) + __popc(ltb);
+#endif
 }
 
-// xs: block shift (blocks of 2^xs codes, superblocks of 4 blocks).
+// The rare case: a list longer than 8 entries (counted in a loop) or a flagged
+// superblock (the plain X_M, global).
+__device__ __noinline__ uint32_t xc4_slow(uint32_t code, const uint32_t* __restrict__ rec4,
+                                          const uint32_t* __restrict__ offs32, const uint32_t* __restrict__ XM) {
+  const uint32_t w = rec4[code >> 9];
+  const uint32_t c1 = w & 127u, c2 = (w >> 7) & 127u;
+  if (c1 == kXc4Flag && c2 == 0u) return __ldg(XM + code);
+  const bool hi = (code & 256u) != 0u;
+  const uint32_t s_rel = hi ? c1 : 0u, e_rel = hi ? c2 : c1;
+  const uint32_t start = (w >> 14) + s_rel, o = code & 255u;
+  DM_ASSERT(e_rel - s_rel <= 2 * kXcMaxBlock, "xc4 list n %u", e_rel - s_rel);
+  uint32_t cnt = 0;
+  for (uint32_t q = start; q < start + (e_rel - s_rel); ++q) cnt += ((offs32[q >> 2] >> (8 * (q & 3u))) & 255u) < o;
+  return code + start + cnt;
+}
+// Staging: the 4-byte pair record h from the global 8-byte superblock record.
+__device__ __forceinline__ uint32_t xc4_record(uint2 r, uint32_t half) {
+  const uint32_t R = r.x & 0x7fffffffu;
+  const uint32_t b0 = r.y & 255u, b1 = (r.y >> 8) & 255u, b2 = (r.y >> 16) & 255u, b3 = r.y >> 24;
+  const uint32_t base = half ? b1 : 0u, c1 = half ? b2 - b1 : b0, c2 = half ? b3 - b1 : b1;
+  const uint32_t Rp = R + base;
+  if ((r.x >> 31) || c2 > 126u || Rp >= kXc4MaxStart) return (umin32(Rp, kXc4MaxStart - 1) << 14) | kXc4Flag;
+  return (Rp << 14) | (c2 << 7) | c1;
+}
+
 // xs: block shift (blocks of 2^xs codes, superblocks of 4 blocks).
 template <bool SM>
 __device__ __forceinline__ uint32_t xc_lookup(uint32_t code, uint32_t xs, const uint2* __restrict__ rec,
@@ -219,15 +352,17 @@ __global__ void __launch_bounds__(rec_threads<XMODE>(), XMODE == XM_XC_SMEM ? 1 
     // + slack: the window reads past the last entry (kXcSmemSlack)
     // xc_dens (auto mode): also require n_new * 2^xc_dens <= |U_M|, i.e. short
     // lists (cfg2: 2.6 entries per 256-code block), else the L2 companion runs
+    // (and n_new < 2^18: the 4-byte shared-memory records hold list starts in 18 bits)
     const bool fits = ((nsb * kXcRecBytes + 15) & ~15ull) + xc_offs_bytes + kXcSmemSlack <= xc_budget &&
-                      (xc_dens == 0 || (n_new << xc_dens) <= dict_len);
+                      (xc_dens == 0 || (n_new << xc_dens) <= dict_len) && n_new < kXc4MaxStart;
     if ((XMODE == XM_XC_SMEM) != fits) return;
   }
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
   uint64_t* empty = full + S;
-  unsigned char* in_ring = smem_raw + 128;
+  uint2* lut = reinterpret_cast<uint2*>(smem_raw + 128);  // XC list masks by length (xc4_fast2)
+  unsigned char* in_ring = smem_raw + kRecHdrBytes;
   uint32_t* sx = reinterpret_cast<uint32_t*>(in_ring + (size_t)S * in_stage_bytes);  // XS only
 
   const uint64_t n_total = n_main + n_delta;
@@ -245,20 +380,24 @@ __global__ void __launch_bounds__(rec_threads<XMODE>(), XMODE == XM_XC_SMEM ? 1 
     }
     fence_mbar_init();
   }
+  if (threadIdx.x < 9) {  // lut[n]: MSB of each of the first min(n, 8) bytes of an 8-byte window
+    const uint32_t n = threadIdx.x;
+    lut[n] = make_uint2(0x80808080u & (n >= 4 ? 0xffffffffu : (1u << (8 * n)) - 1u),
+                        0x80808080u & (n >= 8 ? 0xffffffffu : n <= 4 ? 0u : (1u << (8 * (n - 4))) - 1u));
+  }
   if (XS) {
     for (uint32_t i = threadIdx.x; i < dict_len; i += blockDim.x) sx[i] = __ldg(XM + i);
   }
-  uint2* srec = reinterpret_cast<uint2*>(sx);
+  const uint32_t* srec4 = sx;
   const uint64_t rec_pad = (nsb * kXcRecBytes + 15) & ~15ull;
   const uint32_t* soffs = reinterpret_cast<const uint32_t*>(reinterpret_cast<unsigned char*>(sx) + rec_pad);
   if (XMODE == XM_XC_SMEM) {
-    const uint4* src = reinterpret_cast<const uint4*>(xrec);  // records, then the offsets
+    const uint4* src = reinterpret_cast<const uint4*>(xrec);  // two 8-byte records -> four 4-byte ones
     uint4* dst = reinterpret_cast<uint4*>(sx);
     for (uint64_t i = threadIdx.x; i < rec_pad / 16; i += blockDim.x) {
-      uint4 v = __ldg(src + i);  // two records; flagged ones become {R, kXcFlagY}
-      if ((int)v.x < 0) v.x &= 0x7fffffffu, v.y = kXcFlagY;
-      if ((int)v.z < 0) v.z &= 0x7fffffffu, v.w = kXcFlagY;
-      dst[i] = v;
+      const uint4 v = __ldg(src + i);
+      dst[i] = make_uint4(xc4_record(make_uint2(v.x, v.y), 0), xc4_record(make_uint2(v.x, v.y), 1),
+                          xc4_record(make_uint2(v.z, v.w), 0), xc4_record(make_uint2(v.z, v.w), 1));
     }
     const uint4* go = reinterpret_cast<const uint4*>(xoffs);
     uint4* so = dst + rec_pad / 16;
@@ -273,7 +412,7 @@ __global__ void __launch_bounds__(rec_threads<XMODE>(), XMODE == XM_XC_SMEM ? 1 
         const uint64_t c = blockIdx.x + k * gridDim.x;
         if (c >= nchunks) break;
         const int s = (int)(k % S);
-        if (k >= S) mbar_wait_parity(&empty[s], (uint32_t)(((k / S) - 1) & 1));
+        if (k >= S) mbar_wait_parity_sleep(&empty[s], (uint32_t)(((k / S) - 1) & 1));
         unsigned char* dst = in_ring + (size_t)s * in_stage_bytes;
         const uint64_t start = c * (uint64_t)chunk_in;
         const uint32_t len = start < main_bytes ? (uint32_t)umin64(chunk_in, main_bytes - start) : 0u;
@@ -290,44 +429,88 @@ __global__ void __launch_bounds__(rec_threads<XMODE>(), XMODE == XM_XC_SMEM ? 1 
 
   // ------------------------------------------------------------------ consumers
   const uint64_t pol_x = policy_evict_last();
+  const uint32_t srec4_sa = smem_u32(srec4), soffs_sa = smem_u32(soffs);
+  const Xc4Consts xk{srec4_sa, soffs_sa, smem_u32(lut), 1u << (xs + 15), 1u << (xs + 10), 0x02020202u + (xs - 8),
+                     xs - 4, xs};  // xs = 8 here: four = 4, eight = 8, opaque to ptxas (IMAD, not LEA)
   const uint32_t us = lane * b, uw0 = us >> 5, uo = us & 31;
   const uint32_t umask = b == 32 ? 0xffffffffu : ((1u << b) - 1);
   const uint32_t pr0 = (32 * lane) / nb, pop = 32 * lane - pr0 * nb;
+  const FmaPack<use_fma_pack<NB>() ? NB : 8> fpk(lane);
+  auto pack = [&](uint32_t x) -> uint32_t {
+    if constexpr (use_fma_pack<NB>())
+      return fpk.pack(x);
+    else
+      return warp_pack<NB>(x, nb, pr0, pop);
+  };
   uint32_t* out32 = reinterpret_cast<uint32_t*>(Mout);
   // codes >= |U_M| are clamped (reads stay in the table) and reported once at
   // the end through the running maximum: two ALU ops per row
   const uint32_t dict_last = (uint32_t)dict_len - 1u;  // |U_M| >= 1 when N_M > 0 (validated by the ABI)
   uint32_t code_max = 0;
 
-  for (uint64_t k = 0;; ++k) {
-    const uint64_t c = blockIdx.x + k * gridDim.x;
-    if (c >= nchunks) break;
-    const int s = (int)(k % S);
-    mbar_wait_parity(&full[s], (uint32_t)((k / S) & 1));
+  // chunks [0, n_fast) are all-main and lie wholly inside M': no per-row bounds
+  // and no per-word store predicate beyond lane < b'
+  const uint64_t n_fast = umin64(n_main / R, nw32 / ((uint64_t)G * nb));
+  int s = 0;
+  uint32_t phase = 0;
+  for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    mbar_wait_parity_sleep(&full[s], phase);
     const uint32_t* sin = reinterpret_cast<const uint32_t*>(in_ring + (size_t)s * in_stage_bytes);
-    const uint64_t row_base = c * R;
     uint32_t v[U];
     auto translate = [&](uint32_t code) -> uint32_t {
       code_max = umax32(code_max, code);
       code = umin32(code, dict_last);
       if constexpr (XMODE == XM_RAW_SMEM)
         return sx[code];
-      else if constexpr (XMODE == XM_XC_SMEM)
-        return xc_lookup_smem8(code, srec, soffs, XM);
+      else if constexpr (XMODE == XM_XC_SMEM) {
+        uint32_t slow;
+        const uint32_t x = xc4_fast2(code, xk, slow);
+        return slow ? xc4_slow(code, srec4, soffs, XM) : x;
+      }
       else if constexpr (XMODE == XM_XC_GLOBAL)
         return xc_lookup<false>(code, xs, xrec, reinterpret_cast<const uint32_t*>(xoffs), XM, pol_x);
       else
         return ld_gather_u32(XM + code, pol_x);
     };
-    if (row_base + R <= n_main) {
-      // all-main chunk (all but the last one or two): no per-row bounds
+    const bool fast = c < n_fast;
+    if (fast) {
+      if constexpr (XMODE == XM_XC_SMEM) {
+        // straight-line fast lookups for all U rows of this lane, then one rare
+        // pass for the long lists / flagged superblocks
+        uint32_t cd[U], slow = 0;
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int g = warp + CW * u;
-        const uint32_t lo = sin[g * b + uw0], hi = sin[g * b + uw0 + 1];
-        v[u] = translate(__funnelshift_r(lo, hi, uo) & umask);
+        for (int u = 0; u < U; ++u) {
+          const int g = warp + CW * u;
+          const uint32_t lo = sin[g * b + uw0], hi = sin[g * b + uw0 + 1];
+          const uint32_t code = __funnelshift_r(lo, hi, uo) & umask;
+          code_max = umax32(code_max, code);
+          cd[u] = umin32(code, dict_last);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (u >= U - DM_XC_HYB) {  // experiment: some rows gather the plain X_M through L2 (LSU, not ALU)
+            v[u] = ld_gather_u32(XM + cd[u], pol_x);
+            continue;
+          }
+          uint32_t su;
+          v[u] = xc4_fast2(cd[u], xk, su);
+          slow |= su << u;
+        }
+        if (__builtin_expect(slow != 0u, 0)) {
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (slow & (1u << u)) v[u] = xc4_slow(cd[u], srec4, soffs, XM);
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int g = warp + CW * u;
+          const uint32_t lo = sin[g * b + uw0], hi = sin[g * b + uw0 + 1];
+          v[u] = translate(__funnelshift_r(lo, hi, uo) & umask);
+        }
       }
     } else {
+      const uint64_t row_base = c * R;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int g = warp + CW * u;
@@ -336,7 +519,7 @@ __global__ void __launch_bounds__(rec_threads<XMODE>(), XMODE == XM_XC_SMEM ? 1 
           const uint32_t lo = sin[g * b + uw0], hi = sin[g * b + uw0 + 1];
           v[u] = translate(__funnelshift_r(lo, hi, uo) & umask);
         } else if (row < n_total) {
-          v[u] = __ldg(XD + __ldg(rank + (row - n_main)));
+          v[u] = __ldg(XD + (rank ? __ldg(rank + (row - n_main)) : (uint32_t)(row - n_main)));
         } else {
           v[u] = 0;
         }
@@ -344,19 +527,20 @@ __global__ void __launch_bounds__(rec_threads<XMODE>(), XMODE == XM_XC_SMEM ? 1 
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);  // stage s fully read by this warp
+    if (++s == S) s = 0, phase ^= 1u;
     // output: group g of chunk c is words [(c G + g) b', +b'); lane k < b' writes word k
     uint32_t* outc = out32 + (c * G + warp) * (uint64_t)nb + lane;
     if ((c + 1) * G * (uint64_t)nb <= nw32) {  // the whole chunk is inside M' (all but the last)
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const uint32_t word = warp_pack<NB>(v[u], nb, pr0, pop);
+        const uint32_t word = pack(v[u]);
         if (lane < nb) __stcs(outc + (size_t)CW * u * nb, word);
       }
     } else {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int g = warp + CW * u;
-        const uint32_t word = warp_pack<NB>(v[u], nb, pr0, pop);
+        const uint32_t word = pack(v[u]);
         const uint64_t ow = (c * G + g) * nb + lane;
         if (lane < nb && ow < nw32) __stcs(out32 + ow, word);
       }
@@ -469,14 +653,14 @@ static uint32_t xc_smem_budget(uint32_t in_stage) {
     cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, d);
     return v;
   }();
-  const int64_t b = (int64_t)optin - 1024 - 128 - (int64_t)kRecStagesXc * in_stage;
+  const int64_t b = (int64_t)optin - 1024 - kRecHdrBytes - (int64_t)kRecStagesXc * in_stage;
   return b > 0 ? (uint32_t)(b & ~15ll) : 0u;
 }
 
 template <int NB>
 cudaError_t launch_nb(const dm_column_in* in, const dm_column_out* out, const uint32_t* xm, const uint32_t* xd,
                       const uint32_t* rank, dm_header* hdr, cudaStream_t st, uint32_t fixed_bits, const uint2* xrec,
-                      const uint8_t* xoffs, uint32_t xs) {
+                      const uint8_t* xoffs, uint32_t xs, bool xc_only) {
   const uint32_t in_stage = kRecGroups * in->main_bits * 4 + 16;
   const uint32_t in_stage_xc = rec_groups<XM_XC_SMEM>() * in->main_bits * 4 + 16;
   const int sms = device_sms();
@@ -493,7 +677,7 @@ cudaError_t launch_nb(const dm_column_in* in, const dm_column_out* out, const ui
                                           budget, dens, xs);
     note_launch();
   };
-  const size_t ring = 128 + (size_t)kRecStages * in_stage;
+  const size_t ring = kRecHdrBytes + (size_t)kRecStages * in_stage;
   if (in->dict_len * 4 <= kRecSmemXBytes) {
     go(k_recompress<NB, XM_RAW_SMEM>, ring + in->dict_len * 4, 0);
     return cudaGetLastError();
@@ -501,7 +685,7 @@ cudaError_t launch_nb(const dm_column_in* in, const dm_column_out* out, const ui
   const int knob = tuning(0);
   if constexpr (NB < 0) {  // bounded runtime-width kernels exist for the plain-X_M modes only
     if (xrec && knob != 1)
-      return launch_nb<0>(in, out, xm, xd, rank, hdr, st, fixed_bits, xrec, xoffs, xs);
+      return launch_nb<0>(in, out, xm, xd, rank, hdr, st, fixed_bits, xrec, xoffs, xs, xc_only);
     go(k_recompress<NB, XM_RAW_GLOBAL>, ring, 0);
     return cudaGetLastError();
   } else {
@@ -514,16 +698,16 @@ cudaError_t launch_nb(const dm_column_in* in, const dm_column_out* out, const ui
   const bool auto_smem = knob == 0 && xc_smem_candidate(in);
   const bool want_smem = (knob == 2 || auto_smem) && xs == 8;
   if (auto_smem) dens = 6;  // <= 4 entries per 256-code block on average
-  if (knob == 0 && !auto_smem && in->dict_len * 4 <= kXcGlobalMinBytes) {
+  if (knob == 0 && !auto_smem && !xc_only && in->dict_len * 4 <= kXcGlobalMinBytes) {
     go(k_recompress<NB, XM_RAW_GLOBAL>, ring, 0);
     return cudaGetLastError();
   }
   const uint32_t budget0 = want_smem ? xc_smem_budget(in_stage_xc) : 0u;
   const uint32_t budget = (uint64_t)xc_nsb(in->dict_len, xs) * kXcRecBytes + 16 <= budget0 ? budget0 : 0u;
   if (budget)
-    go(k_recompress<NB, XM_XC_SMEM>, 128 + (size_t)kRecStagesXc * in_stage_xc + budget, budget,
+    go(k_recompress<NB, XM_XC_SMEM>, kRecHdrBytes + (size_t)kRecStagesXc * in_stage_xc + budget, budget,
        rec_threads<XM_XC_SMEM>(), rec_groups<XM_XC_SMEM>());
-  const bool xc_l2 = knob == 2 || knob == 3 || in->dict_len * 4 > kXcGlobalMinBytes;
+  const bool xc_l2 = xc_only || knob == 2 || knob == 3 || in->dict_len * 4 > kXcGlobalMinBytes;
   // (A persisting L2 access-policy window over XC was measured: no gain on
   // cfg5's Step 2(b), and the set-aside slowed Steps 1(a)/1(b) by 40%.)
   if (xc_l2)
@@ -543,7 +727,8 @@ constexpr auto make_xc_table(std::integer_sequence<int, I...>) {
 }
 
 using LaunchFn = cudaError_t (*)(const dm_column_in*, const dm_column_out*, const uint32_t*, const uint32_t*,
-                                 const uint32_t*, dm_header*, cudaStream_t, uint32_t, const uint2*, const uint8_t*, uint32_t);
+                                 const uint32_t*, dm_header*, cudaStream_t, uint32_t, const uint2*, const uint8_t*, uint32_t,
+                                 bool);
 template <int... I>
 constexpr auto make_table(std::integer_sequence<int, I...>) {
   return std::array<LaunchFn, sizeof...(I)>{&launch_nb<I>...};
@@ -553,10 +738,14 @@ constexpr auto make_table(std::integer_sequence<int, I...>) {
 
 cudaError_t launch_recompress(const dm_column_in* in, const dm_column_out* out, const uint32_t* xm,
                               const uint32_t* xd, const uint32_t* rank, dm_header* hdr, cudaStream_t st,
-                              uint32_t fixed_bits, const uint2* xc_rec, const uint8_t* xc_offs, uint32_t xc_shift) {
+                              uint32_t fixed_bits, const uint2* xc_rec, const uint8_t* xc_offs, uint32_t xc_shift,
+                              bool xc_only) {
   if (in->n_main + in->n_delta == 0) return cudaSuccess;
   static const auto table = make_table(std::make_integer_sequence<int, 33>{});  // [0] = runtime width
-  if (fixed_bits) return table[fixed_bits](in, out, xm, xd, rank, hdr, st, fixed_bits, nullptr, nullptr, 8);
+  // fixed b' (dm_recompress, the host path's row chunks): XC when the caller has
+  // one (its shared-memory variant reads n_new from the merge's header)
+  if (fixed_bits)
+    return table[fixed_bits](in, out, xm, xd, rank, hdr, st, fixed_bits, xc_rec, xc_offs, xc_shift, xc_only);
   const uint64_t lo_len = std::max<uint64_t>(in->dict_len, in->n_delta ? 1 : 0);
   const uint32_t nb_lo = host_width(lo_len), nb_hi = host_width(in->dict_len + in->n_delta);
   if (nb_hi > 32) return cudaErrorInvalidValue;  // caller checks DM_E_TOO_WIDE first
@@ -565,7 +754,7 @@ cudaError_t launch_recompress(const dm_column_in* in, const dm_column_out* out, 
   // than the runtime-width kernel (its shuffle-pack loop and spills)
   if (nb_hi - nb_lo <= 3) {
     for (uint32_t nb = nb_lo; nb <= nb_hi; ++nb) {
-      cudaError_t e = table[nb](in, out, xm, xd, rank, hdr, st, 0, xc_rec, xc_offs, xc_shift);
+      cudaError_t e = table[nb](in, out, xm, xd, rank, hdr, st, 0, xc_rec, xc_offs, xc_shift, xc_only);
       if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
@@ -579,8 +768,8 @@ cudaError_t launch_recompress(const dm_column_in* in, const dm_column_out* out, 
   static const int bound[] = {2, 3, 4, 5, 6, 7, 8, 9, 12, 17};
   const int tm = (int)((2 * nb_lo + 30) / nb_lo);
   for (int c = 0; c < 10; ++c)
-    if (tm <= bound[c]) return classes[c](in, out, xm, xd, rank, hdr, st, 0, xc_rec, xc_offs, xc_shift);
-  return table[0](in, out, xm, xd, rank, hdr, st, 0, xc_rec, xc_offs, xc_shift);
+    if (tm <= bound[c]) return classes[c](in, out, xm, xd, rank, hdr, st, 0, xc_rec, xc_offs, xc_shift, xc_only);
+  return table[0](in, out, xm, xd, rank, hdr, st, 0, xc_rec, xc_offs, xc_shift, xc_only);
 }
 
 cudaError_t launch_recompress_xc(const dm_column_in* in, const dm_column_out* out, const uint32_t* xm,
@@ -588,7 +777,7 @@ cudaError_t launch_recompress_xc(const dm_column_in* in, const dm_column_out* ou
                                  uint32_t bits, const uint2* xc_rec, const uint8_t* xc_offs, uint32_t xs) {
   if (in->n_main + in->n_delta == 0) return cudaSuccess;
   const uint32_t in_stage = kRecGroups * in->main_bits * 4 + 16;
-  const size_t smem = 128 + (size_t)kRecStages * in_stage;
+  const size_t smem = kRecHdrBytes + (size_t)kRecStages * in_stage;
   const uint64_t n_total = in->n_main + in->n_delta;
   const uint64_t nchunks = (n_total + 32ull * kRecGroups - 1) / (32ull * kRecGroups);
   static const auto xc_table = make_xc_table(std::make_integer_sequence<int, 33>{});

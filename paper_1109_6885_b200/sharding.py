@@ -10,14 +10,15 @@
   multiples of 4096 rows so every shard starts on a u64-word boundary at both
   the input width b and the output width b' (4096·b and 4096·b' are multiples of
   64, and of 128 bits, so TMA bulk copies stay 16-byte aligned).
-  ``sharded_merge_column`` runs Steps 1(a)/1(b)/2(a) on the root device,
-  broadcasts the header and the translation tables over NCCL (torch.distributed)
-  -- by default the compact table XC (~67 MB for cfg5) instead of the literal X_M
-  (4.3 GB) -- and every rank recompresses its own row range with
-  ``dm_recompress_xc`` (or ``dm_recompress``).
+  ``sharded_merge_column`` is a thin wrapper of the C ABI's
+  ``dm_merge_column_sharded``: the library runs Steps 1(a)/1(b)/2(a) on the root,
+  broadcasts the header and the translation tables over its transport (NCCL, or
+  host callbacks over a torch.distributed group) -- by default the compact table
+  XC (~67 MB for cfg5) instead of the literal X_M (4.3 GB) -- and every rank
+  recompresses its own row range.
 
-The planning functions are plain Python (tested with gloo on the CPU); the
-merge itself needs CUDA devices.
+The column partition (LPT) is plain Python; the row plan is the library's
+(host-only, tested with gloo on the CPU); the merge itself needs CUDA devices.
 """
 from __future__ import annotations
 
@@ -85,14 +86,13 @@ class RowShard:
 
 
 def plan_row_shards(n_main: int, n_delta: int, n_shards: int, align: int = ROW_ALIGN) -> List[RowShard]:
-    """Cut the N' output rows into n_shards contiguous ranges at multiples of `align`
-    (the delta rows follow the main rows)."""
-    total = n_main + n_delta
-    cuts = [0]
-    for g in range(1, n_shards):
-        c = (total * g // n_shards) // align * align
-        cuts.append(max(c, cuts[-1]))
-    cuts.append(total)
+    """The library's row plan (``dm_plan_row_shards``, a pure host function of the
+    C ABI): the N' output rows cut into n_shards contiguous ranges at multiples of
+    4096 (the delta rows follow the main rows)."""
+    if align != ROW_ALIGN:
+        raise ValueError("the library plans at 4096-row multiples")
+    import paper_1109_6885_b200 as dm
+    cuts = dm.plan_row_shards(n_main, n_delta, n_shards)
     shards = []
     for g in range(n_shards):
         r0, r1 = cuts[g], cuts[g + 1]
@@ -102,78 +102,32 @@ def plan_row_shards(n_main: int, n_delta: int, n_shards: int, align: int = ROW_A
     return shards
 
 
-def sharded_merge_column(main_dict, main_codes_shard, n_main: int, main_bits: int, delta, shard: RowShard,
-                         group=None, root: int = 0, tables: str = "xc"):
-    """Row-sharded merge of one column across the ranks of `group` (one GPU each).
+def sharded_merge_column(main_dict, main_codes_shard, n_main: int, main_bits: int, delta, comm=None,
+                         tables: str = "xc", root: int = 0, dict_len=None, n_delta=None, key=None):
+    """Row-sharded merge of one column across the ranks of `comm` (one GPU each),
+    through the C ABI's ``dm_merge_column_sharded``: the root runs Steps
+    1(a)/1(b)/2(a), the library broadcasts the header and XC (or X_M), sends the
+    delta rows' codes to their owner and every rank recompresses its row range.
 
-    Every rank passes its own packed main-code slice (`main_codes_shard`, the words
-    of rows [shard.main_begin, shard.main_end)).  The root also passes U_M and D
-    (other ranks may pass empty tensors with the right dtype).  Returns this rank's
-    packed output slice (rows [shard.row_begin, shard.row_end) at b'), b', |U'|, and
-    on the root U' as well.
-
-    tables="xc" (default): the root broadcasts the compact table XC (8-byte records
-    + one byte per new value; ~67 MB for cfg5) and the X_M slices of the rare
-    flagged superblocks, instead of the literal X_M (4.3 GB for cfg5, SURVEY §8e's
-    control design, tables="plain").  X_D and r follow as before.
-    """
-    import torch
-    import torch.distributed as dist
+    Every rank passes its own packed main-code slice (`main_codes_shard`, the
+    words of rows [shard.main_begin, shard.main_end) of ``plan_row_shards``); the
+    root also passes U_M and D.  `comm`: a ``dm.Comm`` (default: callbacks over
+    the torch.distributed default group).  Returns (this rank's M' words, b',
+    |U'|, U' on the root else None)."""
     import paper_1109_6885_b200 as dm
-
-    rank = dist.get_rank(group)
-    dev = torch.device("cuda", torch.cuda.current_device())
-    # |U'|, |U_D|, b', |U_M|, N_D, use_xc, shift, n_records, offset bytes, exception count
-    hdr = torch.zeros(10, dtype=torch.int64, device=dev)
-    U = merger = xc = None
-    if rank == root:
-        merger = dm.DictionaryMerger(main_dict, n_main, main_bits, delta)
-        merger.run_async()
-        h = merger.header()
-        if h.status != 0:
-            raise dm.DictMergeError(h.status, "dm_dictionary_merge_async")
-        U = merger.U[: h.merged_dict_len]
-        xc = merger.xc() if tables == "xc" else None
-        exc = dm.xc_exceptions_gather(xc, main_dict.shape[0], merger.XM) if xc is not None else None
-        hdr.copy_(torch.tensor([h.merged_dict_len, h.delta_dict_len, h.merged_bits, main_dict.shape[0],
-                                delta.shape[0], int(xc is not None), xc.shift if xc else 0,
-                                xc.n_records if xc else 0, xc.offsets.numel() if xc else 0,
-                                exc[2] if exc else 0], dtype=torch.int64))
-    dist.broadcast(hdr, src=root, group=group)
-    n_u, n_ud, nb, dict_len, n_delta, use_xc, shift, n_rec, n_off, n_exc = (int(x) for x in hdr.tolist())
-
-    def bcast(t_root, shape, dtype):
-        t = t_root if rank == root else torch.empty(shape, dtype=dtype, device=dev)
-        dist.broadcast(t, src=root, group=group)
-        return t
-
-    if use_xc:
-        rec = bcast(xc.records if xc else None, (n_rec * 8,), torch.uint8)
-        offs = bcast(xc.offsets if xc else None, (n_off,), torch.uint8)
-        tabs = dm.XcTables(rec, offs, shift, n_rec)
-        if rank == root:
-            xm = merger.XM[:dict_len]
-        else:
-            xm = torch.empty(max(dict_len, 1), dtype=torch.int32, device=dev)  # only exception slices are read
-        if n_exc:
-            sb = 4 << shift
-            ids = bcast(exc[0] if rank == root else None, (n_exc,), torch.int32)
-            sl = bcast(exc[1] if rank == root else None, (n_exc * sb,), torch.int32)
-            if rank != root:
-                dm.xc_exceptions_scatter(tabs, dict_len, ids, sl, n_exc, xm)
-    else:
-        xm = bcast(merger.XM[:dict_len] if rank == root else None, (max(dict_len, 1),), torch.int32)
-    xd = bcast(merger.XD[: max(n_ud, 1)] if rank == root else None, (max(n_ud, 1),), torch.int32) if n_delta \
-        else torch.empty(1, dtype=torch.int32, device=dev)
-    rk = bcast(merger.R[: max(n_delta, 1)] if rank == root else None, (max(n_delta, 1),), torch.int32) if n_delta \
-        else torch.empty(1, dtype=torch.int32, device=dev)
-    if use_xc:
-        out = dm.recompress_xc(main_codes_shard, shard.n_main, main_bits, dict_len, tabs, xm, xd,
-                               rk[shard.delta_begin:], shard.n_delta, nb)
-    else:
-        out = dm.recompress(main_codes_shard, shard.n_main, main_bits, dict_len, xm, xd, rk[shard.delta_begin:],
-                            shard.n_delta, nb)
-    return out, nb, n_u, U
+    own = comm is None
+    comm = comm if comm is not None else dm.Comm.callbacks()
+    try:
+        if key is None:
+            key = {0: "u64", 1: "b16", 2: "u32"}[dm._key_of(main_dict)]
+        r = dm.merge_column_sharded(comm, main_codes_shard, n_main, main_bits,
+                                    main_dict.shape[0] if dict_len is None else dict_len,
+                                    delta.shape[0] if n_delta is None else n_delta, main_dict=main_dict, delta=delta,
+                                    key=key, tables=tables, root=root)
+    finally:
+        if own:
+            comm.close()
+    return r.merged_codes, r.merged_bits, r.merged_len, r.merged_dict
 
 
 # ----------------------------------------------------------- NEXT2: sharded Step 1(b)
@@ -227,8 +181,18 @@ def sharded_dictionary_merge(main_dict_range, range_begin: int, dict_len: int, m
     import paper_1109_6885_b200 as dm
 
     rank, world = dist.get_rank(group), dist.get_world_size(group)
+    with dm.tuning(dm.KNOB_XC_SHIFT, shift):  # process-wide knob: restored on exit
+        return _sharded_dictionary_merge(main_dict_range, range_begin, dict_len, main_bits, delta, group, root,
+                                         shift)
+
+
+def _sharded_dictionary_merge(main_dict_range, range_begin, dict_len, main_bits, delta, group, root, shift):
+    import torch
+    import torch.distributed as dist
+    import paper_1109_6885_b200 as dm
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
     dev = torch.device("cuda", torch.cuda.current_device())
-    dm.set_tuning(dm.KNOB_XC_SHIFT, shift)
     SB = 4 << shift
     L = int(main_dict_range.shape[0])
     assert L > 0 and range_begin % XC_SUPER == 0

@@ -97,7 +97,7 @@ def test_tuning_knobs_validated_on_the_host():
     anything else is DM_E_INVALID.  Pure host logic (no GPU needed)."""
     import paper_1109_6885_b200 as dm
     L = dm._lib()
-    hi = {0: 3, 1: 2, 2: 2, 3: 1, 5: 2}
+    hi = {0: 3, 1: 3, 2: 2, 3: 1, 5: 2}
     try:
         for k, h in hi.items():
             for v in range(h + 1):
@@ -129,3 +129,37 @@ def test_bucket_path_workspace():
         assert auto - lsd >= 4 * (1_000_000 // 8)  # bucket offsets (u32, >= N_D / 8 buckets)
     finally:
         L.dm_set_tuning(5, 0)
+
+
+def test_recompress_rejects_inconsistent_dictionary_length():
+    """dm_recompress / dm_recompress_xc (include/dictmerge.h): with N_M > 0 the
+    dictionary length must satisfy 1 <= |U_M| < 2^32 and b >= width(|U_M|) --
+    else DM_E_INVALID before any launch (|U_M| = 0 would defeat the kernels'
+    code clamp).  Host-only checks, no GPU needed."""
+    import paper_1109_6885_b200 as dm
+    L = dm._lib()
+    P = 16  # any aligned non-NULL pointer value: the call must fail before touching it
+    assert L.dm_recompress(P, 100, 8, 0, P, None, None, 0, 8, P, 100, None) == dm.Status.E_INVALID
+    assert L.dm_recompress(P, 100, 8, 1 << 32, P, None, None, 0, 8, P, 100, None) == dm.Status.E_INVALID
+    assert L.dm_recompress(P, 100, 3, 9, P, None, None, 0, 8, P, 100, None) == dm.Status.E_INVALID  # b < width(9)
+    xc = dm._Xc(P, 1, P, 32, 8, 1)
+    assert L.dm_recompress_xc(P, 100, 8, 0, ctypes.byref(xc), P, None, None, 0, 8, P, 100, None) == \
+        dm.Status.E_INVALID
+
+
+def test_host_entry_rejects_bad_host_buffers_before_copying():
+    """dm_merge_column_host checks the caller's host buffers first: NULL context
+    or structs are DM_E_INVALID (the capacity rules need a context, i.e. a GPU:
+    tests/test_gpu_host_api.py)."""
+    import paper_1109_6885_b200 as dm
+    L = dm._lib()
+    assert L.dm_merge_column_host(None, None, None) == dm.Status.E_INVALID
+
+
+def test_get_tuning_round_trips():
+    import paper_1109_6885_b200 as dm
+    assert dm.get_tuning(4) == 0
+    with dm.tuning(4, 7):
+        assert dm.get_tuning(4) == 7
+    assert dm.get_tuning(4) == 0
+    assert dm._lib().dm_get_tuning(6) == dm.Status.E_INVALID

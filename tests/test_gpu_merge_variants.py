@@ -39,8 +39,8 @@ CASES = [
 ]
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2])
-@pytest.mark.parametrize("key", ["u64", "b16"])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
+@pytest.mark.parametrize("key", ["u64", "b16", "u32"])
 @pytest.mark.parametrize("case", CASES)
 def test_merge_variant(variant, key, case):
     import paper_1109_6885_b200 as dm
@@ -51,7 +51,7 @@ def test_merge_variant(variant, key, case):
     compare(col, M, r)
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
 def test_merge_ties_at_every_tile_boundary(variant):
     # U_D = every other U_M value plus values between: duplicates land on both
     # sides of many merge-path tile boundaries (tile = 2048 merged elements)
@@ -63,6 +63,43 @@ def test_merge_ties_at_every_tile_boundary(variant):
     D = D[rng.permutation(D.size)]
     codes = rng.integers(0, UM.size, size=60_000, dtype=np.uint64).astype(np.uint32)
     col = datagen.Column("u64", UM, codes, datagen.width_hint(UM.size), D)
+    M, r = run_gpu(col)
+    compare(col, M, r)
+
+
+@pytest.mark.parametrize("shape", ["cluster", "all_below", "all_above", "boundaries", "one_tile", "many_chunks"])
+def test_sparse_tiles_edges(shape):
+    """Step 1(b) sparse-delta tiles (knob 1 = 3): slices larger than one 2048-value
+    chunk (several passes), every new value below U_M[0] or above U_M[-1], values
+    equal to tile-boundary U_M entries (U_M[2048 t]) and their neighbours, a
+    single partial tile."""
+    import paper_1109_6885_b200 as dm
+    dm.set_tuning(1, 3)
+    rng = np.random.default_rng(17)
+    n_dict = 1500 if shape == "one_tile" else 50_000
+    UM = (np.arange(n_dict, dtype=np.uint64) + np.uint64(1)) * np.uint64(1000)
+    if shape == "cluster":       # 9000 new values in one gap (5 chunks) + some spread
+        D = np.concatenate([np.uint64(1000 * 777) + rng.choice(np.arange(1, 1000, dtype=np.uint64) * np.uint64(1),
+                                                                999, replace=False),
+                            UM[rng.integers(0, n_dict, 3000)]])
+    elif shape == "many_chunks":  # a slice of ~7000 values inside one tile: new and reused mixed
+        base = np.uint64(1000 * 4100)
+        D = np.concatenate([base + rng.choice(2_000_000, 7000, replace=False).astype(np.uint64) // np.uint64(1000) *
+                            np.uint64(1000) + np.uint64(500), UM[4096:6000]])
+    elif shape == "all_below":
+        D = rng.choice(999, 600, replace=False).astype(np.uint64) + np.uint64(1)
+    elif shape == "all_above":
+        D = UM[-1] + rng.choice(10**6, 5000, replace=False).astype(np.uint64) + np.uint64(1)
+    elif shape == "boundaries":
+        t = np.arange(0, n_dict, 2048)
+        D = np.concatenate([UM[t], UM[t] - np.uint64(1), UM[t] + np.uint64(1), UM[np.minimum(t + 2047, n_dict - 1)]])
+    else:
+        D = np.concatenate([UM[::7], UM[3::11] + np.uint64(5), np.zeros(1, np.uint64)])
+    D = np.unique(D)[: max(1, n_dict // 2)]
+    D = np.concatenate([D, D[::3]])
+    D = D[rng.permutation(D.size)]
+    codes = rng.integers(0, n_dict, size=80_000, dtype=np.uint64).astype(np.uint32)
+    col = datagen.Column("u64", UM, codes, datagen.width_hint(n_dict), D)
     M, r = run_gpu(col)
     compare(col, M, r)
 

@@ -271,6 +271,24 @@ def test_cfg3_full():
     assert ref.merged_bits == 21
 
 
+# Seed S + 1 (SURVEY §8d "Seeds": every parity run repeats at S + 1), full size
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+def test_configs_full_seed_s_plus_1(cfg):
+    col = datagen.make_config(cfg, seed=datagen.BASE_SEED + 1)
+    M, r = run_gpu(col)
+    compare(col, M, r)
+
+
+@pytest.mark.slow
+def test_cfg2e4_full():
+    """cfg2's shape with 4-byte values (E = 4; NEXT4) at full size."""
+    col = datagen.make_config_e4()
+    M, r = run_gpu(col)
+    ref = compare(col, M, r)
+    assert ref.merged_bits == 24
+
+
 @pytest.mark.slow
 def test_cfg4_columns_full_size():
     for j in (0, 3, 120, 239, 240, 271, 299):
@@ -317,3 +335,41 @@ def test_host_entry_point_pipelined(key, n_main, dict_len, n_delta, p_new):
         assert np.array_equal(keys_np(Uo[:n], col.key), ref.merged_dict)
         assert np.array_equal(Mo[: ref.merged_words.size].numpy().view(np.uint64), ref.merged_words)
         ctx.close()
+
+
+def test_host_entry_rejects_undersized_host_outputs():
+    """dm_merge_column_host (ADVICE): host outputs are checked before any copy --
+    NULL U' / M' buffers are DM_E_INVALID, capacities below dict_len + n_delta
+    keys / dm_merged_codes_cap_words(in) words are DM_E_CAPACITY."""
+    import ctypes
+    import paper_1109_6885_b200 as dm
+    col = datagen.make_random_case(77, 50_000, 3000, 4000, 0.4)
+    UM = torch.from_numpy(col.main_dict.view(np.int64).copy())
+    D = torch.from_numpy(col.delta.view(np.int64).copy())
+    Mw = torch.from_numpy(oracle.pack(col.main_codes, col.main_bits).view(np.int64).copy())
+    cin = dm._make_in(UM, Mw, col.n_main, col.main_bits, D)
+    need = dm.merged_codes_cap_words(cin)
+    Uo = torch.empty(col.dict_len + col.n_delta, dtype=torch.int64)
+    Mo = torch.empty(need, dtype=torch.int64)
+    ctx = dm.HostContext(0)
+    L = dm._lib()
+    cases = [(dm._Out(None, Uo.numel(), Mo.data_ptr(), need), dm.Status.E_INVALID),
+             (dm._Out(Uo.data_ptr(), Uo.numel(), None, need), dm.Status.E_INVALID),
+             (dm._Out(Uo.data_ptr(), Uo.numel() - 1, Mo.data_ptr(), need), dm.Status.E_CAPACITY),
+             (dm._Out(Uo.data_ptr(), Uo.numel(), Mo.data_ptr(), need - 1), dm.Status.E_CAPACITY),
+             (dm._Out(Uo.data_ptr(), Uo.numel(), Mo.data_ptr(), need), dm.Status.OK)]
+    for cout, want in cases:
+        assert L.dm_merge_column_host(ctx.h, ctypes.byref(cin), ctypes.byref(cout)) == want
+    ref = oracle.merge(col)
+    assert np.array_equal(Mo[: ref.merged_words.size].numpy().view(np.uint64), ref.merged_words)
+    ctx.close()
+
+
+def test_recompress_rejects_empty_dictionary_on_device():
+    """dm_recompress with N_M > 0 and |U_M| = 0 (ADVICE): DM_E_INVALID, no launch."""
+    import paper_1109_6885_b200 as dm
+    M = torch.zeros(16, dtype=torch.int64, device="cuda")
+    xm = torch.zeros(4, dtype=torch.int32, device="cuda")
+    with pytest.raises(dm.DictMergeError) as e:
+        dm.recompress(M, 10, 4, 0, xm, xm, xm, 0, 4)
+    assert e.value.status == dm.Status.E_INVALID

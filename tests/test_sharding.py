@@ -1,7 +1,9 @@
-"""Multi-device partitioning: plans and their host logic on the CPU,
-including 2-process gloo runs of the row-sharded Step 2 with the translation
-tables broadcast from the root (the data path each GPU rank follows, with the
-per-shard recompress done by numpy + the oracle's packer instead of the kernel)."""
+"""Multi-device partitioning: plans and their host logic on the CPU
+-- the library's row plan (dm_plan_row_shards) and its host-callback transport
+over 2- and 3-process gloo groups (dm_comm_selftest_host) -- a gloo model of the
+row-sharded data exchange (numpy + the oracle), and, on the GPU, several ranks
+sharing the one device through dm_merge_column_sharded (C ABI) bit-exact
+against the oracle."""
 import os
 import socket
 
@@ -117,49 +119,101 @@ def test_gloo_two_rank_row_sharded_step2():
     assert ok and same_plan
 
 
-def _gpu_worker(rank, world, port, q, tables):
-    """One rank of sharded_merge_column on the (single) GPU: gloo carries the
-    broadcasts of CUDA tensors between the processes; no kernel waits on another
-    rank (every wait is a host-side collective)."""
+def _comm_worker(rank, world, port, q):
+    """Host-only: the library's callback transport over gloo (broadcast from every
+    root, all-gather in rank order, point to point) and the library's row plan,
+    identical on every rank."""
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        import paper_1109_6885_b200 as dm  # noqa: F401
-        from tests.parity import to_device
+        import paper_1109_6885_b200 as dm
+        comm = dm.Comm.callbacks()
+        ok = comm.selftest_host() == dm.Status.OK and comm.rank == rank and comm.size == world
+        plans = [None] * world
+        dist.all_gather_object(plans, dm.plan_row_shards(10**8 + 7, 10**6 + 3, world))
+        comm.close()
+        if rank == 0:
+            q.put((ok, all(p == plans[0] for p in plans), plans[0]))
+        else:
+            q.put((ok, True, None))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_library_transport_and_plan(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_comm_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(r[0] for r in res) and all(r[1] for r in res)
+    cuts = next(r[2] for r in res if r[2] is not None)
+    assert cuts[0] == 0 and cuts[-1] == 10**8 + 7 + 10**6 + 3
+    assert all(c % 4096 == 0 for c in cuts[:-1]) and cuts == sorted(cuts)
+
+
+def _gpu_worker(rank, world, port, q, tables, key, case):
+    """One rank of dm_merge_column_sharded on the (single) GPU: the library's
+    callback transport carries the collectives over gloo between the processes;
+    no kernel waits on another rank (every wait is a host-side collective)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1109_6885_b200 as dm
+        from tests.parity import to_device, keys_np
         torch.cuda.set_device(0)
-        col = datagen.make_random_case(34, 1 << 20, 1 << 16, 60001, 0.6, main_bits=18)
+        if case == "flagged":  # clustered new values: flagged XC superblocks (their X_M slices travel too)
+            col = datagen.make_clustered_case(36, 1 << 19, 200_000, 20_000, key=key)
+        else:
+            col = datagen.make_random_case(34, 1 << 20, 1 << 16, 60001, 0.6, main_bits=18, key=key)
         UM, M, D = to_device(col)
         shard = sharding.plan_row_shards(col.n_main, col.n_delta, world)[rank]
         mslice = M[shard.in_word(col.main_bits):] if shard.n_main else M
         if rank != 0:
             UM, D = UM[:0], D[:0]
-        out, nb, n_u, U = sharding.sharded_merge_column(UM, mslice, col.n_main, col.main_bits, D, shard,
-                                                        tables=tables)
+        comm = dm.Comm.callbacks()
+        out, nb, n_u, U = sharding.sharded_merge_column(UM, mslice, col.n_main, col.main_bits, D, comm=comm,
+                                                        tables=tables, dict_len=col.dict_len, n_delta=col.n_delta,
+                                                        key=key)
+        comm.close()
         gathered = [None] * world
         dist.all_gather_object(gathered, out.cpu().numpy().view(np.uint64).tolist())
         if rank == 0:
             ref = oracle.merge(col)
             full = np.array([w for part in gathered for w in part], dtype=np.uint64)
-            q.put(bool(np.array_equal(full, ref.merged_words)) and nb == ref.merged_bits and n_u == ref.merged_len)
+            q.put((bool(np.array_equal(full, ref.merged_words)), nb == ref.merged_bits, n_u == ref.merged_len,
+                   bool(np.array_equal(keys_np(U, key), ref.merged_dict))))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.gpu
-@pytest.mark.parametrize("tables", ["xc", "plain"])
-def test_sharded_merge_column_two_ranks_on_one_gpu(tables):
+def _run_gpu_ranks(world, *args):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, q, tables)) for r in range(2)]
+    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, q) + args) for r in range(world)]
     for p in procs:
         p.start()
-    ok = q.get(timeout=300)
+    res = q.get(timeout=300)
     for p in procs:
         p.join(timeout=60)
-    assert ok
+    return res
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,tables,key,case", [(2, "xc", "u64", "random"), (2, "plain", "u64", "random"),
+                                                   (3, "xc", "b16", "random"), (2, "xc", "u32", "random"),
+                                                   (3, "xc", "u64", "flagged"), (2, "plain", "u64", "flagged")])
+def test_sharded_merge_column_ranks_on_one_gpu(world, tables, key, case):
+    res = _run_gpu_ranks(world, tables, key, case)
+    assert all(res), res
 
 
 def _next2_worker(rank, world, port, q, key):
@@ -217,4 +271,41 @@ def test_next2_sharded_dictionary_merge(world, key):
     res = q.get(timeout=300)
     for p in procs:
         p.join(timeout=60)
+    assert all(res), res
+
+
+def _nccl1_worker(port, q):
+    """World size 1 over NCCL: the library resolves NCCL from the process and runs
+    its broadcasts / all-gathers through it (NCCL collectives run even at one
+    rank), bit-exact against the oracle."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        import paper_1109_6885_b200 as dm
+        from tests.parity import to_device, keys_np
+        col = datagen.make_random_case(38, 1 << 20, 1 << 16, 60001, 0.6, main_bits=18)
+        UM, M, D = to_device(col)
+        comm = dm.Comm.nccl()
+        r = dm.merge_column_sharded(comm, M, col.n_main, col.main_bits, col.dict_len, col.n_delta, main_dict=UM,
+                                    delta=D)
+        comm.close()
+        ref = oracle.merge(col)
+        q.put((bool(np.array_equal(r.merged_codes.cpu().numpy().view(np.uint64), ref.merged_words)),
+               r.merged_bits == ref.merged_bits, bool(np.array_equal(keys_np(r.merged_dict, "u64"),
+                                                                     ref.merged_dict))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_sharded_merge_column_nccl_one_rank():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl1_worker, args=(_free_port(), q))
+    p.start()
+    res = q.get(timeout=300)
+    p.join(timeout=60)
     assert all(res), res
