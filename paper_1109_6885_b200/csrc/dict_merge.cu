@@ -632,10 +632,14 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge(const void* __restrict_
 //   U_M[a+i] -> U'[a + E_t + i + shift(i)] = X_M[a+i];
 //   new B[j] -> U'[a + E_t + p_j + newrank_j] = X_D[j] (newrank_j = new values
 //           of the slice before j); a duplicate takes its twin's X_M.
-// One read of U_M and U_D, one write of U' (+ X_M when wanted), X_D and the XC
-// inputs -- the streaming bound -- instead of ranking both sides of every
-// merge-path tile twice.
-constexpr uint32_t kSpTile = 2048, kSpThreads = 256, kSpItems = kSpTile / kSpThreads, kSpChunk = 2048;
+// Three phases like the paper's: k_sp_count ranks each slice in its
+// staged tile (p_j | found_j saved, 4 bytes per U_D value) and counts the
+// tile's duplicates; k_scan_counts prefix-sums them (E_t = lo_t - dups before
+// t); k_sp_write copies U_M with gaps straight from global memory and inserts
+// the new values -- no merge-path ranking of both sides.  A single pass with
+// decoupled look-back was slower (cfg2 0.131 vs 0.100 ms, cfg5 12.3 vs 7.6 ms):
+// the look-back serialised the concurrently resident tiles.
+constexpr uint32_t kSpTile = 2048, kSpThreads = 256, kSpItems = kSpTile / kSpThreads, kSpChunk = 512;
 
 template <class KT>
 __global__ void __launch_bounds__(256) k_sp_partition(const void* __restrict__ A, uint64_t nA,
@@ -665,163 +669,153 @@ __global__ void __launch_bounds__(256) k_sp_partition(const void* __restrict__ A
   if (lane == 0) part[t] = lo;
 }
 
+// Phase 1: rank the tile's slice inside the staged tile; pf[j] = p_j | found << 31,
+// cnt[t] = the tile's duplicates (k_scan_counts turns them into prefix sums).
 template <class KT>
-__global__ void __launch_bounds__(kSpThreads) k_sp_merge(const void* __restrict__ A, uint64_t nA,
+__global__ void __launch_bounds__(kSpThreads) k_sp_count(const void* __restrict__ A, uint64_t nA,
                                                          const void* __restrict__ B,
                                                          const uint64_t* __restrict__ part, uint64_t ntiles,
-                                                         uint64_t* status, uint32_t* counter, void* __restrict__ U,
+                                                         uint32_t* __restrict__ pf, uint32_t* __restrict__ cnt) {
+  pdl_prologue();
+  using K = typename KT::K;
+  constexpr uint32_t T = kSpTile, NT = kSpThreads, IT = kSpItems;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  K* sk = reinterpret_cast<K*>(smem_raw);
+  __shared__ uint32_t s_warp[NT / 32 + 1];
+  const uint64_t t = blockIdx.x;
+  const uint64_t a = t * T;
+  const uint32_t na = (uint32_t)umin64(T, nA - a);
+  const uint64_t lo = part[t], nb = part[t + 1] - lo;
+#pragma unroll
+  for (uint32_t r = 0; r < IT; ++r) {
+    const uint32_t i = threadIdx.x + r * NT;
+    if (i < na) sk[i] = KT::load(A, a + i);
+  }
+  __syncthreads();
+  uint32_t dups = 0;
+  for (uint64_t j = threadIdx.x; j < nb; j += NT) {
+    const K v = KT::load(B, lo + j);
+    uint32_t l = 0, h = na;  // #{tile A < v}
+    while (l < h) {
+      const uint32_t m = (l + h) >> 1;
+      if (KT::lt(sk[m], v)) l = m + 1; else h = m;
+    }
+    const bool found = l < na && KT::eq(sk[l], v);
+    dups += found ? 1u : 0u;
+    pf[lo + j] = l | (found ? 0x80000000u : 0u);
+  }
+  uint32_t tot;
+  block_exclusive_scan<NT>(dups, s_warp, tot);
+  if (threadIdx.x == 0) cnt[t] = tot;
+}
+
+// Phase 3: E_t = part[t] - excl[t] new values precede the tile; copy U_M with
+// gaps (straight from global memory, coalesced), insert the new values, write
+// X_M / X_D and the XC inputs.
+template <class KT>
+__global__ void __launch_bounds__(kSpThreads) k_sp_write(const void* __restrict__ A, uint64_t nA,
+                                                         const void* __restrict__ B,
+                                                         const uint64_t* __restrict__ part, uint64_t ntiles,
+                                                         const uint32_t* __restrict__ pf,
+                                                         const uint64_t* __restrict__ excl, void* __restrict__ U,
                                                          uint32_t* __restrict__ XM, uint32_t* __restrict__ XD,
                                                          dm_header* hdr, uint32_t* __restrict__ rblk,
                                                          uint8_t* __restrict__ offs, uint32_t xs) {
   pdl_prologue();
   using K = typename KT::K;
-  constexpr uint32_t T = kSpTile, NT = kSpThreads, IT = kSpItems, C = kSpChunk;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  K* sk = reinterpret_cast<K*>(smem_raw);           // [0] = A[a - 1], then the tile
-  K* sv = sk + (T + 1);                             // slice chunk values
-  uint32_t* sp = reinterpret_cast<uint32_t*>(sv + C);  // p_j | found << 31
-  uint32_t* scnt = sp + C;                          // cnt[p], then inclusive shift(i); [T + 1]
+  constexpr uint32_t T = kSpTile, NT = kSpThreads, IT = kSpItems, C = kSpChunk, JT = C / NT;
+  __shared__ uint32_t scnt[T + 1];  // cnt[p], then the inclusive shift(i)
   __shared__ uint32_t s_warp[NT / 32 + 1];
-  __shared__ uint32_t s_tile;
-  __shared__ uint64_t s_E;
-  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);  // in launch order: look-back predecessors run first
-  __syncthreads();
-  const uint64_t t = s_tile;
-  if (t >= ntiles) return;
+  const unsigned lane = lane_id();
+  const uint64_t t = blockIdx.x;
   const uint64_t a = t * T;
   const uint32_t na = (uint32_t)umin64(T, nA - a);
-  const uint64_t lo = part[t], hi = part[t + 1];
-  const uint64_t nb = hi - lo;
-  const bool has_prev = a > 0;
-  // stage the tile, zero the counts
+  const uint64_t lo = part[t], nb = part[t + 1] - lo;
+  const uint64_t E = lo - excl[t];  // new values of earlier tiles
+  const uint64_t base = a + E;
+  for (uint32_t i = threadIdx.x; i <= T; i += NT) scnt[i] = 0;
+  // the tile's U_M values (registers; the copy needs no staging)
+  K v[IT];
 #pragma unroll
   for (uint32_t r = 0; r < IT; ++r) {
     const uint32_t i = threadIdx.x + r * NT;
-    if (i < na) sk[1 + i] = KT::load(A, a + i);
+    if (i < na) v[r] = KT::load(A, a + i);
   }
-  if (threadIdx.x == 0 && has_prev) sk[0] = KT::load(A, a - 1);
-  for (uint32_t i = threadIdx.x; i <= T; i += NT) scnt[i] = 0;
   __syncthreads();
-  auto rank_in_tile = [&](const K& v, uint32_t& p, bool& found) {
-    uint32_t l = 0, h = na;  // #{tile A < v}
-    while (l < h) {
-      const uint32_t m = (l + h) >> 1;
-      if (KT::lt(sk[1 + m], v)) l = m + 1; else h = m;
-    }
-    p = l;
-    found = l < na && KT::eq(sk[1 + l], v);
-  };
-  // pass 1: rank the slice, count the new values per insertion position
-  const bool one_chunk = nb <= C;
-  for (uint64_t c0 = 0; c0 < nb; c0 += C) {
-    const uint32_t cn = (uint32_t)umin64(C, nb - c0);
-    for (uint32_t j = threadIdx.x; j < cn; j += NT) sv[j] = KT::load(B, lo + c0 + j);
-    __syncthreads();
-    for (uint32_t j = threadIdx.x; j < cn; j += NT) {
-      uint32_t p;
-      bool f;
-      rank_in_tile(sv[j], p, f);
-      if (!f) atomicAdd(&scnt[p], 1u);
-      sp[j] = p | (f ? 0x80000000u : 0u);
-    }
-    __syncthreads();
+  for (uint64_t j = threadIdx.x; j < nb; j += NT) {
+    const uint32_t w = pf[lo + j];
+    if (!(w >> 31)) atomicAdd(&scnt[w], 1u);
   }
-  // inclusive prefix over positions [0, na); n_t adds the values past the tile's end (p = na)
-  uint32_t n_t;
-  {
+  __syncthreads();
+  {  // inclusive prefix over positions [0, na)
     const uint32_t i0 = threadIdx.x * IT;
-    uint32_t v[IT], sum = 0;
+    uint32_t c[IT], sum = 0;
 #pragma unroll
     for (uint32_t r = 0; r < IT; ++r) {
-      v[r] = i0 + r < na ? scnt[i0 + r] : 0u;
-      sum += v[r];
+      c[r] = i0 + r < na ? scnt[i0 + r] : 0u;
+      sum += c[r];
     }
-    const uint32_t tail = scnt[na];
     uint32_t tot;
     uint32_t run = block_exclusive_scan<NT>(sum, s_warp, tot);
 #pragma unroll
     for (uint32_t r = 0; r < IT; ++r) {
-      run += v[r];
+      run += c[r];
       if (i0 + r < na) scnt[i0 + r] = run;
     }
-    n_t = tot + tail;
-  }
-  if (warp == 0) {
-    const uint64_t e = lookback_exclusive(status, t, n_t);
-    if (lane == 0) s_E = e;
   }
   __syncthreads();
-  const uint64_t E = s_E;
-  const uint64_t base = a + E;  // U' index of the tile's first U_M element, before insertions
   const uint32_t bmask = (1u << xs) - 1;
-  // U_M elements: copy with gaps
   bool unsorted = false;
 #pragma unroll
   for (uint32_t r = 0; r < IT; ++r) {
     const uint32_t i = threadIdx.x + r * NT;
-    if (i >= na) break;
+    // predecessor for the sortedness check: the lane below, or a load at warp edges
+    // (every lane shuffles: no lane leaves the loop early)
+    const K prev_l = KT::shfl_up(v[r], 1);
+    if (i >= na) continue;
     const uint32_t sh = scnt[i];
     const uint64_t out = base + i + sh;
-    const K v = sk[1 + i];
-    KT::store(U, out, v);
+    KT::store(U, out, v[r]);
     if (XM) XM[a + i] = (uint32_t)out;
     if (rblk) {  // XC block samples R(g) = X_M[2^xs g] - 2^xs g
       if (((a + i) & bmask) == 0) rblk[(a + i) >> xs] = (uint32_t)(E + sh);
       if (a + i == nA - 1) rblk[(nA + bmask) >> xs] = (uint32_t)(E + sh);
     }
-    if ((i > 0 || has_prev) && !KT::lt(sk[i], v)) unsorted = true;
+    if (a + i > 0) {
+      const K prev = lane > 0 ? prev_l : KT::load(A, a + i - 1);
+      if (!KT::lt(prev, v[r])) unsorted = true;
+    }
   }
   if (__any_sync(FULL, unsorted) && lane == 0) atomicMin(&hdr->status, (int)DM_E_UNSORTED);
-  // pass 2: the slice -- new values into their slots, X_D for all
+  // the slice: new values into their slots, X_D for all (blocked chunks of C for the new-rank scan)
   uint32_t run_new = 0;
   for (uint64_t c0 = 0; c0 < nb; c0 += C) {
     const uint32_t cn = (uint32_t)umin64(C, nb - c0);
-    if (!one_chunk) {
-      __syncthreads();
-      for (uint32_t j = threadIdx.x; j < cn; j += NT) {
-        sv[j] = KT::load(B, lo + c0 + j);
-      }
-      __syncthreads();
-      for (uint32_t j = threadIdx.x; j < cn; j += NT) {
-        uint32_t p;
-        bool f;
-        rank_in_tile(sv[j], p, f);
-        sp[j] = p | (f ? 0x80000000u : 0u);
-      }
-      __syncthreads();
-    }
-    // blocked: thread k owns chunk entries [k IT', (k + 1) IT') for the new-rank scan
-    constexpr uint32_t JT = C / NT;
     const uint32_t j0 = threadIdx.x * JT;
-    uint32_t cntn = 0;
+    uint32_t w[JT], cntn = 0;
 #pragma unroll
-    for (uint32_t r = 0; r < JT; ++r)
-      if (j0 + r < cn && !(sp[j0 + r] >> 31)) ++cntn;
+    for (uint32_t r = 0; r < JT; ++r) {
+      w[r] = j0 + r < cn ? pf[lo + c0 + j0 + r] : 0x80000000u;
+      cntn += (w[r] >> 31) ? 0u : 1u;
+    }
     uint32_t tot;
     uint32_t nr = run_new + block_exclusive_scan<NT>(cntn, s_warp, tot);
 #pragma unroll
     for (uint32_t r = 0; r < JT; ++r) {
       const uint32_t j = j0 + r;
       if (j >= cn) break;
-      const uint32_t w = sp[j], p = w & 0x7fffffffu;
-      if (w >> 31) {  // duplicate: its U_M twin's index
+      const uint32_t p = w[r] & 0x7fffffffu;
+      if (w[r] >> 31) {  // duplicate: its U_M twin's index
         XD[lo + c0 + j] = (uint32_t)(base + p + scnt[p]);
       } else {
         const uint64_t u = base + p + nr;
-        KT::store(U, u, sv[j]);
+        KT::store(U, u, KT::load(B, lo + c0 + j));
         XD[lo + c0 + j] = (uint32_t)u;
         if (offs) offs[E + nr] = (uint8_t)((a + p - 1) & bmask);
         ++nr;
       }
     }
     run_new += tot;
-  }
-  if (t == ntiles - 1 && threadIdx.x == 0) {
-    const uint64_t m = nA + E + n_t;
-    hdr->merged_dict_len = m;
-    hdr->merged_bits = dev_width(m);
-    if (m > (1ull << 32)) atomicMin(&hdr->status, (int)DM_E_TOO_WIDE);
   }
 }
 
@@ -956,11 +950,15 @@ cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, const void*
     const uint64_t ntiles = (in->dict_len + kSpTile - 1) / kSpTile;
     launch_k(k_sp_partition<KT>, (unsigned)((ntiles + 1 + 7) / 8), 256, 0, st, in->main_dict, in->dict_len, udict, hdr,
                                                                         ntiles, part);
-    const size_t smem = sizeof(K) * (kSpTile + 1 + kSpChunk) + sizeof(uint32_t) * (kSpChunk + kSpTile + 1);
-    ensure_smem((const void*)k_sp_merge<KT>, true);
-    launch_k(k_sp_merge<KT>, (unsigned)ntiles, kSpThreads, smem, st, in->main_dict, in->dict_len, udict, part, ntiles,
-                                                                status, counter, U, xm_w, xd, hdr, rblk, offs, xs);
-    note_launch(2);
+    uint32_t* pf = reinterpret_cast<uint32_t*>(ws + L.vals0);  // Step 1(a) scratch, free by now (>= N_D u32)
+    launch_k(k_sp_count<KT>, (unsigned)ntiles, kSpThreads, sizeof(K) * kSpTile, st, in->main_dict, in->dict_len, udict,
+                                                              part, ntiles, pf, cnt);
+    launch_k(k_scan_counts, (unsigned)((ntiles + 2047) / 2048), 256, 0, st, cnt, ntiles, excl, status, counter,
+                                                                  in->dict_len, hdr);
+    launch_k(k_sp_write<KT>, (unsigned)ntiles, kSpThreads, 0, st, in->main_dict, in->dict_len, udict, part, ntiles,
+                                                              (const uint32_t*)pf, (const uint64_t*)excl, U, xm_w, xd,
+                                                              hdr, rblk, offs, xs);
+    note_launch(4);
   } else if (variant == 0 || variant == 2) {  // lean tiles: two passes (default) or single pass
     launch_k(k_partition<KT>, (unsigned)((nt + 1 + 7) / 8), 256, 0, st, in->main_dict, in->dict_len, udict, hdr, nt + 1,
                                                                      part);

@@ -78,6 +78,7 @@ struct KeyU64 {
   __device__ __forceinline__ static bool lt(K a, K b) { return a < b; }
   __device__ __forceinline__ static bool eq(K a, K b) { return a == b; }
   __device__ __forceinline__ static bool le(K a, K b) { return a <= b; }
+  __device__ __forceinline__ static K shfl_up(K v, unsigned d) { return __shfl_up_sync(0xffffffffu, v, d); }
   // raw input and numeric workspace layouts coincide for u64 keys
   __device__ __forceinline__ static K ld_any(const void* p, uint64_t i, bool /*raw*/) {
     return static_cast<const uint64_t*>(p)[i];
@@ -101,6 +102,7 @@ struct KeyU32 {
   __device__ __forceinline__ static bool lt(K a, K b) { return a < b; }
   __device__ __forceinline__ static bool eq(K a, K b) { return a == b; }
   __device__ __forceinline__ static bool le(K a, K b) { return a <= b; }
+  __device__ __forceinline__ static K shfl_up(K v, unsigned d) { return __shfl_up_sync(0xffffffffu, v, d); }
   __device__ __forceinline__ static K ld_any(const void* p, uint64_t i, bool /*raw*/) {
     return static_cast<const uint32_t*>(p)[i];
   }
@@ -135,6 +137,9 @@ struct KeyB16 {
   }
   __device__ __forceinline__ static bool lt(K a, K b) { return a.hi < b.hi || (a.hi == b.hi && a.lo < b.lo); }
   __device__ __forceinline__ static bool eq(K a, K b) { return a.hi == b.hi && a.lo == b.lo; }
+  __device__ __forceinline__ static K shfl_up(K v, unsigned d) {
+    return K128{__shfl_up_sync(0xffffffffu, v.hi, d), __shfl_up_sync(0xffffffffu, v.lo, d)};
+  }
   __device__ __forceinline__ static bool le(K a, K b) { return !lt(b, a); }
   // one 16-byte load; raw (input) layout converted to the numeric (hi, lo) form
   __device__ __forceinline__ static K ld_any(const void* p, uint64_t i, bool raw) {
