@@ -367,12 +367,18 @@ dm_status dm_merge_column_host(dm_ctx* ctx, const dm_column_in* in, dm_column_ou
  *   bitmap-slot tiles in one pass with decoupled look-back; 3 sparse-delta
  *   tiles always (|U_M| > 0): U_M tiles of 2048 with the U_D values that fall
  *   into them, one pass (copy U_M with gaps, insert the new values).
- * knob 2 = Step 1(a) front end: 0 (default) auto -- hash
- *   deduplication of D before the sort for 16-byte keys with N_D >= 65536, and
- *   for bucket-path deltas with N_D > 4 |U_M| (they must repeat values);
- *   1 never; 2 always.  Insert every tuple into a device hash table, sort only
- *   the distinct values, map each tuple to its value's rank (same U_D and r).
- *   Changes the workspace size: call dm_workspace_bytes after setting it.
+ * knob 2 = Step 1(a) front end: 0 (default) auto --
+ *   probe-first for 16-byte keys with N_D >= 65536 and |U_M| * 16 <= 64 MB when
+ *   no U_D / X_D / r output is requested, else hash deduplication of D before
+ *   the sort for 16-byte keys with N_D >= 65536 and for bucket-path deltas with
+ *   N_D > 4 |U_M| (they must repeat values); 1 neither; 2 hash deduplication
+ *   always (insert every tuple into a device hash table, sort only the distinct
+ *   values, map each tuple to its value's rank: same U_D and r); 3 probe-first
+ *   whenever |U_M| > 0 and no U_D / X_D / r output is requested (look every
+ *   delta value up in U_M -- binary search -- and sort only the values not
+ *   found: U' = merge(U_M, U_new), a found value's code is X_M at its U_M
+ *   position; |U_D| is still reported).  Changes the workspace size:
+ *   call dm_workspace_bytes after setting it.
  * knob 3 = Step 2(b) variant: 0 (default) the optimized recompression through
  *   X_M / X_D (Eq 11); 1 the paper's unoptimized form:
  *   every tuple's value binary-searched in U' -- a measured baseline only.

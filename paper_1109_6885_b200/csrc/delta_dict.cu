@@ -671,6 +671,91 @@ __global__ void __launch_bounds__(256) k_dedup_insert(const void* __restrict__ D
   }
 }
 
+// ---------------------------------------------------------- probe-first (NEXT1)
+// "The delta partition's dictionary U_D ... is merged with U_M": a
+// delta value already in U_M needs no sorting -- its new code is X_M at its U_M
+// position.  U_M's positions go into an open-addressing table keyed by value
+// (k_pf_build; U_M is distinct, so inserts never contend), then every tuple
+// probes it (k_pf_probe): the table and U_M are read-only by then, so the probes
+// go through L1 and a skewed reuse (cfg3's Zipf) hits cache instead of hammering
+// one hash slot.  Found -> src = position (and its bit in the "used" bitmap, for
+// |U_D|); not found -> compacted (warp-aggregated atomic) into the keys Step
+// 1(a)'s sort sees.  (A binary search of U_M with a shared-memory sample was
+// measured first: ~10 dependent L2 round trips per tuple, 0.60 ms on cfg3.)
+constexpr uint32_t kPfEmpty = 0xffffffffu;
+template <class KT>
+__global__ void __launch_bounds__(256) k_pf_build(const void* __restrict__ UM, uint64_t nM, uint32_t* __restrict__ table,
+                                                  uint64_t mask) {
+  pdl_prologue();
+  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < nM; p += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t slot = (dd_hash(KT::load(UM, p)) >> 32) & mask;
+    while (atomicCAS(table + slot, kPfEmpty, (uint32_t)p) != kPfEmpty) slot = (slot + 1) & mask;
+  }
+}
+
+template <class KT>
+__global__ void __launch_bounds__(256) k_pf_probe(const void* __restrict__ UM, const uint32_t* __restrict__ table,
+                                                  uint64_t mask, const void* __restrict__ D, uint64_t n,
+                                                  uint32_t* __restrict__ src, void* __restrict__ newkeys,
+                                                  unsigned long long* n_new, uint32_t* __restrict__ used) {
+  pdl_prologue();
+  using K = typename KT::K;
+  const unsigned lane = lane_id();
+  const uint64_t n_round = (n + 31) & ~31ull;  // whole warps iterate together (warp-aggregated atomics)
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n_round;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const bool live = i < n;
+    K v{};
+    uint32_t p = kPfEmpty;
+    if (live) {
+      v = KT::load(D, i);
+      uint64_t slot = (dd_hash(v) >> 32) & mask;
+      for (;;) {
+        const uint32_t q = __ldg(table + slot);
+        if (q == kPfEmpty || KT::eq(KT::load(UM, q), v)) {
+          p = q;
+          break;
+        }
+        slot = (slot + 1) & mask;
+      }
+    }
+    const bool found = p != kPfEmpty;
+    const unsigned newmask = __ballot_sync(FULL, live && !found);
+    unsigned long long base = 0;
+    if (lane == 0 && newmask) base = atomicAdd(n_new, (unsigned long long)__popc(newmask));
+    base = __shfl_sync(FULL, base, 0);
+    if (live) {
+      if (found) {
+        src[i] = p;
+        atomicOr(&used[p >> 5], 1u << (p & 31));
+      } else {
+        const uint64_t j = base + __popc(newmask & lanemask_lt());
+        KT::store(newkeys, j, v);
+        src[i] = kPfNew | (uint32_t)j;
+      }
+    }
+  }
+}
+
+// After Step 1(b) over (U_M, U_new): the tuples' final codes, and |U_D| = |U_new|
+// + #distinct found values (the used bitmap's population, block-reduced).
+__global__ void __launch_bounds__(256) k_pf_codes(const uint32_t* __restrict__ src, uint64_t n,
+                                                  const uint32_t* __restrict__ rank_new,
+                                                  const uint32_t* __restrict__ xm, const uint32_t* __restrict__ xd,
+                                                  uint32_t* __restrict__ codes, const uint32_t* __restrict__ used,
+                                                  uint64_t nwords, dm_header* hdr) {
+  pdl_prologue();
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint32_t s = src[i];
+    codes[i] = (s & kPfNew) ? __ldg(xd + __ldg(rank_new + (s & ~kPfNew))) : __ldg(xm + s);
+  }
+  uint32_t c = 0;
+  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nwords; w += stride) c += __popc(used[w]);
+  c = warp_sum<uint32_t>(c);
+  if (lane_id() == 0 && c) atomicAdd(reinterpret_cast<unsigned long long*>(&hdr->delta_dict_len), (unsigned long long)c);
+}
+
 // r[k] = rank of tuple k's distinct value = rank_of_id[tid[k]].
 __global__ void __launch_bounds__(256) k_dedup_ranks(const uint32_t* __restrict__ tid,
                                                      const uint32_t* __restrict__ rank_of_id, uint64_t n,
@@ -699,7 +784,7 @@ void launch_passes(const void* D, uint64_t n, const unsigned long long* n_dev, c
 
 template <class KT>
 cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, void* udict, uint32_t* rank, dm_header* hdr,
-                cudaStream_t st) {
+                cudaStream_t st, bool probe) {
   const uint64_t n = in->n_delta;
   uint32_t* counters = reinterpret_cast<uint32_t*>(ws + L.counters);
   uint32_t* hist = reinterpret_cast<uint32_t*>(ws + L.hist);
@@ -709,7 +794,22 @@ cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, void* udict
   const void* D = in->delta;
   const unsigned long long* n_dev = nullptr;
   uint32_t* sort_rank = rank;
-  if (L.dedup) {
+  if (probe) {  // NEXT1: only the values not in U_M are sorted
+    unsigned long long* n_new = reinterpret_cast<unsigned long long*>(counters + CNT_PROBE);
+    const int sms = device_sms();
+    uint32_t* table = reinterpret_cast<uint32_t*>(ws + L.pf_table);
+    cudaMemsetAsync(table, 0xff, L.pf_cap * 4, st);
+    launch_k(k_pf_build<KT>, (unsigned)std::min<uint64_t>((in->dict_len + 255) / 256, (uint64_t)sms * 8), 256, 0, st,
+             in->main_dict, in->dict_len, table, L.pf_cap - 1);
+    launch_k(k_pf_probe<KT>, (unsigned)std::min<uint64_t>((n + 255) / 256, (uint64_t)sms * 8), 256, 0, st,
+             in->main_dict, (const uint32_t*)table, L.pf_cap - 1, in->delta, n,
+             reinterpret_cast<uint32_t*>(ws + L.pf_src), (void*)(ws + L.pf_keys), n_new,
+             reinterpret_cast<uint32_t*>(ws + L.pf_used));
+    note_launch(2);
+    D = ws + L.pf_keys;
+    n_dev = n_new;
+    sort_rank = reinterpret_cast<uint32_t*>(ws + L.pf_rank);
+  } else if (L.dedup) {
     unsigned long long* n_dist = reinterpret_cast<unsigned long long*>(counters + CNT_DEDUP);
     const int sms = device_sms();
     launch_k(k_dedup_insert<KT>, (unsigned)std::min<uint64_t>((n + 255) / 256, (uint64_t)sms * 8), 256, 0, st, 
@@ -759,7 +859,7 @@ cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, void* udict
       reinterpret_cast<const uint32_t*>(ws + L.vals1), n, n_dev, plan,
       reinterpret_cast<uint64_t*>(ws + L.status_unique), counters + CNT_UNIQUE, udict, sort_rank, hdr);
   note_launch();
-  if (L.dedup) {
+  if (L.dedup && !probe) {
     const int sms = device_sms();
     launch_k(k_dedup_ranks, (unsigned)std::min<uint64_t>((n + 255) / 256, (uint64_t)sms * 8), 256, 0, st, 
         reinterpret_cast<const uint32_t*>(ws + L.dd_tid), sort_rank, n, rank);
@@ -771,13 +871,26 @@ cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, void* udict
 }  // namespace
 
 cudaError_t launch_delta_dictionary(const dm_column_in* in, char* ws, const WsLayout& L, void* udict, uint32_t* rank,
-                                    dm_header* hdr, cudaStream_t st) {
+                                    dm_header* hdr, cudaStream_t st, bool probe) {
   if (in->n_delta == 0) return cudaSuccess;
   switch (in->key) {
-    case DM_KEY_U64: return run<KeyU64>(in, ws, L, udict, rank, hdr, st);
-    case DM_KEY_U32: return run<KeyU32>(in, ws, L, udict, rank, hdr, st);
-    default: return run<KeyB16>(in, ws, L, udict, rank, hdr, st);
+    case DM_KEY_U64: return run<KeyU64>(in, ws, L, udict, rank, hdr, st, probe);
+    case DM_KEY_U32: return run<KeyU32>(in, ws, L, udict, rank, hdr, st, probe);
+    default: return run<KeyB16>(in, ws, L, udict, rank, hdr, st, probe);
   }
+}
+
+cudaError_t launch_probe_codes(const dm_column_in* in, char* ws, const WsLayout& L, const uint32_t* xm,
+                               const uint32_t* xd, dm_header* hdr, cudaStream_t st) {
+  if (in->n_delta == 0) return cudaSuccess;
+  const uint64_t nwords = (in->dict_len + 31) / 32;
+  const unsigned g = (unsigned)std::max<uint64_t>(
+      1, std::min<uint64_t>((std::max<uint64_t>(in->n_delta, nwords) + 255) / 256, (uint64_t)device_sms() * 8));
+  launch_k(k_pf_codes, g, 256, 0, st, reinterpret_cast<const uint32_t*>(ws + L.pf_src), in->n_delta,
+           reinterpret_cast<const uint32_t*>(ws + L.pf_rank), xm, xd, reinterpret_cast<uint32_t*>(ws + L.pf_codes),
+           reinterpret_cast<const uint32_t*>(ws + L.pf_used), nwords, hdr);
+  note_launch();
+  return cudaGetLastError();
 }
 
 }  // namespace dm

@@ -1026,11 +1026,12 @@ cudaError_t launch_xc_exceptions(bool gather, const uint2* rec, uint64_t nsb, ui
 
 cudaError_t launch_dictionary_merge(const dm_column_in* in, const dm_column_out* out, char* ws, const WsLayout& L,
                                     const void* udict, uint32_t* xm, uint32_t* xd, dm_header* hdr, cudaStream_t st,
-                                    bool force_xc) {
+                                    bool force_xc, bool need_xm) {
+  const bool want_xm = out->x_main != nullptr || need_xm;
   switch (in->key) {
-    case DM_KEY_U64: return run<KeyU64>(in, ws, L, udict, out->merged_dict, xm, xd, hdr, st, force_xc, out->x_main != nullptr);
-    case DM_KEY_U32: return run<KeyU32>(in, ws, L, udict, out->merged_dict, xm, xd, hdr, st, force_xc, out->x_main != nullptr);
-    default: return run<KeyB16>(in, ws, L, udict, out->merged_dict, xm, xd, hdr, st, force_xc, out->x_main != nullptr);
+    case DM_KEY_U64: return run<KeyU64>(in, ws, L, udict, out->merged_dict, xm, xd, hdr, st, force_xc, want_xm);
+    case DM_KEY_U32: return run<KeyU32>(in, ws, L, udict, out->merged_dict, xm, xd, hdr, st, force_xc, want_xm);
+    default: return run<KeyB16>(in, ws, L, udict, out->merged_dict, xm, xd, hdr, st, force_xc, want_xm);
   }
 }
 

@@ -157,6 +157,7 @@ WsLayout ws_layout(const dm_column_in* in) {
     L.bk_state = take(sizeof(BucketState));
     L.bk_status = take(((1ull << L.bk_bits) / (256 * kBkScanItems) + 1) * sizeof(uint64_t));
   }
+  if (probe_possible(in)) L.pf_used = take(((in->dict_len + 31) / 32) * 4);
   L.zero_bytes = o;
   L.plan = take(sizeof(SortPlan));
   L.keys0 = take(nD * E);
@@ -177,6 +178,17 @@ WsLayout ws_layout(const dm_column_in* in) {
     L.bk_off = take(((1ull << L.bk_bits) + 1) * 4);
     if (E <= 8) L.bk_pairs = take(nD * 16);
     L.bk_cur = take((1ull << L.bk_bits) * 4);
+  }
+  L.probe = probe_possible(in);
+  if (L.probe) {
+    L.pf_src = take(nD * 4);
+    L.pf_keys = take(nD * E);
+    L.pf_rank = take(nD * 4);
+    L.pf_codes = take(nD * 4);
+    uint64_t cap = 1024;
+    while (cap < 2 * in->dict_len) cap <<= 1;
+    L.pf_cap = cap;
+    L.pf_table = take(cap * 4);
   }
   L.dedup = dedup_wanted(in);
   if (L.dedup) {
@@ -277,25 +289,30 @@ static dm_status merge_async(const dm_column_in* in, const dm_column_out* out, v
   // Step 1(a): delta dictionary U_D and ranks r -- or, for a
   // delta that already is U_D (the paper reads it off the CSB+ tree's leaves,
   // P:190), just its length.
+  // probe-first (NEXT1) only when nobody asked for U_D / X_D / r, whose index space it skips
+  const bool probe = L.probe && mode == MM_FULL && !out->delta_dict && !out->x_delta && !out->delta_rank;
   if (mode == MM_SORTED_DICT) {
     udict = const_cast<void*>(in->delta);
     if ((e = launch_set_delta_len(d_header, in->n_delta, st)) != cudaSuccess) return cuda_fail(e);
-  } else if ((e = launch_delta_dictionary(in, w, L, udict, rank, d_header, st)) != cudaSuccess) {
+  } else if ((e = launch_delta_dictionary(in, w, L, udict, rank, d_header, st, probe)) != cudaSuccess) {
     return cuda_fail(e);
   }
   if ((e = dbg("step 1(a)")) != cudaSuccess) return cuda_fail(e);
   mark(1);
   if (mode == MM_DELTA) return DM_OK;
   // Step 1(b) + 2(a): U', X_M, X_D, b' (Eq 4).
-  if ((e = launch_dictionary_merge(in, out, w, L, udict, xm, xd, d_header, st, !with_step2)) != cudaSuccess)
+  // (probe-first needs the plain X_M: the found tuples' codes come from it)
+  if ((e = launch_dictionary_merge(in, out, w, L, udict, xm, xd, d_header, st, !with_step2, probe)) != cudaSuccess)
     return cuda_fail(e);
+  if (probe && (e = launch_probe_codes(in, w, L, xm, xd, d_header, st)) != cudaSuccess) return cuda_fail(e);
   if ((e = dbg("step 1(b)")) != cudaSuccess) return cuda_fail(e);
   mark(2);
   // Step 2(b): M' (Eq 11).
   const bool xc = xc_wanted(in);
   if (with_step2 && tuning(3) == 1) {
     if ((e = launch_naive_step2(in, out, d_header, st)) != cudaSuccess) return cuda_fail(e);
-  } else if (with_step2 && (e = launch_recompress(in, out, xm, xd, rank, d_header, st, 0,
+  } else if (with_step2 && (e = launch_recompress(in, out, xm, probe ? reinterpret_cast<const uint32_t*>(w + L.pf_codes) : xd,
+                                                  probe ? nullptr : rank, d_header, st, 0,
                                            xc ? reinterpret_cast<const uint2*>(w + L.xc_rec) : nullptr,
                                            xc ? reinterpret_cast<const uint8_t*>(w + L.xc_offs) : nullptr,
                                            xc_shift(in))) !=
@@ -387,7 +404,7 @@ struct dm_ctx {
 extern "C" {
 
 int dm_set_tuning(int knob, int value) {
-  static const int hi[6] = {3, 3, 2, 1, 8, 2};
+  static const int hi[6] = {3, 3, 3, 1, 8, 2};
   if (knob < 0 || knob > 5 || value < 0 || value > hi[knob]) return DM_E_INVALID;
   if (knob == 4 && value != 0 && value != 7 && value != 8) return DM_E_INVALID;
   g_tuning[knob].store(value);

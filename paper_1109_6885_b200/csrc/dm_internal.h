@@ -89,13 +89,25 @@ inline uint32_t bucket_bits(uint64_t n) {
 }
 inline bool dedup_wanted(const dm_column_in* in) {
   const int k = tuning(2);
-  if (in->n_delta == 0 || k == 1) return false;
+  if (in->n_delta == 0 || k == 1 || k == 3) return false;
   // 16-byte keys with many tuples (16 radix passes), or -- for the bucket path,
   // whose buckets must stay small -- a delta that must repeat values heavily
   // (at most |U_M| of its distinct values can be old ones)
   return k == 2 || (in->key == DM_KEY_B16 && in->n_delta >= (1u << 16)) ||
          (bucket_wanted(in) && in->dict_len * 4 < in->n_delta);
 }
+// Probe-first Step 1(a) (knob 2 = 3; auto for 16-byte keys with
+// N_D >= 2^16 and U_M <= 64 MB): every delta value is first looked up in U_M
+// (a hash table of U_M's positions, read-only while probed); only the values
+// not found are sorted into U_new, and U' = merge(U_M, U_new).  Runs only when
+// the caller asked for none of U_D / X_D / r (their index space is U_D's).
+constexpr uint32_t kPfNew = 0x80000000u;
+inline bool probe_possible(const dm_column_in* in) {
+  const int k = tuning(2);
+  if (in->n_delta == 0 || in->dict_len == 0 || k == 1 || k == 2) return false;
+  return k == 3 || (in->key == DM_KEY_B16 && in->n_delta >= (1u << 16) && in->dict_len * 16 <= (64ull << 20));
+}
+
 // Block shift: 256-code blocks when N_D / |U_M| promises <= 6 entries per block
 // (and always for the shared-memory variant, knob 2), else 128-code blocks.
 int xc_shift_override();  // knob 4 / DM_XC_SHIFT: 7 or 8, 0 = none
@@ -160,6 +172,14 @@ struct WsLayout {
   size_t xc_rblk;        // XC: u32[nblk + 1], new values inserted before each 256-block
   size_t xc_rec;         // XC: uint2[nsb] superblock records
   size_t xc_offs;        // XC: u8[n_delta] insertion position mod 256 per new value
+  size_t pf_used;        // probe-first (NEXT1): bitmap over U_M positions hit by the delta (zeroed region)
+  size_t pf_src;         // probe-first: u32[n_delta] per tuple: U_M position, or kPfNew | compacted index
+  size_t pf_keys;        // probe-first: the delta values not found in U_M (raw layout), n_delta capacity
+  size_t pf_rank;        // probe-first: u32[n_delta] rank of each compacted value among the new values
+  size_t pf_codes;       // probe-first: u32[n_delta] the delta tuples' final codes (Step 2(b) input)
+  size_t pf_table;       // probe-first: u32[pf_cap] U_M positions by value hash (0xff.. = empty)
+  uint64_t pf_cap;       // probe-first: table slots (power of two >= 2 |U_M|)
+  bool probe;            // probe-first buffers laid out (probe_possible)
   size_t dd_slots;       // dedup (NEXT1): u64[dd_cap] (tag | id << 32) slots (memset per call)
   size_t dd_keys;        // dedup: distinct values, raw layout, n_delta capacity
   size_t dd_tid;         // dedup: u32[n_delta] distinct id per tuple
@@ -178,7 +198,8 @@ struct WsLayout {
   int npass;
 };
 
-enum { CNT_SORT = 0, CNT_UNIQUE = 16, CNT_MERGE = 17, CNT_HIST = 18, CNT_DEDUP = 20 /* u64, 2 slots */, CNT_BKSCAN = 22 };
+enum { CNT_SORT = 0, CNT_UNIQUE = 16, CNT_MERGE = 17, CNT_HIST = 18, CNT_DEDUP = 20 /* u64, 2 slots */, CNT_BKSCAN = 22,
+       CNT_PROBE = 24 /* u64, 2 slots */ };
 
 WsLayout ws_layout(const dm_column_in* in);
 inline size_t key_bytes(int key) { return key == DM_KEY_U64 ? 8 : key == DM_KEY_U32 ? 4 : 16; }
@@ -214,14 +235,22 @@ cudaError_t last_error_check();
 
 // ---- kernel launchers (each .cu file)
 // Step 1(a): sort + unique of D -> U_D (udict), r (rank), hdr->delta_dict_len.
+// probe: the probe-first front end (L.probe, no U_D / X_D / r requested): U_new
+// into udict, the new values' ranks into L.pf_rank, hdr->delta_dict_len = |U_new|
+// until launch_probe_codes adds the distinct found values.
 cudaError_t launch_delta_dictionary(const dm_column_in* in, char* ws, const WsLayout& L, void* udict, uint32_t* rank,
-                                    dm_header* hdr, cudaStream_t st);
+                                    dm_header* hdr, cudaStream_t st, bool probe = false);
+// Probe-first, after Step 1(b): codes[k] = X_M[p] (found) or X_D[rank_new] (new);
+// hdr->delta_dict_len += #distinct found values (|U_D| = |U_new| + that).
+cudaError_t launch_probe_codes(const dm_column_in* in, char* ws, const WsLayout& L, const uint32_t* xm,
+                               const uint32_t* xd, dm_header* hdr, cudaStream_t st);
 // Step 1(b) + 2(a): merge-path merge -> U', X_M, X_D, hdr->merged_dict_len / merged_bits.
 // When xc_enabled(dict_len), also builds the compact table XC in the workspace.
 // force_xc: build XC whenever xc_enabled (the row-sharded root exports it).
+// need_xm: materialise X_M even where Step 2(b) would not read it (probe-first).
 cudaError_t launch_dictionary_merge(const dm_column_in* in, const dm_column_out* out, char* ws, const WsLayout& L,
                                     const void* udict, uint32_t* xm, uint32_t* xd, dm_header* hdr, cudaStream_t st,
-                                    bool force_xc = false);
+                                    bool force_xc = false, bool need_xm = false);
 // Step 2(b): recompress main through X_M and append delta through X_D.
 // fixed_bits != 0: b' given by the caller (dm_recompress); else read from hdr->merged_bits.
 // xc_rec / xc_offs: the compact table (NULL: plain X_M only).

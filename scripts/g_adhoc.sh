@@ -1,4 +1,4 @@
 set -u
 O=gpurun_out/$1; mkdir -p $O; shift
-timeout 900 python -m pytest tests/test_gpu_merge_variants.py tests/test_gpu_parity.py -x -q -k "variant or sparse or tile or cfg2 or cfg5" > $O/pytest.log 2>&1; echo "pytest rc=$?" >> $O/pytest.log; tail -3 $O/pytest.log
-bash scripts/quick_bench.sh cfg2 cfg5 | tee $O/quick.txt
+timeout 900 python -m pytest tests/test_gpu_merge_variants.py -x -q -k "probe or dedup" > $O/pytest.log 2>&1; echo "pytest rc=$?" >> $O/pytest.log; tail -3 $O/pytest.log
+bash scripts/quick_bench.sh cfg3 | tee $O/quick.txt

@@ -97,7 +97,7 @@ def test_tuning_knobs_validated_on_the_host():
     anything else is DM_E_INVALID.  Pure host logic (no GPU needed)."""
     import paper_1109_6885_b200 as dm
     L = dm._lib()
-    hi = {0: 3, 1: 3, 2: 2, 3: 1, 5: 2}
+    hi = {0: 3, 1: 3, 2: 3, 3: 1, 5: 2}
     try:
         for k, h in hi.items():
             for v in range(h + 1):

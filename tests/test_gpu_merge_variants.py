@@ -8,7 +8,7 @@ import torch
 
 import datagen
 import oracle
-from tests.parity import compare, run_gpu
+from tests.parity import compare, run_gpu, to_device
 
 pytestmark = pytest.mark.gpu
 
@@ -175,3 +175,47 @@ def test_naive_step2(key, case, _naive):
     col = datagen.make_random_case(97 + n_main, n_main, dict_len, n_delta, p_new, key=key)
     M, r = run_gpu(col)
     compare(col, M, r)
+
+
+# ------------------------------------------------- probe-first Step 1(a) (NEXT1)
+@pytest.fixture()
+def _reset_probe():
+    yield
+    import paper_1109_6885_b200 as dm
+    dm.set_tuning(2, 0)
+
+
+PROBE_CASES = [
+    # key, n_main, dict_len, n_delta, p_new
+    ("b16", 300_000, 40_000, 200_000, 0.2),   # cfg3-like: skewed reuse, some new
+    ("b16", 50_000, 3_000, 100_000, 0.0),     # every delta value already in U_M: nothing to sort
+    ("b16", 50_000, 3_000, 70_000, 1.0),      # all new
+    ("u64", 400_000, 100_000, 300_000, 0.3),
+    ("u32", 100_000, 20_000, 90_000, 0.5),
+    ("u64", 20_000, 1, 5_000, 0.5),           # one-entry dictionary
+]
+
+
+@pytest.mark.parametrize("case", PROBE_CASES)
+@pytest.mark.parametrize("knob", [3, 0])
+def test_probe_first_step1a(case, knob, _reset_probe):
+    """NEXT1 (knob 2 = 3, and auto for 16-byte keys): each delta value is looked up
+    in U_M first, only the values not found are sorted, U' = merge(U_M, U_new).
+    Active only when no U_D / X_D / r output is requested, so the merge runs
+    without tables; U', M', b', |U'| and |U_D| must match the oracle."""
+    import paper_1109_6885_b200 as dm
+    dm.set_tuning(2, knob)
+    key, n_main, dict_len, n_delta, p_new = case
+    col = datagen.make_random_case(4242 + n_delta, n_main, dict_len, n_delta, p_new, key=key)
+    UM, M, D = to_device(col)
+    r = dm.merge_column(UM, M, col.n_main, col.main_bits, D)
+    compare(col, M, r, check_tables=False)
+
+
+def test_probe_first_cfg3_scaled(_reset_probe):
+    import paper_1109_6885_b200 as dm
+    dm.set_tuning(2, 0)  # auto: cfg3 takes the probe-first front end
+    col = datagen.make_config(3, scale=0.05)
+    UM, M, D = to_device(col)
+    r = dm.merge_column(UM, M, col.n_main, col.main_bits, D)
+    compare(col, M, r, check_tables=False)
