@@ -24,7 +24,11 @@
 //                scan with look-back -> U_D[rank] and r[original index] = rank
 #include <algorithm>
 
+#include <cooperative_groups.h>
+
 #include "dm_device.cuh"
+
+namespace cg = cooperative_groups;
 
 #ifdef DM_TRACE
 __device__ unsigned long long dm_trace_buf[8 * 32];
@@ -117,22 +121,16 @@ __global__ void __launch_bounds__(256) k_hist(const void* __restrict__ D, uint64
 
 // One stable LSD radix pass over (key, original-index) pairs.  NT threads,
 // ITEMS keys per thread, tile = NT * ITEMS keys in (warp, item, lane) order.
+// One tile of one pass (claimed in order from `counter`); false once the tiles
+// run past n.  Shared by the per-pass kernel and the cooperative all-passes one.
 template <class KT, int NT, int ITEMS>
-__global__ void __launch_bounds__(NT) k_onesweep(const void* __restrict__ D, void* kbuf0, void* kbuf1,
-                                                uint32_t* vbuf0, uint32_t* vbuf1, uint64_t n_host,
-                                                const unsigned long long* __restrict__ n_dev, int pass,
-                                                const SortPlan* __restrict__ plan, uint32_t* status,
-                                                uint32_t* counter) {
-  pdl_prologue();
-  // n_dev: the key count is only known on the device (deduplicated delta); the
-  // grid covers n_host >= n and tiles past n exit (nothing waits on them)
-  const uint64_t n = n_dev ? (uint64_t)*n_dev : n_host;
+__device__ __forceinline__ bool onesweep_tile(const void* __restrict__ D, void* kbuf0, void* kbuf1, uint32_t* vbuf0,
+                                              uint32_t* vbuf1, uint64_t n, int pass,
+                                              const SortPlan* __restrict__ plan, uint32_t* status,
+                                              uint32_t* counter) {
   using K = typename KT::K;
   constexpr int W = NT / 32;
   constexpr int TILE = NT * ITEMS;
-  DM_T(0);
-  if (!plan->active[pass]) return;
-  DM_T(1);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   K* s_keys = reinterpret_cast<K*>(smem_raw);
   uint32_t* s_vals = reinterpret_cast<uint32_t*>(smem_raw + sizeof(K) * TILE);
@@ -150,7 +148,7 @@ __global__ void __launch_bounds__(NT) k_onesweep(const void* __restrict__ D, voi
   DM_T(2);
   const uint64_t tile = s_tile;
   const uint64_t base = tile * TILE;
-  if (base >= n) return;
+  if (base >= n) return false;
   const int src = plan->src[pass];
   const void* ksrc = src == SEL_BUF0 ? kbuf0 : kbuf1;
   const uint32_t* vsrc = src == SEL_BUF0 ? vbuf0 : vbuf1;
@@ -272,6 +270,47 @@ __global__ void __launch_bounds__(NT) k_onesweep(const void* __restrict__ D, voi
     vdst[dst] = s_vals[j];
   }
   DM_T(8);
+  __syncthreads();  // the shared tile is reused by the next claim
+  return true;
+}
+
+template <class KT, int NT, int ITEMS>
+__global__ void __launch_bounds__(NT) k_onesweep(const void* __restrict__ D, void* kbuf0, void* kbuf1,
+                                                uint32_t* vbuf0, uint32_t* vbuf1, uint64_t n_host,
+                                                const unsigned long long* __restrict__ n_dev, int pass,
+                                                const SortPlan* __restrict__ plan, uint32_t* status,
+                                                uint32_t* counter) {
+  pdl_prologue();
+  // n_dev: the key count is only known on the device (deduplicated delta); the
+  // grid covers n_host >= n and tiles past n exit (nothing waits on them)
+  const uint64_t n = n_dev ? (uint64_t)*n_dev : n_host;
+  DM_T(0);
+  if (!plan->active[pass]) return;
+  DM_T(1);
+  onesweep_tile<KT, NT, ITEMS>(D, kbuf0, kbuf1, vbuf0, vbuf1, n, pass, plan, status, counter);
+}
+
+// All LSD passes in one cooperative, persistent launch: the CTAs claim the tiles
+// of each active pass in order (the per-digit look-back needs every claimed
+// predecessor running -- a cooperative grid is co-resident) and meet at a grid
+// barrier between passes.  One launch instead of one per byte: the bucket path's
+// gated fallback (the passes only run when a bucket overflowed) then costs a
+// single early-exit launch per merge, not 8 or 16.
+template <class KT, int NT, int ITEMS>
+__global__ void __launch_bounds__(NT) k_onesweep_all(const void* __restrict__ D, void* kbuf0, void* kbuf1,
+                                                    uint32_t* vbuf0, uint32_t* vbuf1, uint64_t n_host,
+                                                    const unsigned long long* __restrict__ n_dev,
+                                                    const SortPlan* __restrict__ plan, uint32_t* status_base,
+                                                    uint64_t status_stride, uint32_t* counters) {
+  const uint64_t n = n_dev ? (uint64_t)*n_dev : n_host;
+  cg::grid_group grid = cg::this_grid();
+  for (int p = 0; p < KT::kPasses; ++p) {
+    if (!plan->active[p]) continue;  // uniform: every CTA reads the same plan
+    while (onesweep_tile<KT, NT, ITEMS>(D, kbuf0, kbuf1, vbuf0, vbuf1, n, p, plan,
+                                        status_base + (uint64_t)p * status_stride, counters + p)) {
+    }
+    grid.sync();
+  }
 }
 
 // Head flags + single-pass scan over the sorted keys -> U_D and r.
@@ -765,6 +804,15 @@ __global__ void __launch_bounds__(256) k_dedup_ranks(const uint32_t* __restrict_
     rank[i] = __ldg(rank_of_id + __ldg(tid + i));
 }
 
+// DM_SORT_COOP=0: one launch per pass (the round-1 form; experiments)
+bool onesweep_coop() {
+  static const bool v = [] {
+    const char* e = std::getenv("DM_SORT_COOP");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 template <class KT, int NT, int ITEMS>
 void launch_passes(const void* D, uint64_t n, const unsigned long long* n_dev, char* ws, const WsLayout& L,
                    SortPlan* plan, uint32_t* counters, cudaStream_t st) {
@@ -773,6 +821,28 @@ void launch_passes(const void* D, uint64_t n, const unsigned long long* n_dev, c
   const size_t dsmem = (sizeof(K) + sizeof(uint32_t)) * TILE;
   ensure_smem((const void*)k_onesweep<KT, NT, ITEMS>);
   const uint64_t ntiles = (n + TILE - 1) / TILE;
+  if (onesweep_coop()) {  // one cooperative launch for all passes
+    auto kern = k_onesweep_all<KT, NT, ITEMS>;
+    ensure_smem((const void*)kern);
+    const int occ = occupancy((const void*)kern, NT, dsmem);
+    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ntiles, (uint64_t)device_sms() * occ));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = NT;
+    cfg.dynamicSmemBytes = dsmem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, D, (void*)(ws + L.keys0), (void*)(ws + L.keys1),
+                       reinterpret_cast<uint32_t*>(ws + L.vals0), reinterpret_cast<uint32_t*>(ws + L.vals1), n,
+                       n_dev, (const SortPlan*)plan, reinterpret_cast<uint32_t*>(ws + L.status_sort),
+                       (uint64_t)ntiles * 256, counters + CNT_SORT);
+    note_launch();
+    return;
+  }
   for (int p = 0; p < KT::kPasses; ++p) {
     uint32_t* status = reinterpret_cast<uint32_t*>(ws + L.status_sort) + (uint64_t)p * ntiles * 256;
     launch_k(k_onesweep<KT, NT, ITEMS>, (unsigned)ntiles, NT, dsmem, st, 

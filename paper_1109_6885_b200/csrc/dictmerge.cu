@@ -13,6 +13,8 @@
 #include <tuple>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "dm_internal.h"
 
 namespace dm {
@@ -212,6 +214,19 @@ static dm_status cuda_fail(cudaError_t e) {
 }
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// One NVTX range at a time, popped on every exit path.
+struct NvtxSteps {
+  bool open = false;
+  void next(const char* name) {
+    if (open) nvtxRangePop();
+    open = name != nullptr;
+    if (open) nvtxRangePushA(name);
+  }
+  ~NvtxSteps() {
+    if (open) nvtxRangePop();
+  }
+};
 // Main codes index a dictionary: with N_M > 0, 1 <= |U_M| < 2^32 and b >= width(|U_M|)
 // (the recompress kernels clamp codes to |U_M| - 1, so |U_M| = 0 must not reach them).
 static bool main_dict_len_ok(uint64_t n_main, uint64_t dict_len, uint32_t main_bits) {
@@ -266,8 +281,14 @@ static dm_status merge_async(const dm_column_in* in, const dm_column_out* out, v
   if (!ws || ws_bytes < L.total) return DM_E_CAPACITY;
   if (!d_header || !aligned16(d_header)) return DM_E_INVALID;
   char* w = static_cast<char*>(ws);
+  // NVTX ranges per step (host enqueue spans; nsys / ncu timelines show them)
+  static const char* const kStepNames[3] = {"dm Step 1(a) delta dictionary (P:181, P:218-222)",
+                                            "dm Step 1(b) dictionary merge + 2(a) width (P:192, P:224-226, Eq 4)",
+                                            "dm Step 2(b) recompress (Eq 11, P:272)"};
+  NvtxSteps nv;
   auto mark = [&](int i) {
     if (events && events[i]) cudaEventRecord(static_cast<cudaEvent_t>(events[i]), st);
+    nv.next(i < 3 ? kStepNames[i] : nullptr);
   };
   mark(0);
   cudaError_t e = cudaMemsetAsync(w, 0, L.zero_bytes, st);
