@@ -487,10 +487,12 @@ def main():
     s2b = sum(step2_bytes(n_m, b, D.shape[0], UM.shape[0], r.merged_bits, r.delta_dict_len)
               for (UM, _, n_m, b, D), r in zip(dev_cols, results))
     traffic = None
+    tinfo = {}
     tp = os.path.join(ROOT, "profiles", "recompress_traffic.json")
     if os.path.exists(tp) and not table:
         try:
-            traffic = json.load(open(tp)).get(args.workload, {}).get("traffic_bytes_per_launch")
+            tinfo = json.load(open(tp)).get(args.workload, {})
+            traffic = tinfo.get("traffic_bytes_per_launch")
         except Exception:
             traffic = None
     if not table:
@@ -502,6 +504,19 @@ def main():
                     "algorithmic_bytes_per_launch": s2b,
                     "gather_bound_note": "X_M lookups: measured L2 random-gather ceiling 2.8e11/s "
                                          "(profiles/r01/microbench_gather.jsonl)"}
+        if tinfo.get("warp_instructions_per_launch"):
+            # the same kernel against the instruction-issue roofline: one warp instruction per
+            # cycle per SM sub-partition (148 SMs x 4) at the SM clock -- what bounds the
+            # shared-memory XC lookups of cfg2
+            clk_mhz = (pk or {}).get("sm_max_mhz", 1965.0)
+            ipeak = 148 * 4 * clk_mhz * 1e6
+            iach = tinfo["warp_instructions_per_launch"] / (s2_ms / 1e3)
+            roofline["issue"] = {"bound": "issue", "achieved": iach, "peak": ipeak, "unit": "warp-instructions/s",
+                                 "frac": iach / ipeak,
+                                 "warp_instructions_per_launch": tinfo["warp_instructions_per_launch"],
+                                 "ncu_issue_active_pct": tinfo.get("issue_active_pct"),
+                                 "source": "instruction count from ncu --set full of this kernel "
+                                           "(profiles/recompress_traffic.json), time from the events here"}
     else:
         achieved = sb / (ms_per_step / 1e3) / 1e9
         roofline = {"kernel": "whole table merge (all kernels, 300 columns)", "bound": "hbm", "achieved": achieved,

@@ -526,10 +526,12 @@ dm_status dm_merge_table_async(int ncols, const dm_column_in* in, const dm_colum
   for (int k = 0; k < K && e == cudaSuccess; ++k) e = cudaStreamWaitEvent(pool.streams[k], pool.fork, 0);
   if (e != cudaSuccess) return cuda_fail(e);
   dm_status bad = DM_OK;
+  set_table_merge(ncols > 1);
   for (int t = 0; t < ncols && bad == DM_OK; ++t) {
     const int c = order[t];
     bad = merge_async(&in[c], &out[c], ws[c], ws_bytes[c], hdrs[c], pool.streams[t % K], true);
   }
+  set_table_merge(false);
   // always join every forked stream back (an active graph capture must not end
   // with forked streams, even when a column failed to launch)
   for (int k = 0; k < K; ++k) {

@@ -261,6 +261,9 @@ cudaError_t launch_recompress(const dm_column_in* in, const dm_column_out* out, 
                               const uint32_t* xd, const uint32_t* rank, dm_header* hdr, cudaStream_t st,
                               uint32_t fixed_bits = 0, const uint2* xc_rec = nullptr,
                               const uint8_t* xc_offs = nullptr, uint32_t xc_shift = 8, bool xc_only = false);
+// dm_merge_table marks its launches (this thread) so Step 2(b) leaves SMs to
+// the other columns' kernels.
+void set_table_merge(bool on);
 // Step 2(b) of a row shard through XC read from L2 (dm_recompress_xc).
 cudaError_t launch_recompress_xc(const dm_column_in* in, const dm_column_out* out, const uint32_t* xm,
                                  const uint32_t* xd, const uint32_t* rank, dm_header* hdr, cudaStream_t st,

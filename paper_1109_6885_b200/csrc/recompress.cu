@@ -634,15 +634,18 @@ __global__ void __launch_bounds__(256) k_unpack(const uint32_t* __restrict__ wor
   }
 }
 
-// Share of the SM slots a recompress launch may take (DM_REC_GRID_PCT, 1..100;
-// experiments: a smaller share lets concurrent columns' Step 1 kernels co-run).
+// Share of the SM slots a recompress launch may take: all of them for one
+// column; a quarter inside dm_merge_table, where other columns' latency-bound
+// Step 1 kernels then co-run (cfg4: 15.3 -> 14.6 ms; 50%: 14.8 ms).
+// DM_REC_GRID_PCT (1..100) overrides both (experiments).
+static thread_local bool t_table_merge = false;
 static int rec_grid_percent() {
   static const int v = [] {
     const char* e = std::getenv("DM_REC_GRID_PCT");
-    const int x = e ? std::atoi(e) : 100;
-    return (x >= 1 && x <= 100) ? x : 100;
+    const int x = e ? std::atoi(e) : 0;
+    return (x >= 1 && x <= 100) ? x : 0;
   }();
-  return v;
+  return v ? v : t_table_merge ? 25 : 100;
 }
 
 // Shared-memory bytes left for XC next to a kRecStagesXc-deep ring.
@@ -735,6 +738,8 @@ constexpr auto make_table(std::integer_sequence<int, I...>) {
 }
 
 }  // namespace
+
+void set_table_merge(bool on) { t_table_merge = on; }
 
 cudaError_t launch_recompress(const dm_column_in* in, const dm_column_out* out, const uint32_t* xm,
                               const uint32_t* xd, const uint32_t* rank, dm_header* hdr, cudaStream_t st,

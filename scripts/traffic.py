@@ -48,9 +48,13 @@ def summarize():
             b = num("dram__bytes_read.sum") * scale("dram__bytes_read.sum") + \
                 num("dram__bytes_write.sum") * scale("dram__bytes_write.sum")
             if best is None or t > best[0]:
-                best = (t, b, d["Kernel Name"][:60])
+                inst = num("smsp__inst_executed.sum") if "smsp__inst_executed.sum" in d else None
+                issue = num("smsp__issue_active.avg.pct_of_peak_sustained_active") \
+                    if "smsp__issue_active.avg.pct_of_peak_sustained_active" in d else None
+                best = (t, b, d["Kernel Name"][:60], inst, issue)
         if best:
             res[w] = {"traffic_bytes_per_launch": best[1], "kernel_time_s_under_ncu": best[0], "kernel": best[2],
+                      "warp_instructions_per_launch": best[3], "issue_active_pct": best[4],
                       "source": f"ncu --set full (gpurun_out/{f}), longest k_recompress launch of one merge"}
     path = os.path.join(ROOT, "profiles", "recompress_traffic.json")
     json.dump(res, open(path, "w"), indent=1)
