@@ -251,6 +251,37 @@ def reference_arm(args, rank, world):
     return 0
 
 
+def pcie_bidirectional_gbs(dev, n=256 << 20):
+    """Concurrent H2D + D2H pinned copy rate (GB/s, both directions summed)."""
+    import torch
+    try:
+        h1 = torch.empty(n, dtype=torch.uint8).pin_memory()
+        h2 = torch.empty(n, dtype=torch.uint8).pin_memory()
+        d1 = torch.empty(n, dtype=torch.uint8, device=dev)
+        d2 = torch.empty(n, dtype=torch.uint8, device=dev)
+        s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        best = None
+        for _ in range(3):
+            torch.cuda.synchronize()
+            a.record()
+            s1.wait_event(a)
+            s2.wait_event(a)
+            with torch.cuda.stream(s1):
+                d1.copy_(h1, non_blocking=True)
+            with torch.cuda.stream(s2):
+                h2.copy_(d2, non_blocking=True)
+            torch.cuda.current_stream().wait_stream(s1)
+            torch.cuda.current_stream().wait_stream(s2)
+            b.record()
+            torch.cuda.synchronize()
+            t = a.elapsed_time(b) / 1e3
+            best = t if best is None else min(best, t)
+        return 2 * n / best / 1e9
+    except Exception:
+        return None
+
+
 # ----------------------------------------------------------- N > 1: one column row-sharded
 def sharded_inputs(workload: str, rank: int, world: int, dev):
     """(UM, D on the root else None, this rank's packed main-code shard, n_main,
@@ -573,9 +604,14 @@ def main():
             e2e_s = float(t.item())
         h2d = hUM.numel() * hUM.element_size() + hD.numel() * hD.element_size() + hM.numel() * 8
         d2h = nU * kb + dm.words(n_tuples, nb) * 8
+        bi = pcie_bidirectional_gbs(dev)
         e2e = {"value": all_tuples / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_s * 1e3,
-               "path": "dm_merge_column_host (pinned host buffers, copies inside the timed call)"}
+               "path": "dm_merge_column_host (pinned host buffers, copies inside the timed call)",
+               "pcie_bidirectional_gbs": bi,
+               "pcie_bound_ms": (h2d + d2h) / (bi * 1e9) * 1e3 if bi else None,
+               "pcie_note": "the copies' floor: (H2D + D2H bytes) / the measured concurrent both-direction "
+                            "pinned copy rate of this box"}
         ctx.close()
 
     cpu_baseline = None
