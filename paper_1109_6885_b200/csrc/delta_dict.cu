@@ -689,7 +689,13 @@ __global__ void __launch_bounds__(256) k_dedup_insert(const void* __restrict__ D
       if ((uint32_t)sv == 0) {
         sv = atomicCAS(reinterpret_cast<unsigned long long*>(slots + slot), 0ull, (unsigned long long)tg);
         if (sv == 0) {  // claimed: publish the value, then (id, ready)
-          id = (uint32_t)atomicAdd(n_dist, 1ull);
+          // ids for all lanes that claimed in this step: one atomic per warp, not per value
+          const unsigned m = __activemask();
+          const int leader = __ffs(m) - 1;
+          unsigned long long b0 = 0;
+          if ((int)lane_id() == leader) b0 = atomicAdd(n_dist, (unsigned long long)__popc(m));
+          b0 = __shfl_sync(m, b0, leader);
+          id = (uint32_t)(b0 + __popc(m & lanemask_lt()));
           KT::store(dkeys, id, k);
           st_release_u64(slots + slot, ((uint64_t)id << 32) | tg | 2u);
           break;
@@ -732,47 +738,65 @@ __global__ void __launch_bounds__(256) k_pf_build(const void* __restrict__ UM, u
   }
 }
 
+// Each block takes 1024 tuples per round: one atomic per block and round
+// claims the compacted slots of its new values (a per-warp atomic on one counter
+// serialised ~1.6e5 warps on cfg3), and a tuple whose "used" bit is already set
+// (a Zipf-hot value) skips its atomicOr.
+constexpr int kPfThreads = 256, kPfItems = 4;
 template <class KT>
-__global__ void __launch_bounds__(256) k_pf_probe(const void* __restrict__ UM, const uint32_t* __restrict__ table,
-                                                  uint64_t mask, const void* __restrict__ D, uint64_t n,
-                                                  uint32_t* __restrict__ src, void* __restrict__ newkeys,
-                                                  unsigned long long* n_new, uint32_t* __restrict__ used) {
+__global__ void __launch_bounds__(kPfThreads) k_pf_probe(const void* __restrict__ UM,
+                                                         const uint32_t* __restrict__ table, uint64_t mask,
+                                                         const void* __restrict__ D, uint64_t n,
+                                                         uint32_t* __restrict__ src, void* __restrict__ newkeys,
+                                                         unsigned long long* n_new, uint32_t* used) {
   pdl_prologue();
   using K = typename KT::K;
-  const unsigned lane = lane_id();
-  const uint64_t n_round = (n + 31) & ~31ull;  // whole warps iterate together (warp-aggregated atomics)
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n_round;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const bool live = i < n;
-    K v{};
-    uint32_t p = kPfEmpty;
-    if (live) {
-      v = KT::load(D, i);
-      uint64_t slot = (dd_hash(v) >> 32) & mask;
-      for (;;) {
-        const uint32_t q = __ldg(table + slot);
-        if (q == kPfEmpty || KT::eq(KT::load(UM, q), v)) {
-          p = q;
-          break;
+  constexpr int TILE = kPfThreads * kPfItems;
+  __shared__ uint32_t s_warp[kPfThreads / 32 + 1];
+  __shared__ unsigned long long s_base;
+  for (uint64_t base = (uint64_t)blockIdx.x * TILE; base < n; base += (uint64_t)gridDim.x * TILE) {
+    K v[kPfItems];
+    uint32_t p[kPfItems];
+    uint32_t nnew = 0;
+#pragma unroll
+    for (int r = 0; r < kPfItems; ++r) {
+      const uint64_t i = base + (uint64_t)r * kPfThreads + threadIdx.x;
+      p[r] = kPfEmpty;
+      if (i < n) {
+        v[r] = KT::load(D, i);
+        uint64_t slot = (dd_hash(v[r]) >> 32) & mask;
+        for (;;) {
+          const uint32_t q = __ldg(table + slot);
+          if (q == kPfEmpty || KT::eq(KT::load(UM, q), v[r])) {
+            p[r] = q;
+            break;
+          }
+          slot = (slot + 1) & mask;
         }
-        slot = (slot + 1) & mask;
+        if (p[r] == kPfEmpty) {
+          ++nnew;
+        } else {
+          src[i] = p[r];
+          const uint32_t bit = 1u << (p[r] & 31);
+          if (!(used[p[r] >> 5] & bit)) atomicOr(&used[p[r] >> 5], bit);
+        }
       }
     }
-    const bool found = p != kPfEmpty;
-    const unsigned newmask = __ballot_sync(FULL, live && !found);
-    unsigned long long base = 0;
-    if (lane == 0 && newmask) base = atomicAdd(n_new, (unsigned long long)__popc(newmask));
-    base = __shfl_sync(FULL, base, 0);
-    if (live) {
-      if (found) {
-        src[i] = p;
-        atomicOr(&used[p >> 5], 1u << (p & 31));
-      } else {
-        const uint64_t j = base + __popc(newmask & lanemask_lt());
-        KT::store(newkeys, j, v);
+    uint32_t tot;
+    uint32_t off = block_exclusive_scan<kPfThreads>(nnew, s_warp, tot);
+    if (threadIdx.x == 0) s_base = tot ? atomicAdd(n_new, (unsigned long long)tot) : 0ull;
+    __syncthreads();
+    const unsigned long long b0 = s_base;
+#pragma unroll
+    for (int r = 0; r < kPfItems; ++r) {
+      const uint64_t i = base + (uint64_t)r * kPfThreads + threadIdx.x;
+      if (i < n && p[r] == kPfEmpty) {
+        const uint64_t j = b0 + off++;
+        KT::store(newkeys, j, v[r]);
         src[i] = kPfNew | (uint32_t)j;
       }
     }
+    __syncthreads();  // s_base / s_warp reused next round
   }
 }
 
@@ -871,7 +895,7 @@ cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, void* udict
     cudaMemsetAsync(table, 0xff, L.pf_cap * 4, st);
     launch_k(k_pf_build<KT>, (unsigned)std::min<uint64_t>((in->dict_len + 255) / 256, (uint64_t)sms * 8), 256, 0, st,
              in->main_dict, in->dict_len, table, L.pf_cap - 1);
-    launch_k(k_pf_probe<KT>, (unsigned)std::min<uint64_t>((n + 255) / 256, (uint64_t)sms * 8), 256, 0, st,
+    launch_k(k_pf_probe<KT>, (unsigned)std::min<uint64_t>((n + 1023) / 1024, (uint64_t)sms * 8), kPfThreads, 0, st,
              in->main_dict, (const uint32_t*)table, L.pf_cap - 1, in->delta, n,
              reinterpret_cast<uint32_t*>(ws + L.pf_src), (void*)(ws + L.pf_keys), n_new,
              reinterpret_cast<uint32_t*>(ws + L.pf_used));
