@@ -314,7 +314,9 @@ def sharded_inputs(workload: str, rank: int, world: int, dev):
     shard = dm.pack_codes(codes[m0:m1].to(dev), bits) if m1 > m0 else torch.zeros(2, dtype=torch.int64, device=dev)
     del codes
     if rank != 0:
-        UM = D = None
+        D = None
+        if cfg != 5:
+            UM = None
     return UM, D, shard, n_main, bits, dict_len, n_delta, key, cuts
 
 
@@ -327,11 +329,20 @@ def run_sharded(args, rank, world, local, dev, backend):
     import torch.distributed as dist
     import paper_1109_6885_b200 as dm
     UM, D, shard, n_main, bits, dict_len, n_delta, key, cuts = sharded_inputs(args.workload, rank, world, dev)
+    # cfg5's 1.07e9-entry dictionary: Step 1(b) by U_M value ranges on every rank (NEXT2);
+    # smaller dictionaries: the root merges them (fewer collectives)
+    step1b = "ranges" if cfg_number(args.workload) == 5 else "root"
+    range_begin = 0
+    if step1b == "ranges":
+        a, b = dm.plan_dict_ranges(dict_len, world)[rank:rank + 2]
+        UM, range_begin = UM[a:b].clone(), a
+        torch.cuda.empty_cache()
     comm = dm.Comm.nccl() if backend == "nccl" else dm.Comm.callbacks()
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
     def step():
-        return dm.merge_column_sharded(comm, shard, n_main, bits, dict_len, n_delta, main_dict=UM, delta=D, key=key)
+        return dm.merge_column_sharded(comm, shard, n_main, bits, dict_len, n_delta, main_dict=UM, delta=D, key=key,
+                                       step1b=step1b, range_begin=range_begin)
 
     for _ in range(max(args.warmup, 0)):
         r = step()
@@ -369,8 +380,9 @@ def run_sharded(args, rank, world, local, dev, backend):
             "vs_baseline": None, "dtype": key_dtype(args.workload),
             "data": f"synthetic (datagen, seeded; BASELINE configs[{cfg_number(args.workload) - 1}])",
             "config": {"workload": WORKLOADS[args.workload],
-                       "parallelism": f"row-sharded x{world}: root Steps 1(a)-2(a), XC broadcast, "
-                                      f"Step 2(b) by output rows (dm_merge_column_sharded, "
+                       "parallelism": f"row-sharded x{world}: root Step 1(a), Step 1(b) "
+                                      f"{'by U_M value ranges on every rank (NEXT2)' if step1b == 'ranges' else 'on the root'}"
+                                      f", XC broadcast, Step 2(b) by output rows (dm_merge_column_sharded, "
                                       f"{'NCCL' if backend == 'nccl' else 'host callbacks over ' + backend})",
                        "row_cuts": cuts, "l2": "flushed (512 MB write) before every timed step",
                        "timing": "CUDA events around the collective call on each rank, max over ranks"},

@@ -284,15 +284,32 @@ void dm_plan_row_shards(uint64_t n_main, uint64_t n_delta, int nranks, uint64_t*
  * b' = width(dict_len + n_delta).  Host, pure. */
 uint64_t dm_sharded_codes_cap_words(uint64_t dict_len, uint64_t n_main, uint64_t n_delta, int nranks, int rank);
 
+/* U_M value ranges for DM_STEP1B_RANGES: cuts[0..nranks], rank g holds
+ * U_M[cuts[g], cuts[g+1]); every cut but the last a multiple of 1024 (whole XC
+ * superblocks).  Host, pure. */
+void dm_plan_dict_ranges(uint64_t dict_len, int nranks, uint64_t* cuts);
+
 enum { DM_TABLES_XC = 0, DM_TABLES_PLAIN = 1 };
+enum { DM_STEP1B_ROOT = 0, DM_STEP1B_RANGES = 1 };
 typedef struct {
   int32_t key;                 /* dm_key, the same on every rank                         */
   int32_t tables;              /* DM_TABLES_XC: broadcast the compact table XC (NEXT3)   *
                                 * (+ the X_M slices of flagged superblocks); PLAIN: the  *
                                 * literal X_M (SURVEY §8e's control design)              */
-  int32_t root;                /* rank that holds U_M and D and runs Steps 1(a)-2(a)     */
-  const void* main_dict;       /* root: U_M (device), strictly increasing; others ignored */
+  int32_t root;                /* rank that holds D and runs Step 1(a) (and, ROOT mode,  *
+                                * Step 1(b))                                             */
+  int32_t step1b;              /* DM_STEP1B_ROOT: the root merges the whole dictionary;  *
+                                * DM_STEP1B_RANGES (the paper's        *
+                                * quantile-split parallel merge, one level up):*
+                                * rank g merges its U_M value range with the U_D values  *
+                                * that fall into it, an all-gather of (|U'_g|, new       *
+                                * values_g) rebases every range's tables; XC only        *
+                                * (tables = DM_TABLES_XC, 128-code blocks)               */
+  const void* main_dict;       /* ROOT: the root's U_M (device), strictly increasing;    *
+                                * RANGES: this rank's range U_M[range_begin, +range_len) */
   uint64_t dict_len;           /* |U_M| (every rank)                                     */
+  uint64_t range_begin;        /* RANGES: dm_plan_dict_ranges(dict_len, nranks)[g]       */
+  uint64_t range_len;          /* RANGES: the range's length (> 0)                       */
   const void* delta;           /* root: D (device), insertion order; others ignored      */
   uint64_t n_delta;            /* N_D (every rank)                                       */
   const uint64_t* main_codes;  /* this rank's main rows [min(cuts[g], N_M),              *
@@ -302,13 +319,19 @@ typedef struct {
   uint32_t main_bits;          /* b (every rank)                                         */
 } dm_sharded_in;
 typedef struct {
-  void* merged_dict;               /* root: U' (device), capacity merged_dict_cap keys   */
-  uint64_t merged_dict_cap;        /* root: >= dict_len + n_delta                        */
+  void* merged_dict;               /* ROOT: the root's U' (device), capacity             *
+                                    * merged_dict_cap keys; RANGES: this rank's slice of  *
+                                    * U' (its range's values and the new ones among them) */
+  uint64_t merged_dict_cap;        /* ROOT (root): >= dict_len + n_delta; RANGES (every   *
+                                    * rank): >= range_len + n_delta                       */
   uint64_t* merged_codes;          /* this rank's M' words: rows [cuts[g], cuts[g+1])    *
                                     * at b' from bit 0 (device, 16-byte aligned)         */
   uint64_t merged_codes_cap_words; /* >= dm_sharded_codes_cap_words(...)                 */
   uint64_t merged_dict_len;        /* out (every rank): |U'|                            */
   uint32_t merged_bits;            /* out (every rank): b'                              */
+  uint64_t merged_dict_offset;     /* out, RANGES: U' index of this rank's slice; its   *
+                                    * length = merged_slice_len                         */
+  uint64_t merged_slice_len;       /* out, RANGES: entries in this rank's U' slice      */
 } dm_sharded_out;
 /* Collective, synchronous.  1. every rank's descriptor (key, tables, root,
  * |U_M|, N_M, N_D, b) must agree (all-gather; else DM_E_INVALID everywhere);
@@ -317,6 +340,13 @@ typedef struct {
  * X_D[r[k]] and sends each owner its slice; 6. every rank:
  * Step 2(b) of its rows (Eq 11).  Concatenating the ranks' M' words in
  * rank order gives the merged code vector of dm_merge_column, bit for bit.
+ * DM_STEP1B_RANGES replaces 2-4 by: all-gather of every range's first value,
+ * the root cuts U_D there (lower bound) and broadcasts U_D and the cuts; every
+ * rank merges its range (Steps 1(b)-2(a)); all-gather of (|U'_g|, new_g); every
+ * rank rebases its X_M / X_D / XC records by the counts of earlier ranges; the
+ * XC pieces and the flagged superblocks' X_M slices are all-gathered (rank =
+ * value order), the X_D pieces gathered on the root.  Concatenating the ranks'
+ * U' slices in rank order gives U'.
  * Temporaries come from the device's stream-ordered memory pool and are
  * released before return (a non-root rank holding flagged-superblock slices
  * allocates a sparse |U_M|-entry X_M).  Returns the worst status of all ranks;

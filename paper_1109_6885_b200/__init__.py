@@ -31,6 +31,7 @@ __all__ = [
     "ColumnMerger", "HostContext", "launch_count", "lib_path", "set_tuning", "XcTables", "recompress_xc",
     "xc_exceptions_gather", "xc_exceptions_scatter", "lower_bound", "rebase", "DictionaryMerger", "get_tuning",
     "tuning", "Comm", "plan_row_shards", "merge_column_sharded", "ShardedResult", "sharded_codes_cap_words",
+    "plan_dict_ranges",
 ]
 
 KEY_U64, KEY_B16, KEY_U32 = 0, 1, 2
@@ -71,7 +72,8 @@ class _Xc(ctypes.Structure):
 
 class _ShIn(ctypes.Structure):
     _fields_ = [("key", ctypes.c_int32), ("tables", ctypes.c_int32), ("root", ctypes.c_int32),
-                ("main_dict", ctypes.c_void_p), ("dict_len", ctypes.c_uint64), ("delta", ctypes.c_void_p),
+                ("step1b", ctypes.c_int32), ("main_dict", ctypes.c_void_p), ("dict_len", ctypes.c_uint64),
+                ("range_begin", ctypes.c_uint64), ("range_len", ctypes.c_uint64), ("delta", ctypes.c_void_p),
                 ("n_delta", ctypes.c_uint64), ("main_codes", ctypes.c_void_p), ("n_main", ctypes.c_uint64),
                 ("main_bits", ctypes.c_uint32)]
 
@@ -79,7 +81,8 @@ class _ShIn(ctypes.Structure):
 class _ShOut(ctypes.Structure):
     _fields_ = [("merged_dict", ctypes.c_void_p), ("merged_dict_cap", ctypes.c_uint64),
                 ("merged_codes", ctypes.c_void_p), ("merged_codes_cap_words", ctypes.c_uint64),
-                ("merged_dict_len", ctypes.c_uint64), ("merged_bits", ctypes.c_uint32)]
+                ("merged_dict_len", ctypes.c_uint64), ("merged_bits", ctypes.c_uint32),
+                ("merged_dict_offset", ctypes.c_uint64), ("merged_slice_len", ctypes.c_uint64)]
 
 
 _CB_BCAST = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_void_p)
@@ -153,6 +156,7 @@ def _lib():
             "dm_comm_size": (i32, [vp]),
             "dm_comm_selftest_host": (i32, [vp]),
             "dm_plan_row_shards": (None, [u64, u64, i32, P(u64)]),
+            "dm_plan_dict_ranges": (None, [u64, i32, P(u64)]),
             "dm_sharded_codes_cap_words": (u64, [u64, u64, u64, i32, i32]),
             "dm_merge_column_sharded": (i32, [vp, P(_ShIn), P(_ShOut), vp]),
             "dm_status_str": (ctypes.c_char_p, [i32]),
@@ -645,6 +649,14 @@ def plan_row_shards(n_main: int, n_delta: int, nranks: int) -> list:
     return [int(c) for c in cuts]
 
 
+def plan_dict_ranges(dict_len: int, nranks: int) -> list:
+    """dm_plan_dict_ranges: U_M position cuts for the value-range sharded Step 1(b)
+    (every cut but the last a multiple of 1024)."""
+    cuts = (ctypes.c_uint64 * (nranks + 1))()
+    _lib().dm_plan_dict_ranges(dict_len, nranks, cuts)
+    return [int(c) for c in cuts]
+
+
 def sharded_codes_cap_words(dict_len: int, n_main: int, n_delta: int, nranks: int, rank: int) -> int:
     return int(_lib().dm_sharded_codes_cap_words(dict_len, n_main, n_delta, nranks, rank))
 
@@ -743,32 +755,44 @@ class ShardedResult:
     merged_codes: torch.Tensor           # this rank's M' words (rows [cuts[g], cuts[g+1]) at b')
     merged_bits: int                     # b'
     merged_len: int                      # |U'|
-    merged_dict: Optional[torch.Tensor]  # U' on the root, else None
+    merged_dict: Optional[torch.Tensor]  # U' on the root (step1b "root"), this rank's U' slice ("ranges")
     row_begin: int
     row_end: int
+    merged_dict_offset: int = 0          # "ranges": U' index of merged_dict[0]
 
 
 def merge_column_sharded(comm: Comm, main_codes_shard: torch.Tensor, n_main: int, main_bits: int, dict_len: int,
                          n_delta: int, *, main_dict: Optional[torch.Tensor] = None,
                          delta: Optional[torch.Tensor] = None, key: str = "u64", tables: str = "xc",
-                         root: int = 0, stream=None) -> ShardedResult:
+                         root: int = 0, step1b: str = "root", range_begin: int = 0,
+                         stream=None) -> ShardedResult:
     """dm_merge_column_sharded: this rank's part of one column's merge (collective).
     ``main_codes_shard``: the packed main codes of this rank's main rows
-    (plan_row_shards); the root also passes U_M (``main_dict``) and D (``delta``)."""
+    (plan_row_shards); the root also passes D (``delta``).  step1b "root": the
+    root passes the whole U_M (``main_dict``) and merges the dictionary;
+    "ranges" (NEXT2): every rank passes its U_M range (``main_dict``, starting at
+    ``range_begin``, a plan_dict_ranges cut) and gets its slice of U'."""
     nr, me = comm.size, comm.rank
     cuts = plan_row_shards(n_main, n_delta, nr)
     dev = main_codes_shard.device if main_codes_shard is not None else torch.device("cuda", torch.cuda.current_device())
     cap = sharded_codes_cap_words(dict_len, n_main, n_delta, nr, me)
     out_codes = torch.empty(max(cap, 2), dtype=torch.int64, device=dev)
-    U = _empty_keys(_KEY[key], dict_len + n_delta, dev) if me == root else None
-    cin = _ShIn(_KEY[key], 0 if tables == "xc" else 1, root, _ptr(main_dict) if me == root else None, dict_len,
+    ranges = step1b == "ranges"
+    rlen = int(main_dict.shape[0]) if ranges else 0
+    ucap = rlen + n_delta if ranges else (dict_len + n_delta if me == root else 0)
+    U = _empty_keys(_KEY[key], ucap, dev) if (ranges or me == root) else None
+    md = _ptr(main_dict) if (ranges or me == root) else None
+    cin = _ShIn(_KEY[key], 0 if tables == "xc" else 1, root, 1 if ranges else 0, md, dict_len, range_begin, rlen,
                 _ptr(delta) if me == root else None, n_delta, _ptr(main_codes_shard), n_main, main_bits)
-    cout = _ShOut(_ptr(U), dict_len + n_delta if U is not None else 0, out_codes.data_ptr(), out_codes.numel(), 0, 0)
+    cout = _ShOut(_ptr(U), ucap, out_codes.data_ptr(), out_codes.numel(), 0, 0, 0, 0)
     st = _lib().dm_merge_column_sharded(comm.h, ctypes.byref(cin), ctypes.byref(cout), _stream_handle(stream))
     if st != Status.OK:
         raise DictMergeError(st, "dm_merge_column_sharded")
     nb = int(cout.merged_bits)
     r0, r1 = cuts[me], cuts[me + 1]
     nw = (r1 * nb + 63) // 64 - r0 * nb // 64
-    return ShardedResult(out_codes[:nw], nb, int(cout.merged_dict_len),
-                         U[: cout.merged_dict_len] if U is not None else None, r0, r1)
+    if ranges:
+        Uo = U[: cout.merged_slice_len]
+    else:
+        Uo = U[: cout.merged_dict_len] if U is not None else None
+    return ShardedResult(out_codes[:nw], nb, int(cout.merged_dict_len), Uo, r0, r1, int(cout.merged_dict_offset))

@@ -111,8 +111,11 @@ static std::atomic<int> g_tuning[6] = {env_knob("DM_XMODE", 3), env_knob("DM_MER
                                        env_knob("DM_STEP2", 1), env_knob("DM_XC_SHIFT", 8), env_knob("DM_SORT1A", 2)};
 int tuning(int knob) { return (knob >= 0 && knob < 6) ? g_tuning[knob].load(std::memory_order_relaxed) : 0; }
 
+static thread_local int t_xc_shift = 0;
+void set_xc_shift_override(int xs) { t_xc_shift = xs; }
 int xc_shift_override() {
-  const int x = tuning(4);  // knob 4 (DM_XC_SHIFT): the sharded Step 1(b) fixes one shift for all ranges
+  if (t_xc_shift) return t_xc_shift;  // this thread's sharded Step 1(b): one shift for all ranges
+  const int x = tuning(4);  // knob 4 (DM_XC_SHIFT)
   return (x == 7 || x == 8) ? x : 0;
 }
 

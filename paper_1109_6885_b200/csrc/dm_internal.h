@@ -110,7 +110,8 @@ inline bool probe_possible(const dm_column_in* in) {
 
 // Block shift: 256-code blocks when N_D / |U_M| promises <= 6 entries per block
 // (and always for the shared-memory variant, knob 2), else 128-code blocks.
-int xc_shift_override();  // knob 4 / DM_XC_SHIFT: 7 or 8, 0 = none
+int xc_shift_override();  // knob 4 / DM_XC_SHIFT: 7 or 8, 0 = none (a thread override first)
+void set_xc_shift_override(int xs);  // this thread only; 0 clears (the library's sharded Step 1(b))
 inline uint32_t xc_shift(const dm_column_in* in) {
   if (const int o = xc_shift_override()) return (uint32_t)o;
   if (tuning(0) == 2 || xc_smem_candidate(in)) return 8;

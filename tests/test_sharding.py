@@ -192,6 +192,64 @@ def _gpu_worker(rank, world, port, q, tables, key, case):
         dist.destroy_process_group()
 
 
+def _ranges_worker(rank, world, port, q, key, case):
+    """NEXT2 inside the library: dm_merge_column_sharded with step1b = "ranges" --
+    every rank merges its U_M value range with the U_D values that fall into it
+    (gloo callback transport, ranks sharing the one GPU); U' slices and M' words
+    concatenated in rank order must equal the oracle's."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1109_6885_b200 as dm
+        from tests.parity import to_device, keys_np
+        torch.cuda.set_device(0)
+        if case == "flagged":
+            col = datagen.make_clustered_case(37, 1 << 19, 200_000, 20_000, key=key)
+        elif case == "small":  # X_M <= 96 KB: the plain X_M is gathered instead of XC
+            col = datagen.make_random_case(39, 300_000, 9_000, 7_001, 0.5, key=key)
+        else:
+            col = datagen.make_random_case(35, 600_000, 200_000, 90_001, 0.5, key=key)
+        UM, M, D = to_device(col)
+        a, b = dm.plan_dict_ranges(col.dict_len, world)[rank:rank + 2]
+        shard = sharding.plan_row_shards(col.n_main, col.n_delta, world)[rank]
+        mslice = M[shard.in_word(col.main_bits):] if shard.n_main else M
+        comm = dm.Comm.callbacks()
+        r = dm.merge_column_sharded(comm, mslice, col.n_main, col.main_bits, col.dict_len, col.n_delta,
+                                    main_dict=UM[a:b].clone(), delta=D if rank == 0 else D[:0], key=key,
+                                    step1b="ranges", range_begin=a)
+        comm.close()
+        pieces = [None] * world
+        dist.all_gather_object(pieces, (r.merged_dict_offset, keys_np_list(keys_np(r.merged_dict, key), key),
+                                        r.merged_codes.cpu().numpy().view(np.uint64).tolist(), r.merged_bits,
+                                        r.merged_len))
+        if rank == 0:
+            ref = oracle.merge(col)
+            U = [v for p in sorted(pieces, key=lambda p: p[0]) for v in p[1]]
+            words = np.array([w for p in pieces for w in p[2]], dtype=np.uint64)
+            q.put((U == keys_np_list(ref.merged_dict, key), bool(np.array_equal(words, ref.merged_words)),
+                   all(p[3] == ref.merged_bits and p[4] == ref.merged_len for p in pieces)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,key,case", [(2, "u64", "random"), (3, "b16", "random"), (2, "u32", "random"),
+                                            (3, "u64", "flagged"), (2, "u64", "small")])
+def test_sharded_merge_column_ranges_in_library(world, key, case):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ranges_worker, args=(r, world, port, q, key, case)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+    assert all(res), res
+
+
 def _run_gpu_ranks(world, *args):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
@@ -309,3 +367,16 @@ def test_sharded_merge_column_nccl_one_rank():
     res = q.get(timeout=300)
     p.join(timeout=60)
     assert all(res), res
+
+
+@pytest.mark.parametrize("dict_len,g", [(10**7, 8), (1 << 30, 8), (5000, 3), (1024, 4), (7, 2), (200_000, 3)])
+def test_library_plan_dict_ranges(dict_len, g):
+    """dm_plan_dict_ranges (host, pure): U_M cut into g contiguous ranges at
+    multiples of 1024 positions (whole XC superblocks of 128- and 256-code
+    blocks), tiling [0, |U_M|)."""
+    import paper_1109_6885_b200 as dm
+    cuts = dm.plan_dict_ranges(dict_len, g)
+    assert len(cuts) == g + 1 and cuts[0] == 0 and cuts[-1] == dict_len
+    assert cuts == sorted(cuts) and all(c % 1024 == 0 for c in cuts[:-1])
+    py = sharding.plan_dict_ranges(dict_len, g)  # the Python NEXT2 orchestration's plan agrees
+    assert [b for (b, _) in py] == cuts[:-1] and [e for (_, e) in py] == cuts[1:]
