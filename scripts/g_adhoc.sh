@@ -1,6 +1,4 @@
 set -u
 O=gpurun_out/$1; mkdir -p $O; shift
-timeout 1200 python -m pytest tests/test_sharding.py -x -q -m gpu > $O/pytest.log 2>&1; echo "pytest rc=$?" >> $O/pytest.log; tail -15 $O/pytest.log
-BENCH_PG_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 \
-  --master-port 29541 bench.py --gpus 2 --steps 2 --warmup 1 --workload cfg5 > $O/bench_cfg5_n2.jsonl 2> $O/bench_cfg5_n2.err; echo "n2 rc=$?"
-tail -c 700 $O/bench_cfg5_n2.jsonl; tail -5 $O/bench_cfg5_n2.err
+export DM_LIB_PATH=$PWD/paper_1109_6885_b200/libdictmerge_check.so
+timeout 1500 python -m pytest tests/test_gpu_merge_variants.py tests/test_gpu_sort1a.py tests/test_gpu_xc.py tests/test_gpu_parity.py tests/test_sharding.py -x -q -m gpu > $O/pytest_check.log 2>&1; echo "pytest rc=$?" >> $O/pytest_check.log; tail -4 $O/pytest_check.log
