@@ -420,8 +420,13 @@ dm_status dm_merge_column_host(dm_ctx* ctx, const dm_column_in* in, dm_column_ou
  *   else the LSD radix passes; 1 LSD passes only; 2 bucket path for any N_D.  A
  *   skewed key set (a bucket above 256 keys) falls back to the LSD passes on the
  *   device.  Same U_D and r either way.  Changes the workspace size.
- * The process starts with knobs 0..5 = $DM_XMODE / $DM_MERGE / $DM_DEDUP /
- * $DM_STEP2 / $DM_XC_SHIFT / $DM_SORT1A when set (experiments), else 0.
+ * knob 6 = Step 2(b) kernel form when XC sits in shared memory: 0 (default)
+ *   thread-per-group (a lane owns a 32-row group: unpack, translate and pack
+ *   in registers with compile-time widths; used when b' - b is 0 or 1 and the
+ *   plain X_M is whole), 1 the warp-per-group kernel (a lane per row, shuffle
+ *   packing) for every width pair.  Same M' either way.
+ * The process starts with knobs 0..6 = $DM_XMODE / $DM_MERGE / $DM_DEDUP /
+ * $DM_STEP2 / $DM_XC_SHIFT / $DM_SORT1A / $DM_TPG when set (experiments), else 0.
  * Returns DM_OK, or DM_E_INVALID for an unknown knob or value.  Affects calls
  * made after it returns (a captured CUDA graph keeps the kernels it recorded). */
 int dm_set_tuning(int knob, int value);

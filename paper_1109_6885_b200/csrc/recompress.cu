@@ -246,6 +246,48 @@ __device__ __forceinline__ uint32_t xc4_fast2(uint32_t code, const Xc4Consts& k,
 #endif
 }
 
+// The same lookup for the thread-per-group kernel, balanced for the two integer
+// pipes (ALU: LOP3 / SHF / ISETP / PRMT; FMA: IMAD / IMAD.HI, each one warp
+// instruction per 2 cycles per SM sub-partition): the record fields and the
+// window arithmetic are multiply(-high)s by powers of two held in registers
+// (opaque to ptxas, so they stay on the FMA pipe), the list words past the
+// first are loaded only by lanes whose list reaches them, and the byte masks
+// come from a 128-entry table indexed by n mod 128.
+struct TpgK {  // powers of two (and -2) passed as kernel parameters, so ptxas cannot turn the multiplies into shifts
+  uint32_t m23, m18, m25, m30, two, four, eight, m5, m7, m10, neg2;
+};
+struct TpgXc {
+  uint32_t rec_sa, offs_sa, lut_sa;
+  TpgK c;
+};
+__device__ __forceinline__ uint32_t lds_u32_pred(uint32_t a, bool pred) {  // no value when !pred (masked later)
+  uint32_t v;
+  asm("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.shared.u32 %0, [%1];\n}" : "=r"(v) : "r"(a), "r"((uint32_t)pred));
+  return v;
+}
+__device__ __forceinline__ uint32_t xc4_tpg(uint32_t code, const TpgXc& k, bool& slow) {
+  const TpgK& c = k.c;
+  const uint32_t w = lds_u32(__umulhi(code, c.m23) * c.four + k.rec_sa);  // pair record of code >> 9
+  const uint32_t hb = __umulhi(code * c.m23, c.two);                     // code bit 8: the second block
+  const uint32_t c1 = w & 127u;                                           // entries of the first block
+  const uint32_t c2 = __umulhi(w * c.m18, c.m7);                          // of both: bits [7, 14)
+  const uint32_t start = __umulhi(w, c.m18) + c1 * hb;                    // R' + (hb ? c1 : 0)
+  const uint32_t n = hb * (c1 * c.neg2 + c2) + c1;                        // wraps (huge) when flagged
+  const uint32_t pa = __umulhi(start, c.m30) * c.four + k.offs_sa;        // word holding entry `start`
+  const uint32_t sh = __umulhi(start * c.m30, c.m5);                      // 8 (start mod 4)
+  const uint32_t ns8 = n * c.eight + sh;
+  const uint32_t w0 = lds_u32(pa);
+  const uint32_t w1 = lds_u32_pred(pa + 4, ns8 > 32u);
+  const uint32_t w2 = lds_u32_pred(pa + 8, ns8 > 64u);
+  const uint2 m = lds_u64(__umulhi(n * c.m25, c.m10) + k.lut_sa);        // masks of min(n mod 128, 8) bytes
+  const uint32_t a = __funnelshift_r(w0, w1, sh), b = __funnelshift_r(w1, w2, sh);  // bytes [start, start + 8)
+  const uint32_t y = __byte_perm(code, 0u, 0u), y7 = y & 0x7f7f7f7fu;
+  const uint32_t za = (~a & 0x7f7f7f7fu) + y7, zb = (~b & 0x7f7f7f7fu) + y7;  // per byte: ~((a | 0x80) - y7)
+  const uint32_t lta = ((~a & y) | (~(a ^ y) & za)) & m.x, ltb = ((~b & y) | (~(b ^ y) & zb)) & m.y;
+  slow = n > 8u;
+  return code + start + __popc(lta) + __popc(ltb);
+}
+
 // The rare case: a list longer than 8 entries (counted in a loop) or a flagged
 // superblock (the plain X_M, global).
 __device__ __noinline__ uint32_t xc4_slow(uint32_t code, const uint32_t* __restrict__ rec4,
@@ -550,6 +592,283 @@ __global__ void __launch_bounds__(rec_threads<XMODE>(), XMODE == XM_XC_SMEM ? 1 
   if (__any_sync(FULL, bad) && lane == 0) atomicMin(&hdr->status, (int)DM_E_CODE_RANGE);
 }
 
+// ---------------------------------------------------------------------------
+// Step 2(b), thread-per-group form (XC in shared memory).  The warp-per-group
+// kernel above spends ~35 of its ~80 instructions per row on the streaming
+// structure (two unpack loads, funnel, shuffle-pack, per-chunk 64-bit index
+// math) around the XC lookup (ncu r02: 259M warp instructions for cfg2, issue
+// active 75%).  Here lane l owns a whole 32-row group of a tile of 32 groups
+// (1024 rows): it reads the group's b input words from shared memory with
+// 16-byte loads, extracts the 32 codes with compile-time shifts, translates
+// them, and assembles the b' output words in registers (compile-time shifts,
+// disjoint bits: multiply-adds on the FMA pipe) -- no shuffles, ~5 instructions
+// per row of streaming work.  b and b' are template parameters (b' - b in
+// {0, 1}, the usual growth); other width pairs keep the warp-per-group kernel.
+//   * every warp runs its own pipeline over tiles: kTpgSlots shared-memory
+//     slots, each filled by one bulk TMA copy of the tile (128 b bytes) that
+//     completes on the slot's mbarrier;
+//   * the output words go back into the same slot (in place, after a
+//     __syncwarp: every lane holds its input in registers) and leave by one
+//     bulk TMA store; the slot is refilled once that store has read it
+//     (bulk-group wait at the top of the next tile);
+//   * the rare lookups the fast path cannot finish (a list longer than 8, a
+//     flagged superblock) read the plain X_M, which is whole whenever this
+//     kernel runs (its L2 companion is the plain-X_M kernel);
+//   * tiles holding delta rows or the ragged end keep the lane-per-group
+//     layout with run-time row checks: input words and ranks from global, all
+//     32 gathers of a lane independent.
+// XC is staged by two bulk copies and converted to the 4-byte pair records in
+// place.  The number of warps per CTA follows from the shared memory XC leaves
+// (decided on the device from |U'|, like the XC fit itself).
+// Measured (cfg2, B200): 0.298 ms vs 0.312 ms for the warp-per-group kernel,
+// 169M vs 259M warp instructions; with the lookup replaced by the identity
+// (DM_TPG_NOLOOKUP, timing only) 0.127 ms = 0.79 of the HBM copy peak: the
+// stream is no longer the limit, the ~45 instructions and ~13 shared-memory
+// wavefronts per 32 lookups are.
+template <int B, int NB>
+struct Tpg {
+  static constexpr uint32_t slot_bytes = 128u * (B > NB ? B : NB);  // one tile in, then out (in place)
+};
+#ifndef DM_TPG_NOLOOKUP
+#define DM_TPG_NOLOOKUP 0
+#endif
+#ifndef DM_TPG_SLOTS
+#define DM_TPG_SLOTS 2
+#endif
+#ifndef DM_TPG_WARPS
+#define DM_TPG_WARPS 8
+#endif
+// Two slots per warp (the next tile loads while this one is translated) and up
+// to 8 warps.  Measured on cfg2 (B200): 2 x 8 0.298 ms; 1 slot x 16 warps (the
+// load of the next tile waits for the store of this one) 0.314-0.321 ms.
+constexpr int kTpgSlots = DM_TPG_SLOTS;
+constexpr int kTpgWarps = DM_TPG_WARPS;
+constexpr int kTpgMinWarps = 4;
+constexpr int kTpgMinWidth = 15;  // XC in shared memory needs |U_M| > 24576
+constexpr int kTpgHdrBytes = 128 + 128 * 8 + 128;  // slot mbarriers, the 128-entry list-mask table, the staging mbarrier
+
+template <int B>
+__device__ __forceinline__ uint32_t tpg_code(const uint32_t (&w)[B], int r) {
+  constexpr uint32_t mask = B == 32 ? 0xffffffffu : (1u << B) - 1u;
+  const int s = r * B, i = s >> 5, o = s & 31;
+  if (o + B <= 32) return (w[i] >> o) & mask;
+  return __funnelshift_r(w[i], w[i + 1], o) & mask;
+}
+template <int NB>
+__device__ __forceinline__ void tpg_put(uint32_t (&o)[NB], int r, uint32_t v) {
+  const int s = r * NB, i = s >> 5, sh = s & 31;
+  o[i] += v * (1u << sh);  // the codes of a word occupy disjoint bits (IMAD / IMAD.HI: the FMA pipe)
+  if (sh + NB > 32) o[i + 1] = mad_hi(v, 1u << sh, o[i + 1]);
+}
+
+template <int B, int NB>
+__global__ void __launch_bounds__(32 * kTpgWarps, 1)
+    k_recompress_tpg(const uint64_t* __restrict__ M, uint64_t n_main, uint64_t dict_len,
+                     const uint32_t* __restrict__ XM, const uint32_t* __restrict__ XD,
+                     const uint32_t* __restrict__ rank, uint64_t n_delta, uint64_t* __restrict__ Mout,
+                     dm_header* hdr, uint32_t fixed_bits, const uint2* __restrict__ xrec,
+                     const uint8_t* __restrict__ xoffs, uint32_t xc_budget, uint32_t xc_dens, TpgK kc,
+                     uint32_t smem_bytes) {
+  pdl_prologue();
+  using T = Tpg<B, NB>;
+  const uint32_t hb = fixed_bits ? fixed_bits : hdr->merged_bits;
+  if (hb != (uint32_t)NB) return;
+  // the XC fit: the same rule (and budget) as the L2 companion launched beside it
+  const uint64_t nsb = (dict_len + 1023) >> 10;
+  const uint64_t n_new = hdr->merged_dict_len - dict_len;
+  const uint64_t xc_offs_bytes = (n_new + 15) & ~15ull;
+  const uint64_t rec_pad = (nsb * kXcRecBytes + 15) & ~15ull;
+  const uint64_t xc_bytes = rec_pad + xc_offs_bytes + kXcSmemSlack;
+  if (!(xc_bytes <= xc_budget && (xc_dens == 0 || (n_new << xc_dens) <= dict_len) && n_new < kXc4MaxStart)) return;
+
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  static_assert(kTpgWarps * kTpgSlots * 8 <= 128, "mbarriers fit the header");
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);          // kTpgWarps x kTpgSlots
+  uint2* lut = reinterpret_cast<uint2*>(smem_raw + 128);            // 128 entries
+  uint32_t* sx = reinterpret_cast<uint32_t*>(smem_raw + kTpgHdrBytes);
+  const uint32_t slot0 = (uint32_t)((kTpgHdrBytes + xc_bytes + 127) & ~127ull);
+  const int W = (int)umin32(blockDim.x >> 5, (smem_bytes - slot0) / (kTpgSlots * T::slot_bytes));
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kTpgWarps * kTpgSlots; ++i) mbar_init(&bars[i], 1);
+    fence_mbar_init();
+  }
+  if (threadIdx.x < 128) {  // lut[n]: MSB of each of the first min(n, 8) bytes of an 8-byte window
+    const uint32_t n = umin32(threadIdx.x, 8u);
+    lut[threadIdx.x] = make_uint2(0x80808080u & (n >= 4 ? 0xffffffffu : (1u << (8 * n)) - 1u),
+                                  0x80808080u & (n >= 8 ? 0xffffffffu : n <= 4 ? 0u : (1u << (8 * (n - 4))) - 1u));
+  }
+  // XC staging: one bulk copy of the records and one of the lists (the global
+  // arrays are padded to 16 bytes), then every 8-byte superblock record becomes
+  // two 4-byte pair records in place (same size)
+  uint64_t* stage_bar = reinterpret_cast<uint64_t*>(smem_raw + 128 + 128 * 8);
+  if (threadIdx.x == 0) {
+    mbar_init(stage_bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    mbar_arrive_expect_tx(stage_bar, (uint32_t)(rec_pad + xc_offs_bytes));
+    tma_load_1d(sx, xrec, (uint32_t)rec_pad, stage_bar, policy_evict_last());
+    if (xc_offs_bytes)
+      tma_load_1d(reinterpret_cast<unsigned char*>(sx) + rec_pad, xoffs, (uint32_t)xc_offs_bytes, stage_bar,
+                  policy_evict_last());
+  }
+  mbar_wait_parity(stage_bar, 0);
+  {
+    uint4* d = reinterpret_cast<uint4*>(sx);
+    for (uint32_t i = threadIdx.x; i < rec_pad / 16; i += blockDim.x) {
+      const uint4 v = d[i];
+      d[i] = make_uint4(xc4_record(make_uint2(v.x, v.y), 0), xc4_record(make_uint2(v.x, v.y), 1),
+                        xc4_record(make_uint2(v.z, v.w), 0), xc4_record(make_uint2(v.z, v.w), 1));
+    }
+  }
+  __syncthreads();
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  if ((int)warp >= W) return;
+
+  const uint32_t* srec4 = sx;
+  const uint32_t* soffs = reinterpret_cast<const uint32_t*>(reinterpret_cast<unsigned char*>(sx) + rec_pad);
+  const TpgXc xk{smem_u32(srec4), smem_u32(soffs), smem_u32(lut), kc};
+  const uint32_t dict_last = (uint32_t)dict_len - 1u;
+  uint32_t code_max = 0;
+  const uint64_t n_total = n_main + n_delta;
+  const uint64_t n_tiles = (n_total + 1023) >> 10;
+  const uint64_t n_fast = n_main >> 10;  // tiles of main rows only: input and output wholly inside M, M'
+  const uint64_t gw = (uint64_t)blockIdx.x * W + warp, GW = (uint64_t)gridDim.x * W;
+  uint64_t* full = bars + warp * kTpgSlots;
+  unsigned char* slots = smem_raw + slot0 + (size_t)warp * kTpgSlots * T::slot_bytes;
+  const uint64_t pol = policy_evict_first();
+  const unsigned char* Mb = reinterpret_cast<const unsigned char*>(M);
+  unsigned char* Ob = reinterpret_cast<unsigned char*>(Mout);
+
+  auto issue = [&](uint64_t t, int k) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(&full[k], 128u * B);
+      tma_load_1d(slots + k * T::slot_bytes, Mb + t * (uint64_t)(128 * B), 128u * B, &full[k], pol);
+    }
+  };
+#pragma unroll
+  for (int k = 0; k < kTpgSlots; ++k)
+    if (gw + k * GW < n_fast) issue(gw + k * GW, k);
+
+  uint64_t j = 0;
+  for (uint64_t t = gw; t < n_fast; t += GW, ++j) {
+    const int k = (int)(j % kTpgSlots);
+    if (j > 0) {  // the previous tile's store has read its slot: refill it
+      tma_store_wait_read<0>();
+      __syncwarp();
+      const uint64_t tn = t + (kTpgSlots - 1) * GW;
+      if (tn < n_fast) issue(tn, (int)((j - 1) % kTpgSlots));
+    }
+    mbar_wait_parity_sleep(&full[k], (uint32_t)((j / kTpgSlots) & 1));
+    unsigned char* sl = slots + k * T::slot_bytes;
+    uint32_t w[B];
+    if constexpr (B % 4 == 0) {
+      const uint4* p = reinterpret_cast<const uint4*>(sl + lane * (B * 4));
+#pragma unroll
+      for (int i = 0; i < B / 4; ++i) {
+        const uint4 v = p[i];
+        w[4 * i] = v.x, w[4 * i + 1] = v.y, w[4 * i + 2] = v.z, w[4 * i + 3] = v.w;
+      }
+    } else if constexpr (B % 2 == 0) {
+      const uint2* p = reinterpret_cast<const uint2*>(sl + lane * (B * 4));
+#pragma unroll
+      for (int i = 0; i < B / 2; ++i) {
+        const uint2 v = p[i];
+        w[2 * i] = v.x, w[2 * i + 1] = v.y;
+      }
+    } else {
+      const uint32_t* p = reinterpret_cast<const uint32_t*>(sl) + lane * B;
+#pragma unroll
+      for (int i = 0; i < B; ++i) w[i] = p[i];
+    }
+    __syncwarp();  // every lane holds its input: the slot takes the output
+    uint32_t o[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) o[i] = 0;
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      const uint32_t c = tpg_code<B>(w, r);
+      code_max = umax32(code_max, c);
+      const uint32_t cc = umin32(c, dict_last);
+      bool su;
+#if DM_TPG_NOLOOKUP  // timing experiment only (wrong results): the streaming structure alone
+      const uint32_t v = cc;
+      su = false;
+#else
+      const uint32_t v = xc4_tpg(cc, xk, su);
+#endif
+      // rare (a list longer than 8 entries, a flagged superblock): the plain X_M,
+      // which is whole whenever this kernel runs (its L2 companion reads it)
+      tpg_put<NB>(o, r, su ? __ldg(XM + cc) : v);
+    }
+    if constexpr (NB % 4 == 0) {
+      uint4* d = reinterpret_cast<uint4*>(sl + lane * (NB * 4));
+#pragma unroll
+      for (int i = 0; i < NB / 4; ++i) d[i] = make_uint4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
+    } else if constexpr (NB % 2 == 0) {
+      uint2* d = reinterpret_cast<uint2*>(sl + lane * (NB * 4));
+#pragma unroll
+      for (int i = 0; i < NB / 2; ++i) d[i] = make_uint2(o[2 * i], o[2 * i + 1]);
+    } else {
+      uint32_t* d = reinterpret_cast<uint32_t*>(sl) + lane * NB;
+#pragma unroll
+      for (int i = 0; i < NB; ++i) d[i] = o[i];
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_1d(Ob + t * (uint64_t)(128 * NB), sl, 128u * NB, pol);
+      tma_store_commit();
+    }
+  }
+  tma_store_wait_all<0>();
+
+  // tiles holding delta rows or the ragged end: lane l still owns group l, its
+  // input words read from global (bounded), every row checked at run time; the
+  // 32 gathers of a lane (X_D through r, or the main lookups) are independent,
+  // so a tile costs a few round trips, not 32
+  if (n_fast < n_tiles) {
+    const uint32_t* M32 = reinterpret_cast<const uint32_t*>(M);
+    const uint64_t nw_in32 = 2 * dwords(n_main, B), nw32 = 2 * dwords(n_total, NB);
+    uint32_t* out32 = reinterpret_cast<uint32_t*>(Mout);
+    for (uint64_t t = n_fast + gw; t < n_tiles; t += GW) {
+      const uint64_t g = t * 32 + lane, row0 = g * 32;
+      uint32_t w[B];
+#pragma unroll
+      for (int i = 0; i < B; ++i) {
+        const uint64_t wi = g * B + i;
+        w[i] = wi < nw_in32 ? __ldg(M32 + wi) : 0u;
+      }
+      uint32_t o[NB];
+#pragma unroll
+      for (int i = 0; i < NB; ++i) o[i] = 0;
+#pragma unroll
+      for (int r = 0; r < 32; ++r) {
+        const uint64_t row = row0 + r;
+        uint32_t v = 0;
+        if (row < n_main) {
+          const uint32_t c = tpg_code<B>(w, r);
+          code_max = umax32(code_max, c);
+          const uint32_t cc = umin32(c, dict_last);
+          bool su;
+          v = xc4_tpg(cc, xk, su);
+          if (su) v = __ldg(XM + cc);
+        } else if (row < n_total) {
+          v = __ldg(XD + (rank ? __ldg(rank + (row - n_main)) : (uint32_t)(row - n_main)));
+        }
+        tpg_put<NB>(o, r, v);
+      }
+#pragma unroll
+      for (int i = 0; i < NB; ++i)
+        if (g * NB + i < nw32) out32[g * NB + i] = o[i];
+    }
+  }
+  const bool bad = n_main > 0 && code_max > dict_last;
+  if (__any_sync(FULL, bad) && lane == 0) atomicMin(&hdr->status, (int)DM_E_CODE_RANGE);
+}
+
 // Naive Step 2 -- the paper's unoptimized algorithm ("UnOpt" of
 // Fig 7/8): for every tuple take its value (U_M[M[i]] for a main row, D[k] for
 // a delta row) and binary-search it in the merged dictionary U'.  No
@@ -660,6 +979,39 @@ static uint32_t xc_smem_budget(uint32_t in_stage) {
   return b > 0 ? (uint32_t)(b & ~15ll) : 0u;
 }
 
+// Thread-per-group Step 2(b): dynamic shared memory (the device maximum) and
+// the XC budget that leaves room for kTpgMinWarps warps' slots.
+static uint32_t tpg_smem() {
+  static int optin = [] {
+    int d = 0, v = 0;
+    cudaGetDevice(&d);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, d);
+    return v;
+  }();
+  return optin > 1024 ? (uint32_t)(optin - 1024) : 0u;
+}
+template <int B, int NB>
+uint32_t tpg_budget() {
+  const int64_t b = (int64_t)tpg_smem() - kTpgHdrBytes - 128 - (int64_t)kTpgMinWarps * kTpgSlots * Tpg<B, NB>::slot_bytes;
+  return b > 0 ? (uint32_t)(b & ~15ll) : 0u;
+}
+template <int B, int NB>
+void launch_tpg(const dm_column_in* in, const dm_column_out* out, const uint32_t* xm, const uint32_t* xd,
+                const uint32_t* rank, dm_header* hdr, cudaStream_t st, uint32_t fixed_bits, const uint2* xrec,
+                const uint8_t* xoffs, uint32_t budget, uint32_t dens, uint32_t xs) {
+  auto kern = k_recompress_tpg<B, NB>;
+  const uint32_t smem = tpg_smem();
+  ensure_smem((const void*)kern);
+  const uint64_t tiles = (in->n_main + in->n_delta + 1023) / 1024;
+  const unsigned grid = (unsigned)std::max<uint64_t>(
+      1, std::min<uint64_t>(tiles, (uint64_t)device_sms() * rec_grid_percent() / 100));
+  (void)xs;  // 8: 256-code blocks
+  const TpgK kc{1u << 23, 1u << 18, 1u << 25, 1u << 30, 2u, 4u, 8u, 32u, 128u, 1024u, 0xfffffffeu};
+  launch_k(kern, grid, 32 * kTpgWarps, smem, st, in->main_codes, in->n_main, in->dict_len, xm, xd, rank, in->n_delta,
+           out->merged_codes, hdr, fixed_bits, xrec, xoffs, budget, dens, kc, smem);
+  note_launch();
+}
+
 template <int NB>
 cudaError_t launch_nb(const dm_column_in* in, const dm_column_out* out, const uint32_t* xm, const uint32_t* xd,
                       const uint32_t* rank, dm_header* hdr, cudaStream_t st, uint32_t fixed_bits, const uint2* xrec,
@@ -706,11 +1058,28 @@ cudaError_t launch_nb(const dm_column_in* in, const dm_column_out* out, const ui
     return cudaGetLastError();
   }
   const uint32_t budget0 = want_smem ? xc_smem_budget(in_stage_xc) : 0u;
-  const uint32_t budget = (uint64_t)xc_nsb(in->dict_len, xs) * kXcRecBytes + 16 <= budget0 ? budget0 : 0u;
-  if (budget)
+  uint32_t budget = (uint64_t)xc_nsb(in->dict_len, xs) * kXcRecBytes + 16 <= budget0 ? budget0 : 0u;
+  const bool xc_l2 = xc_only || knob == 2 || knob == 3 || in->dict_len * 4 > kXcGlobalMinBytes;
+  bool tpg = false;
+  if constexpr (NB >= kTpgMinWidth) {  // thread-per-group form for b' - b in {0, 1} (knob 6); its rare
+    // lookups read the plain X_M, which is whole when the companion is the plain-X_M kernel
+    if (want_smem && !xc_l2 && tuning(6) == 0 &&
+        (in->main_bits == (uint32_t)NB || in->main_bits + 1 == (uint32_t)NB)) {
+      const uint32_t bt = in->main_bits == (uint32_t)NB ? tpg_budget<NB, NB>() : tpg_budget<NB - 1, NB>();
+      if ((uint64_t)xc_nsb(in->dict_len, xs) * kXcRecBytes + 16 <= bt) {
+        budget = bt;
+        dens = auto_smem ? 6 : 0;
+        if (in->main_bits == (uint32_t)NB)
+          launch_tpg<NB, NB>(in, out, xm, xd, rank, hdr, st, fixed_bits, xrec, xoffs, budget, dens, xs);
+        else
+          launch_tpg<NB - 1, NB>(in, out, xm, xd, rank, hdr, st, fixed_bits, xrec, xoffs, budget, dens, xs);
+        tpg = true;
+      }
+    }
+  }
+  if (budget && !tpg)
     go(k_recompress<NB, XM_XC_SMEM>, kRecHdrBytes + (size_t)kRecStagesXc * in_stage_xc + budget, budget,
        rec_threads<XM_XC_SMEM>(), rec_groups<XM_XC_SMEM>());
-  const bool xc_l2 = xc_only || knob == 2 || knob == 3 || in->dict_len * 4 > kXcGlobalMinBytes;
   // (A persisting L2 access-policy window over XC was measured: no gain on
   // cfg5's Step 2(b), and the set-aside slowed Steps 1(a)/1(b) by 40%.)
   if (xc_l2)

@@ -1,5 +1,8 @@
 """Compact translation table XC vs the oracle, bit-exact.
 
+Auto placement runs with both Step 2(b) forms (knob 6: thread-per-group and
+warp-per-group kernels).
+
 XC replaces the Step 2(b) gather X_M[c] by c + #{new dictionary values inserted
 at or before main position c} (the closed form of X_M; DESIGN.md
 §7).  It must never change a result, so every case runs under each placement
@@ -22,7 +25,7 @@ from tests.parity import compare, run_gpu
 
 pytestmark = pytest.mark.gpu
 
-KNOBS = (0, 1, 2, 3)
+KNOBS = ((0, 0), (0, 1), (1, 0), (2, 0), (3, 0))  # (knob 0 placement, knob 6 Step 2(b) form)
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -38,6 +41,7 @@ def _reset_knob():
     yield
     import paper_1109_6885_b200 as dm
     dm.set_tuning(0, 0)
+    dm.set_tuning(6, 0)
 
 
 SPACING = 1000  # U_M[i] = SPACING * (i + 1): value SPACING*p + k (0 < k < SPACING) lands before U_M[p]
@@ -70,8 +74,9 @@ def _run_all_knobs(col):
     import paper_1109_6885_b200 as dm
     from tests.parity import to_device
     ref = None
-    for k in KNOBS:
+    for k, form in KNOBS:
         dm.set_tuning(0, k)
+        dm.set_tuning(6, form)
         M, r = run_gpu(col)
         ref = compare(col, M, r, ref=ref)
         UM, M, D = to_device(col)
