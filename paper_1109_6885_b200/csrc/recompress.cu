@@ -33,6 +33,7 @@
 #include <algorithm>
 #include <array>
 #include <cstdlib>
+#include <type_traits>
 #include <utility>
 
 #include "dm_device.cuh"
@@ -255,6 +256,7 @@ __device__ __forceinline__ uint32_t xc4_fast2(uint32_t code, const Xc4Consts& k,
 // come from a 128-entry table indexed by n mod 128.
 struct TpgK {  // powers of two (and -2) passed as kernel parameters, so ptxas cannot turn the multiplies into shifts
   uint32_t m23, m18, m25, m30, two, four, eight, m5, m7, m10, neg2;
+  uint32_t xs;  // XC block shift (XC read through L2)
 };
 struct TpgXc {
   uint32_t rec_sa, offs_sa, lut_sa;
@@ -661,7 +663,7 @@ __device__ __forceinline__ void tpg_put(uint32_t (&o)[NB], int r, uint32_t v) {
   if (sh + NB > 32) o[i + 1] = mad_hi(v, 1u << sh, o[i + 1]);
 }
 
-template <int B, int NB>
+template <int B, int NB, int XMODE>
 __global__ void __launch_bounds__(32 * kTpgWarps, 1)
     k_recompress_tpg(const uint64_t* __restrict__ M, uint64_t n_main, uint64_t dict_len,
                      const uint32_t* __restrict__ XM, const uint32_t* __restrict__ XD,
@@ -671,57 +673,65 @@ __global__ void __launch_bounds__(32 * kTpgWarps, 1)
                      uint32_t smem_bytes) {
   pdl_prologue();
   using T = Tpg<B, NB>;
+  constexpr bool XCS = XMODE == XM_XC_SMEM, XS = XMODE == XM_RAW_SMEM;
   const uint32_t hb = fixed_bits ? fixed_bits : hdr->merged_bits;
   if (hb != (uint32_t)NB) return;
-  // the XC fit: the same rule (and budget) as the L2 companion launched beside it
+  // the XC fit: the same rule (and budget) for the shared-memory kernel and its
+  // L2 companion (exactly one of them runs)
   const uint64_t nsb = (dict_len + 1023) >> 10;
   const uint64_t n_new = hdr->merged_dict_len - dict_len;
   const uint64_t xc_offs_bytes = (n_new + 15) & ~15ull;
   const uint64_t rec_pad = (nsb * kXcRecBytes + 15) & ~15ull;
   const uint64_t xc_bytes = rec_pad + xc_offs_bytes + kXcSmemSlack;
-  if (!(xc_bytes <= xc_budget && (xc_dens == 0 || (n_new << xc_dens) <= dict_len) && n_new < kXc4MaxStart)) return;
+  if (xc_budget) {
+    const bool fits = xc_bytes <= xc_budget && (xc_dens == 0 || (n_new << xc_dens) <= dict_len) && n_new < kXc4MaxStart;
+    if (XCS != fits) return;
+  }
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   static_assert(kTpgWarps * kTpgSlots * 8 <= 128, "mbarriers fit the header");
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);          // kTpgWarps x kTpgSlots
   uint2* lut = reinterpret_cast<uint2*>(smem_raw + 128);            // 128 entries
   uint32_t* sx = reinterpret_cast<uint32_t*>(smem_raw + kTpgHdrBytes);
-  const uint32_t slot0 = (uint32_t)((kTpgHdrBytes + xc_bytes + 127) & ~127ull);
+  const uint64_t table_bytes = XCS ? xc_bytes : XS ? dict_len * 4 : 0;
+  const uint32_t slot0 = (uint32_t)((kTpgHdrBytes + table_bytes + 127) & ~127ull);
   const int W = (int)umin32(blockDim.x >> 5, (smem_bytes - slot0) / (kTpgSlots * T::slot_bytes));
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kTpgWarps * kTpgSlots; ++i) mbar_init(&bars[i], 1);
     fence_mbar_init();
   }
-  if (threadIdx.x < 128) {  // lut[n]: MSB of each of the first min(n, 8) bytes of an 8-byte window
+  if (XCS && threadIdx.x < 128) {  // lut[n]: MSB of each of the first min(n, 8) bytes of an 8-byte window
     const uint32_t n = umin32(threadIdx.x, 8u);
     lut[threadIdx.x] = make_uint2(0x80808080u & (n >= 4 ? 0xffffffffu : (1u << (8 * n)) - 1u),
                                   0x80808080u & (n >= 8 ? 0xffffffffu : n <= 4 ? 0u : (1u << (8 * (n - 4))) - 1u));
   }
-  // XC staging: one bulk copy of the records and one of the lists (the global
-  // arrays are padded to 16 bytes), then every 8-byte superblock record becomes
-  // two 4-byte pair records in place (same size)
-  uint64_t* stage_bar = reinterpret_cast<uint64_t*>(smem_raw + 128 + 128 * 8);
-  if (threadIdx.x == 0) {
-    mbar_init(stage_bar, 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    mbar_arrive_expect_tx(stage_bar, (uint32_t)(rec_pad + xc_offs_bytes));
-    tma_load_1d(sx, xrec, (uint32_t)rec_pad, stage_bar, policy_evict_last());
-    if (xc_offs_bytes)
-      tma_load_1d(reinterpret_cast<unsigned char*>(sx) + rec_pad, xoffs, (uint32_t)xc_offs_bytes, stage_bar,
-                  policy_evict_last());
-  }
-  mbar_wait_parity(stage_bar, 0);
-  {
+  if constexpr (XCS) {
+    // XC staging: one bulk copy of the records and one of the lists (the global
+    // arrays are padded to 16 bytes), then every 8-byte superblock record becomes
+    // two 4-byte pair records in place (same size)
+    uint64_t* stage_bar = reinterpret_cast<uint64_t*>(smem_raw + 128 + 128 * 8);
+    if (threadIdx.x == 0) {
+      mbar_init(stage_bar, 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      mbar_arrive_expect_tx(stage_bar, (uint32_t)(rec_pad + xc_offs_bytes));
+      tma_load_1d(sx, xrec, (uint32_t)rec_pad, stage_bar, policy_evict_last());
+      if (xc_offs_bytes)
+        tma_load_1d(reinterpret_cast<unsigned char*>(sx) + rec_pad, xoffs, (uint32_t)xc_offs_bytes, stage_bar,
+                    policy_evict_last());
+    }
+    mbar_wait_parity(stage_bar, 0);
     uint4* d = reinterpret_cast<uint4*>(sx);
     for (uint32_t i = threadIdx.x; i < rec_pad / 16; i += blockDim.x) {
       const uint4 v = d[i];
       d[i] = make_uint4(xc4_record(make_uint2(v.x, v.y), 0), xc4_record(make_uint2(v.x, v.y), 1),
                         xc4_record(make_uint2(v.z, v.w), 0), xc4_record(make_uint2(v.z, v.w), 1));
     }
+  } else if constexpr (XS) {
+    for (uint32_t i = threadIdx.x; i < dict_len; i += blockDim.x) sx[i] = __ldg(XM + i);
   }
   __syncthreads();
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
@@ -730,6 +740,24 @@ __global__ void __launch_bounds__(32 * kTpgWarps, 1)
   const uint32_t* srec4 = sx;
   const uint32_t* soffs = reinterpret_cast<const uint32_t*>(reinterpret_cast<unsigned char*>(sx) + rec_pad);
   const TpgXc xk{smem_u32(srec4), smem_u32(soffs), smem_u32(lut), kc};
+  const uint64_t pol_x = policy_evict_last();
+  // X_M[cc]; XC in shared memory: `slow` set when the fast lookup cannot finish
+  // (a list longer than 8, a flagged superblock) -- then the plain X_M, which is
+  // whole whenever this kernel runs (its L2 companion is the plain-X_M kernel)
+  auto translate = [&](uint32_t cc, bool& slow) -> uint32_t {
+    slow = false;
+#if DM_TPG_NOLOOKUP  // timing experiment only (wrong results): the streaming structure alone
+    return cc;
+#endif
+    if constexpr (XCS)
+      return xc4_tpg(cc, xk, slow);
+    else if constexpr (XS)
+      return sx[cc];
+    else if constexpr (XMODE == XM_XC_GLOBAL)
+      return xc_lookup<false>(cc, kc.xs, xrec, reinterpret_cast<const uint32_t*>(xoffs), XM, pol_x);
+    else
+      return ld_gather_u32(XM + cc, pol_x);
+  };
   const uint32_t dict_last = (uint32_t)dict_len - 1u;
   uint32_t code_max = 0;
   const uint64_t n_total = n_main + n_delta;
@@ -793,15 +821,8 @@ __global__ void __launch_bounds__(32 * kTpgWarps, 1)
       code_max = umax32(code_max, c);
       const uint32_t cc = umin32(c, dict_last);
       bool su;
-#if DM_TPG_NOLOOKUP  // timing experiment only (wrong results): the streaming structure alone
-      const uint32_t v = cc;
-      su = false;
-#else
-      const uint32_t v = xc4_tpg(cc, xk, su);
-#endif
-      // rare (a list longer than 8 entries, a flagged superblock): the plain X_M,
-      // which is whole whenever this kernel runs (its L2 companion reads it)
-      tpg_put<NB>(o, r, su ? __ldg(XM + cc) : v);
+      const uint32_t v = translate(cc, su);
+      tpg_put<NB>(o, r, (XCS && su) ? __ldg(XM + cc) : v);
     }
     if constexpr (NB % 4 == 0) {
       uint4* d = reinterpret_cast<uint4*>(sl + lane * (NB * 4));
@@ -853,8 +874,8 @@ __global__ void __launch_bounds__(32 * kTpgWarps, 1)
           code_max = umax32(code_max, c);
           const uint32_t cc = umin32(c, dict_last);
           bool su;
-          v = xc4_tpg(cc, xk, su);
-          if (su) v = __ldg(XM + cc);
+          v = translate(cc, su);
+          if (XCS && su) v = __ldg(XM + cc);
         } else if (row < n_total) {
           v = __ldg(XD + (rank ? __ldg(rank + (row - n_main)) : (uint32_t)(row - n_main)));
         }
@@ -990,26 +1011,62 @@ static uint32_t tpg_smem() {
   }();
   return optin > 1024 ? (uint32_t)(optin - 1024) : 0u;
 }
-template <int B, int NB>
+// XC budget that leaves room for kTpgMinWarps warps' slots (slots: 128 b' bytes for b' - b in {0, 1})
+template <int NB>
 uint32_t tpg_budget() {
-  const int64_t b = (int64_t)tpg_smem() - kTpgHdrBytes - 128 - (int64_t)kTpgMinWarps * kTpgSlots * Tpg<B, NB>::slot_bytes;
+  const int64_t b = (int64_t)tpg_smem() - kTpgHdrBytes - 128 - (int64_t)kTpgMinWarps * kTpgSlots * Tpg<NB, NB>::slot_bytes;
   return b > 0 ? (uint32_t)(b & ~15ll) : 0u;
 }
-template <int B, int NB>
+// Which (b', mode) pairs use the thread-per-group kernel: XC in shared memory
+// and the plain X_M through L2 (b, b' >= 15: |U_M| * 4 > 96 KB).  Measured and
+// not used: XC through L2 (cfg5 Step 2(b) 39.2 vs 11.9 ms: 32 dependent-load
+// chains per lane) and the plain X_M in shared memory (cfg1 0.031 vs 0.017 ms:
+// a small column is latency-bound on the per-CTA staging and the few tiles).
+// cfg3 (plain X_M through L2): 0.298 vs 0.318 ms.
+template <int NB, int XMODE>
+constexpr bool tpg_has() {
+  return NB >= kTpgMinWidth && NB <= 32 && (XMODE == XM_XC_SMEM || XMODE == XM_RAW_GLOBAL);
+}
+template <int B, int NB, int XMODE>
 void launch_tpg(const dm_column_in* in, const dm_column_out* out, const uint32_t* xm, const uint32_t* xd,
                 const uint32_t* rank, dm_header* hdr, cudaStream_t st, uint32_t fixed_bits, const uint2* xrec,
                 const uint8_t* xoffs, uint32_t budget, uint32_t dens, uint32_t xs) {
-  auto kern = k_recompress_tpg<B, NB>;
-  const uint32_t smem = tpg_smem();
+  auto kern = k_recompress_tpg<B, NB, XMODE>;
+  constexpr uint32_t slots = kTpgWarps * kTpgSlots * Tpg<B, NB>::slot_bytes;
+  const uint32_t smem = XMODE == XM_XC_SMEM ? tpg_smem()
+                        : XMODE == XM_RAW_SMEM
+                            ? (uint32_t)((kTpgHdrBytes + in->dict_len * 4 + 127) & ~127ull) + slots
+                            : kTpgHdrBytes + slots;
   ensure_smem((const void*)kern);
   const uint64_t tiles = (in->n_main + in->n_delta + 1023) / 1024;
   const unsigned grid = (unsigned)std::max<uint64_t>(
       1, std::min<uint64_t>(tiles, (uint64_t)device_sms() * rec_grid_percent() / 100));
-  (void)xs;  // 8: 256-code blocks
-  const TpgK kc{1u << 23, 1u << 18, 1u << 25, 1u << 30, 2u, 4u, 8u, 32u, 128u, 1024u, 0xfffffffeu};
+  const TpgK kc{1u << 23, 1u << 18, 1u << 25, 1u << 30, 2u, 4u, 8u, 32u, 128u, 1024u, 0xfffffffeu, xs};
   launch_k(kern, grid, 32 * kTpgWarps, smem, st, in->main_codes, in->n_main, in->dict_len, xm, xd, rank, in->n_delta,
            out->merged_codes, hdr, fixed_bits, xrec, xoffs, budget, dens, kc, smem);
   note_launch();
+}
+// The thread-per-group kernel for b' = NB and the caller's b when one exists
+// (knob 6 = 0, b' - b in {0, 1}); false: the caller launches the warp-per-group kernel.
+template <int NB, int XMODE>
+bool try_tpg(const dm_column_in* in, const dm_column_out* out, const uint32_t* xm, const uint32_t* xd,
+             const uint32_t* rank, dm_header* hdr, cudaStream_t st, uint32_t fixed_bits, const uint2* xrec,
+             const uint8_t* xoffs, uint32_t budget, uint32_t dens, uint32_t xs) {
+  if constexpr (!tpg_has<NB, XMODE>()) {
+    return false;
+  } else {
+    // not inside dm_merge_table: there the capped Step 2(b) grids co-run with other
+    // columns' Step 1 kernels, and the warp-per-group kernel measured faster
+    // (cfg4 13.99 vs 14.31 ms)
+    if (tuning(6) != 0 || t_table_merge) return false;
+    if (in->main_bits == (uint32_t)NB)
+      launch_tpg<NB, NB, XMODE>(in, out, xm, xd, rank, hdr, st, fixed_bits, xrec, xoffs, budget, dens, xs);
+    else if (in->main_bits + 1 == (uint32_t)NB)
+      launch_tpg<NB - 1, NB, XMODE>(in, out, xm, xd, rank, hdr, st, fixed_bits, xrec, xoffs, budget, dens, xs);
+    else
+      return false;
+    return true;
+  }
 }
 
 template <int NB>
@@ -1033,8 +1090,19 @@ cudaError_t launch_nb(const dm_column_in* in, const dm_column_out* out, const ui
     note_launch();
   };
   const size_t ring = kRecHdrBytes + (size_t)kRecStages * in_stage;
+  auto tpg = [&](auto mode, uint32_t budget) {
+    if constexpr (NB <= 0)
+      return false;
+    else
+      return try_tpg<NB, decltype(mode)::value>(in, out, xm, xd, rank, hdr, st, fixed_bits, xrec, xoffs, budget, dens,
+                                                xs);
+  };
+  using RawSmem = std::integral_constant<int, XM_RAW_SMEM>;
+  using RawGlobal = std::integral_constant<int, XM_RAW_GLOBAL>;
+  using XcSmem = std::integral_constant<int, XM_XC_SMEM>;
+  using XcGlobal = std::integral_constant<int, XM_XC_GLOBAL>;
   if (in->dict_len * 4 <= kRecSmemXBytes) {
-    go(k_recompress<NB, XM_RAW_SMEM>, ring + in->dict_len * 4, 0);
+    if (!tpg(RawSmem{}, 0)) go(k_recompress<NB, XM_RAW_SMEM>, ring + in->dict_len * 4, 0);
     return cudaGetLastError();
   }
   const int knob = tuning(0);
@@ -1045,7 +1113,7 @@ cudaError_t launch_nb(const dm_column_in* in, const dm_column_out* out, const ui
     return cudaGetLastError();
   } else {
   if (!xrec || knob == 1) {
-    go(k_recompress<NB, XM_RAW_GLOBAL>, ring, 0);
+    if (!tpg(RawGlobal{}, 0)) go(k_recompress<NB, XM_RAW_GLOBAL>, ring, 0);
     return cudaGetLastError();
   }
   // compact table available: the smem variant (if its records can fit at all)
@@ -1054,38 +1122,34 @@ cudaError_t launch_nb(const dm_column_in* in, const dm_column_out* out, const ui
   const bool want_smem = (knob == 2 || auto_smem) && xs == 8;
   if (auto_smem) dens = 6;  // <= 4 entries per 256-code block on average
   if (knob == 0 && !auto_smem && !xc_only && in->dict_len * 4 <= kXcGlobalMinBytes) {
-    go(k_recompress<NB, XM_RAW_GLOBAL>, ring, 0);
+    if (!tpg(RawGlobal{}, 0)) go(k_recompress<NB, XM_RAW_GLOBAL>, ring, 0);
     return cudaGetLastError();
   }
   const uint32_t budget0 = want_smem ? xc_smem_budget(in_stage_xc) : 0u;
   uint32_t budget = (uint64_t)xc_nsb(in->dict_len, xs) * kXcRecBytes + 16 <= budget0 ? budget0 : 0u;
   const bool xc_l2 = xc_only || knob == 2 || knob == 3 || in->dict_len * 4 > kXcGlobalMinBytes;
-  bool tpg = false;
+  bool tpg_smem_run = false;
   if constexpr (NB >= kTpgMinWidth) {  // thread-per-group form for b' - b in {0, 1} (knob 6); its rare
     // lookups read the plain X_M, which is whole when the companion is the plain-X_M kernel
-    if (want_smem && !xc_l2 && tuning(6) == 0 &&
+    if (want_smem && !xc_l2 && tpg_has<NB, XM_XC_SMEM>() && tuning(6) == 0 && !t_table_merge &&
         (in->main_bits == (uint32_t)NB || in->main_bits + 1 == (uint32_t)NB)) {
-      const uint32_t bt = in->main_bits == (uint32_t)NB ? tpg_budget<NB, NB>() : tpg_budget<NB - 1, NB>();
+      const uint32_t bt = tpg_budget<NB>();
       if ((uint64_t)xc_nsb(in->dict_len, xs) * kXcRecBytes + 16 <= bt) {
         budget = bt;
-        dens = auto_smem ? 6 : 0;
-        if (in->main_bits == (uint32_t)NB)
-          launch_tpg<NB, NB>(in, out, xm, xd, rank, hdr, st, fixed_bits, xrec, xoffs, budget, dens, xs);
-        else
-          launch_tpg<NB - 1, NB>(in, out, xm, xd, rank, hdr, st, fixed_bits, xrec, xoffs, budget, dens, xs);
-        tpg = true;
+        tpg_smem_run = tpg(XcSmem{}, budget);
       }
     }
   }
-  if (budget && !tpg)
+  if (budget && !tpg_smem_run)
     go(k_recompress<NB, XM_XC_SMEM>, kRecHdrBytes + (size_t)kRecStagesXc * in_stage_xc + budget, budget,
        rec_threads<XM_XC_SMEM>(), rec_groups<XM_XC_SMEM>());
   // (A persisting L2 access-policy window over XC was measured: no gain on
   // cfg5's Step 2(b), and the set-aside slowed Steps 1(a)/1(b) by 40%.)
-  if (xc_l2)
-    go(k_recompress<NB, XM_XC_GLOBAL>, ring, budget);
-  else
-    go(k_recompress<NB, XM_RAW_GLOBAL>, ring, budget);
+  if (xc_l2) {
+    if (!tpg(XcGlobal{}, budget)) go(k_recompress<NB, XM_XC_GLOBAL>, ring, budget);
+  } else {
+    if (!tpg(RawGlobal{}, budget)) go(k_recompress<NB, XM_RAW_GLOBAL>, ring, budget);
+  }
   return cudaGetLastError();
   }
 }
