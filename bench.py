@@ -541,7 +541,8 @@ def main():
     if not table:
         s2_ms = statistics.mean(s2)
         achieved = s2b / (s2_ms / 1e3) / 1e9
-        roofline = {"kernel": "k_recompress (Step 2(b))", "bound": "hbm", "achieved": achieved,
+        roofline = {"kernel": "Step 2(b) (%s)" % (tinfo.get("kernel") or "k_recompress").split("(")[0].strip(),
+                    "bound": "hbm", "achieved": achieved,
                     "peak": peak_hbm, "unit": "GB/s", "frac": achieved / peak_hbm, "traffic": traffic,
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if pk else "fallback 6.65 TB/s",
                     "algorithmic_bytes_per_launch": s2b,

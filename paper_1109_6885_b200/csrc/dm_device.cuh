@@ -68,6 +68,16 @@ struct KeyU64 {
   __device__ __forceinline__ static void store(void* p, uint64_t i, K k) {
     static_cast<uint64_t*>(p)[i] = k;
   }
+  // read-only load with an L2 eviction-priority hint (createpolicy); streaming store
+  __device__ __forceinline__ static K load_hint(const void* p, uint64_t i, uint64_t pol) {
+    K v;
+    asm volatile("ld.global.nc.L2::cache_hint.u64 %0, [%1], %2;"
+                 : "=l"(v) : "l"(static_cast<const uint64_t*>(p) + i), "l"(pol));
+    return v;
+  }
+  __device__ __forceinline__ static void store_cs(void* p, uint64_t i, K k) {
+    __stcs(reinterpret_cast<unsigned long long*>(static_cast<uint64_t*>(p) + i), (unsigned long long)k);
+  }
   // coherent (L2) load of a value written by another SM in the same kernel
   __device__ __forceinline__ static K load_cg(const void* p, uint64_t i) {
     return __ldcg(static_cast<const uint64_t*>(p) + i);
@@ -95,6 +105,13 @@ struct KeyU32 {
     return __ldg(static_cast<const uint32_t*>(p) + i);
   }
   __device__ __forceinline__ static void store(void* p, uint64_t i, K k) { static_cast<uint32_t*>(p)[i] = k; }
+  __device__ __forceinline__ static K load_hint(const void* p, uint64_t i, uint64_t pol) {
+    K v;
+    asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;"
+                 : "=r"(v) : "l"(static_cast<const uint32_t*>(p) + i), "l"(pol));
+    return v;
+  }
+  __device__ __forceinline__ static void store_cs(void* p, uint64_t i, K k) { __stcs(static_cast<uint32_t*>(p) + i, k); }
   __device__ __forceinline__ static K load_cg(const void* p, uint64_t i) {
     return __ldcg(static_cast<const uint32_t*>(p) + i);
   }
@@ -127,6 +144,17 @@ struct KeyB16 {
   }
   __device__ __forceinline__ static void store(void* p, uint64_t i, K k) {
     static_cast<ulonglong2*>(p)[i] = make_ulonglong2(bswap(k.hi), bswap(k.lo));
+  }
+  __device__ __forceinline__ static K load_hint(const void* p, uint64_t i, uint64_t pol) {
+    uint64_t x, y;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.u64 {%0, %1}, [%2], %3;"
+                 : "=l"(x), "=l"(y) : "l"(static_cast<const ulonglong2*>(p) + i), "l"(pol));
+    return K{bswap(x), bswap(y)};
+  }
+  __device__ __forceinline__ static void store_cs(void* p, uint64_t i, K k) {
+    const uint64_t a = bswap(k.hi), b = bswap(k.lo);
+    __stcs(reinterpret_cast<uint4*>(static_cast<ulonglong2*>(p) + i),
+           make_uint4((uint32_t)a, (uint32_t)(a >> 32), (uint32_t)b, (uint32_t)(b >> 32)));
   }
   __device__ __forceinline__ static K load_cg(const void* p, uint64_t i) {
     const ulonglong2 v = __ldcg(static_cast<const ulonglong2*>(p) + i);

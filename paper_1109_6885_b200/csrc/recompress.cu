@@ -436,16 +436,29 @@ __global__ void __launch_bounds__(rec_threads<XMODE>(), XMODE == XM_XC_SMEM ? 1 
   const uint64_t rec_pad = (nsb * kXcRecBytes + 15) & ~15ull;
   const uint32_t* soffs = reinterpret_cast<const uint32_t*>(reinterpret_cast<unsigned char*>(sx) + rec_pad);
   if (XMODE == XM_XC_SMEM) {
-    const uint4* src = reinterpret_cast<const uint4*>(xrec);  // two 8-byte records -> four 4-byte ones
-    uint4* dst = reinterpret_cast<uint4*>(sx);
-    for (uint64_t i = threadIdx.x; i < rec_pad / 16; i += blockDim.x) {
-      const uint4 v = __ldg(src + i);
-      dst[i] = make_uint4(xc4_record(make_uint2(v.x, v.y), 0), xc4_record(make_uint2(v.x, v.y), 1),
-                          xc4_record(make_uint2(v.z, v.w), 0), xc4_record(make_uint2(v.z, v.w), 1));
+    // one bulk copy of the records and one of the lists (the global arrays are
+    // padded to 16 bytes), then two 8-byte records -> four 4-byte ones in place
+    uint64_t* stage_bar = empty + S;  // header bytes [64, 72): after full[4], empty[4]
+    static_assert(2 * S * 8 + 8 <= 128, "staging barrier fits before the mask table");
+    if (threadIdx.x == 0) {
+      mbar_init(stage_bar, 1);
+      fence_mbar_init();
     }
-    const uint4* go = reinterpret_cast<const uint4*>(xoffs);
-    uint4* so = dst + rec_pad / 16;
-    for (uint64_t i = threadIdx.x; i < xc_offs_bytes / 16; i += blockDim.x) so[i] = __ldg(go + i);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      mbar_arrive_expect_tx(stage_bar, (uint32_t)(rec_pad + xc_offs_bytes));
+      tma_load_1d(sx, xrec, (uint32_t)rec_pad, stage_bar, policy_evict_last());
+      if (xc_offs_bytes)
+        tma_load_1d(reinterpret_cast<unsigned char*>(sx) + rec_pad, xoffs, (uint32_t)xc_offs_bytes, stage_bar,
+                    policy_evict_last());
+    }
+    mbar_wait_parity(stage_bar, 0);
+    uint4* d = reinterpret_cast<uint4*>(sx);
+    for (uint32_t i = threadIdx.x; i < rec_pad / 16; i += blockDim.x) {
+      const uint4 v = d[i];
+      d[i] = make_uint4(xc4_record(make_uint2(v.x, v.y), 0), xc4_record(make_uint2(v.x, v.y), 1),
+                        xc4_record(make_uint2(v.z, v.w), 0), xc4_record(make_uint2(v.z, v.w), 1));
+    }
   }
   __syncthreads();
 
