@@ -686,12 +686,12 @@ __global__ void __launch_bounds__(kSpThreads) k_sp_count(const void* __restrict_
   const uint64_t a = t * T;
   const uint32_t na = (uint32_t)umin64(T, nA - a);
   const uint64_t lo = part[t], nb = part[t + 1] - lo;
-  // U_M is read again by the write pass: keep it in L2 (evict-last; cfg2's 80 MB fits)
-  const uint64_t pol = policy_evict_last();
+  // (measured: an evict-last hint here, evict-first / streaming in the write pass,
+  // made Step 1(b) slower: cfg2 0.100 -> 0.103 ms, cfg5 7.56 -> 8.81 ms)
 #pragma unroll
   for (uint32_t r = 0; r < IT; ++r) {
     const uint32_t i = threadIdx.x + r * NT;
-    if (i < na) sk[i] = KT::load_hint(A, a + i, pol);
+    if (i < na) sk[i] = KT::load(A, a + i);
   }
   __syncthreads();
   uint32_t dups = 0;
@@ -737,13 +737,11 @@ __global__ void __launch_bounds__(kSpThreads) k_sp_write(const void* __restrict_
   const uint64_t base = a + E;
   for (uint32_t i = threadIdx.x; i <= T; i += NT) scnt[i] = 0;
   // the tile's U_M values (registers; the copy needs no staging)
-  // last read of U_M (evict-first); U' and X_M leave by streaming stores (not re-read by the merge)
-  const uint64_t pol = policy_evict_first();
   K v[IT];
 #pragma unroll
   for (uint32_t r = 0; r < IT; ++r) {
     const uint32_t i = threadIdx.x + r * NT;
-    if (i < na) v[r] = KT::load_hint(A, a + i, pol);
+    if (i < na) v[r] = KT::load(A, a + i);
   }
   __syncthreads();
   for (uint64_t j = threadIdx.x; j < nb; j += NT) {
@@ -779,8 +777,8 @@ __global__ void __launch_bounds__(kSpThreads) k_sp_write(const void* __restrict_
     if (i >= na) continue;
     const uint32_t sh = scnt[i];
     const uint64_t out = base + i + sh;
-    KT::store_cs(U, out, v[r]);
-    if (XM) __stcs(XM + a + i, (uint32_t)out);
+    KT::store(U, out, v[r]);
+    if (XM) XM[a + i] = (uint32_t)out;
     if (rblk) {  // XC block samples R(g) = X_M[2^xs g] - 2^xs g
       if (((a + i) & bmask) == 0) rblk[(a + i) >> xs] = (uint32_t)(E + sh);
       if (a + i == nA - 1) rblk[(nA + bmask) >> xs] = (uint32_t)(E + sh);
