@@ -727,14 +727,32 @@ __global__ void __launch_bounds__(256) k_dedup_insert(const void* __restrict__ D
 // |U_D|); not found -> compacted (warp-aggregated atomic) into the keys Step
 // 1(a)'s sort sees.  (A binary search of U_M with a shared-memory sample was
 // measured first: ~10 dependent L2 round trips per tuple, 0.60 ms on cfg3.)
+// Table entries are (tag | position): the position in the low pos_bits =
+// ceil(log2 |U_M|) bits, the value hash's low bits above them (the lowest tag
+// bit cleared, so no entry equals the empty word), so a probe loads U_M only
+// when the tag matches.  Measured on cfg3 before the tags (load factor 1/2,
+// every probe loading U_M): a warp walked ~6.8 probe steps per tuple batch (the
+// longest chain of its 32 lanes), each two dependent loads -- 152 us for 5e6 tuples.
 constexpr uint32_t kPfEmpty = 0xffffffffu;
+struct PfTag {
+  uint32_t pos_mask, tag_mask;
+  __host__ __device__ static PfTag make(uint64_t nM) {
+    uint32_t b = 1;
+    while (b < 32 && (1ull << b) < nM) ++b;
+    const uint32_t pm = b >= 32 ? 0xffffffffu : (1u << b) - 1u;
+    return PfTag{pm, b >= 32 ? 0u : ~pm & ~(1u << b)};
+  }
+  __device__ __forceinline__ uint32_t tag(uint64_t h) const { return (uint32_t)h & tag_mask; }
+};
 template <class KT>
 __global__ void __launch_bounds__(256) k_pf_build(const void* __restrict__ UM, uint64_t nM, uint32_t* __restrict__ table,
-                                                  uint64_t mask) {
+                                                  uint64_t mask, PfTag tg) {
   pdl_prologue();
   for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < nM; p += (uint64_t)gridDim.x * blockDim.x) {
-    uint64_t slot = (dd_hash(KT::load(UM, p)) >> 32) & mask;
-    while (atomicCAS(table + slot, kPfEmpty, (uint32_t)p) != kPfEmpty) slot = (slot + 1) & mask;
+    const uint64_t h = dd_hash(KT::load(UM, p));
+    uint64_t slot = (h >> 32) & mask;
+    const uint32_t e = (uint32_t)p | tg.tag(h);
+    while (atomicCAS(table + slot, kPfEmpty, e) != kPfEmpty) slot = (slot + 1) & mask;
   }
 }
 
@@ -748,7 +766,7 @@ __global__ void __launch_bounds__(kPfThreads) k_pf_probe(const void* __restrict_
                                                          const uint32_t* __restrict__ table, uint64_t mask,
                                                          const void* __restrict__ D, uint64_t n,
                                                          uint32_t* __restrict__ src, void* __restrict__ newkeys,
-                                                         unsigned long long* n_new, uint32_t* used) {
+                                                         unsigned long long* n_new, uint32_t* used, PfTag tg) {
   pdl_prologue();
   using K = typename KT::K;
   constexpr int TILE = kPfThreads * kPfItems;
@@ -758,28 +776,60 @@ __global__ void __launch_bounds__(kPfThreads) k_pf_probe(const void* __restrict_
     K v[kPfItems];
     uint32_t p[kPfItems];
     uint32_t nnew = 0;
+    // the kPfItems probes of a thread as independent loads, step by step (key,
+    // first slot, candidate's U_M value); an item whose first slot holds another
+    // value continues alone in a loop
+    uint64_t h[kPfItems];
+    uint32_t q[kPfItems];
+#pragma unroll
+    for (int r = 0; r < kPfItems; ++r) {
+      const uint64_t i = base + (uint64_t)r * kPfThreads + threadIdx.x;
+      v[r] = KT::load(D, i < n ? i : n - 1);
+      h[r] = dd_hash(v[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < kPfItems; ++r) q[r] = __ldg(table + ((h[r] >> 32) & mask));
+    bool hit[kPfItems];
+#pragma unroll
+    for (int r = 0; r < kPfItems; ++r) {
+      const bool cand = q[r] != kPfEmpty && (q[r] & tg.tag_mask) == tg.tag(h[r]);
+      hit[r] = cand && KT::eq(KT::load(UM, cand ? q[r] & tg.pos_mask : 0u), v[r]);
+    }
 #pragma unroll
     for (int r = 0; r < kPfItems; ++r) {
       const uint64_t i = base + (uint64_t)r * kPfThreads + threadIdx.x;
       p[r] = kPfEmpty;
       if (i < n) {
-        v[r] = KT::load(D, i);
-        uint64_t slot = (dd_hash(v[r]) >> 32) & mask;
-        for (;;) {
-          const uint32_t q = __ldg(table + slot);
-          if (q == kPfEmpty || KT::eq(KT::load(UM, q), v[r])) {
-            p[r] = q;
-            break;
+        if (hit[r]) {
+          p[r] = q[r] & tg.pos_mask;
+        } else if (q[r] != kPfEmpty) {  // the first slot holds another value: walk on
+          const uint32_t tag = tg.tag(h[r]);
+          uint64_t slot = (h[r] >> 32) & mask;
+          for (;;) {
+            slot = (slot + 1) & mask;
+            const uint32_t e = __ldg(table + slot);
+            if (e == kPfEmpty) break;
+            if ((e & tg.tag_mask) == tag && KT::eq(KT::load(UM, e & tg.pos_mask), v[r])) {
+              p[r] = e & tg.pos_mask;
+              break;
+            }
           }
-          slot = (slot + 1) & mask;
         }
-        if (p[r] == kPfEmpty) {
-          ++nnew;
-        } else {
-          src[i] = p[r];
-          const uint32_t bit = 1u << (p[r] & 31);
-          if (!(used[p[r] >> 5] & bit)) atomicOr(&used[p[r] >> 5], bit);
-        }
+      }
+    }
+    uint32_t uw[kPfItems];  // the "used" words, loaded together
+#pragma unroll
+    for (int r = 0; r < kPfItems; ++r) uw[r] = p[r] != kPfEmpty ? used[p[r] >> 5] : 0xffffffffu;
+#pragma unroll
+    for (int r = 0; r < kPfItems; ++r) {
+      const uint64_t i = base + (uint64_t)r * kPfThreads + threadIdx.x;
+      if (i >= n) continue;
+      if (p[r] == kPfEmpty) {
+        ++nnew;
+      } else {
+        src[i] = p[r];
+        const uint32_t bit = 1u << (p[r] & 31);
+        if (!(uw[r] & bit)) atomicOr(&used[p[r] >> 5], bit);
       }
     }
     uint32_t tot;
@@ -893,12 +943,13 @@ cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, void* udict
     const int sms = device_sms();
     uint32_t* table = reinterpret_cast<uint32_t*>(ws + L.pf_table);
     cudaMemsetAsync(table, 0xff, L.pf_cap * 4, st);
+    const PfTag tg = PfTag::make(in->dict_len);
     launch_k(k_pf_build<KT>, (unsigned)std::min<uint64_t>((in->dict_len + 255) / 256, (uint64_t)sms * 8), 256, 0, st,
-             in->main_dict, in->dict_len, table, L.pf_cap - 1);
+             in->main_dict, in->dict_len, table, L.pf_cap - 1, tg);
     launch_k(k_pf_probe<KT>, (unsigned)std::min<uint64_t>((n + 1023) / 1024, (uint64_t)sms * 8), kPfThreads, 0, st,
              in->main_dict, (const uint32_t*)table, L.pf_cap - 1, in->delta, n,
              reinterpret_cast<uint32_t*>(ws + L.pf_src), (void*)(ws + L.pf_keys), n_new,
-             reinterpret_cast<uint32_t*>(ws + L.pf_used));
+             reinterpret_cast<uint32_t*>(ws + L.pf_used), tg);
     note_launch(2);
     D = ws + L.pf_keys;
     n_dev = n_new;

@@ -191,8 +191,8 @@ WsLayout ws_layout(const dm_column_in* in) {
     L.pf_keys = take(nD * E);
     L.pf_rank = take(nD * 4);
     L.pf_codes = take(nD * 4);
-    uint64_t cap = 1024;
-    while (cap < 2 * in->dict_len) cap <<= 1;
+    uint64_t cap = 1024;  // load factor <= 1/4: a warp's longest probe chain stays short
+    while (cap < 4 * in->dict_len) cap <<= 1;
     L.pf_cap = cap;
     L.pf_table = take(cap * 4);
   }

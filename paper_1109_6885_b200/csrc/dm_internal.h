@@ -178,8 +178,8 @@ struct WsLayout {
   size_t pf_keys;        // probe-first: the delta values not found in U_M (raw layout), n_delta capacity
   size_t pf_rank;        // probe-first: u32[n_delta] rank of each compacted value among the new values
   size_t pf_codes;       // probe-first: u32[n_delta] the delta tuples' final codes (Step 2(b) input)
-  size_t pf_table;       // probe-first: u32[pf_cap] U_M positions by value hash (0xff.. = empty)
-  uint64_t pf_cap;       // probe-first: table slots (power of two >= 2 |U_M|)
+  size_t pf_table;       // probe-first: u32[pf_cap] (hash tag | U_M position) by value hash (0xff.. = empty)
+  uint64_t pf_cap;       // probe-first: table slots (power of two >= 4 |U_M|)
   bool probe;            // probe-first buffers laid out (probe_possible)
   size_t dd_slots;       // dedup (NEXT1): u64[dd_cap] (tag | id << 32) slots (memset per call)
   size_t dd_keys;        // dedup: distinct values, raw layout, n_delta capacity
