@@ -1001,6 +1001,15 @@ static int rec_grid_percent() {
   return v ? v : t_table_merge ? 25 : 100;
 }
 
+// Experiments: DM_TPG_TABLE=1 lets dm_merge_table use the thread-per-group kernel too.
+static bool tpg_in_tables() {
+  static const bool v = [] {
+    const char* e = std::getenv("DM_TPG_TABLE");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+
 // Shared-memory bytes left for XC next to a kRecStagesXc-deep ring.
 static uint32_t xc_smem_budget(uint32_t in_stage) {
   static int optin = [] {
@@ -1071,7 +1080,7 @@ bool try_tpg(const dm_column_in* in, const dm_column_out* out, const uint32_t* x
     // not inside dm_merge_table: there the capped Step 2(b) grids co-run with other
     // columns' Step 1 kernels, and the warp-per-group kernel measured faster
     // (cfg4 13.99 vs 14.31 ms)
-    if (tuning(6) != 0 || t_table_merge) return false;
+    if (tuning(6) != 0 || (t_table_merge && !tpg_in_tables())) return false;
     if (in->main_bits == (uint32_t)NB)
       launch_tpg<NB, NB, XMODE>(in, out, xm, xd, rank, hdr, st, fixed_bits, xrec, xoffs, budget, dens, xs);
     else if (in->main_bits + 1 == (uint32_t)NB)
@@ -1144,7 +1153,7 @@ cudaError_t launch_nb(const dm_column_in* in, const dm_column_out* out, const ui
   bool tpg_smem_run = false;
   if constexpr (NB >= kTpgMinWidth) {  // thread-per-group form for b' - b in {0, 1} (knob 6); its rare
     // lookups read the plain X_M, which is whole when the companion is the plain-X_M kernel
-    if (want_smem && !xc_l2 && tpg_has<NB, XM_XC_SMEM>() && tuning(6) == 0 && !t_table_merge &&
+    if (want_smem && !xc_l2 && tpg_has<NB, XM_XC_SMEM>() && tuning(6) == 0 && (!t_table_merge || tpg_in_tables()) &&
         (in->main_bits == (uint32_t)NB || in->main_bits + 1 == (uint32_t)NB)) {
       const uint32_t bt = tpg_budget<NB>();
       if ((uint64_t)xc_nsb(in->dict_len, xs) * kXcRecBytes + 16 <= bt) {
