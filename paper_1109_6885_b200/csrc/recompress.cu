@@ -359,6 +359,31 @@ __device__ __forceinline__ uint32_t xc_lookup(uint32_t code, uint32_t xs, const 
   return flagged ? xm_flagged : code + start + (cnt >> 3);
 }
 
+// xc_lookup<false> without its tail loop, for the thread-per-group kernel: `slow`
+// when the list runs past the two 16-byte windows (rare: > 16 entries from the
+// window start); the caller finishes those rows after the straight-line pass.
+__device__ __forceinline__ uint32_t xc_l2_fast(uint32_t code, uint32_t xs, const uint2* __restrict__ rec,
+                                               const uint32_t* __restrict__ offs32, const uint32_t* __restrict__ XM,
+                                               uint64_t pol, bool& slow) {
+  const uint32_t sb = code >> (xs + 2), t8 = 8 * ((code >> xs) & 3u), o = code & ((1u << xs) - 1u);
+  const uint2 r = ld_gather_v2(rec + sb, pol);
+  const bool flagged = r.x >> 31;
+  const uint32_t xm_flagged = flagged ? __ldg(XM + code) : 0u;
+  const uint32_t s_rel = ((r.y << 8) >> t8) & 255, e_rel = (r.y >> t8) & 255;
+  const uint32_t start = (r.x & 0x7fffffffu) + s_rel, n = flagged ? 0u : e_rel - s_rel;
+  const uint32_t ob = o * 0x01010101u;
+  const uint32_t s0 = start & 15u;
+  const uint4* base4 = reinterpret_cast<const uint4*>(offs32) + (start >> 4);
+  const uint4 v = ld_gather_v4(base4, pol);
+  const uint4 w = s0 + n > 16u ? ld_gather_v4(base4 + 1, pol) : make_uint4(0, 0, 0, 0);
+  const uint32_t k = umin32(n, 32u - s0), e0 = s0 + k;
+  const uint32_t cnt = count_lt(v.x, ob, 0, s0, e0) + count_lt(v.y, ob, 1, s0, e0) + count_lt(v.z, ob, 2, s0, e0) +
+                       count_lt(v.w, ob, 3, s0, e0) + count_lt(w.x, ob, 4, s0, e0) + count_lt(w.y, ob, 5, s0, e0) +
+                       count_lt(w.z, ob, 6, s0, e0) + count_lt(w.w, ob, 7, s0, e0);
+  slow = n > k;
+  return flagged ? xm_flagged : code + start + (cnt >> 3);
+}
+
 template <int XMODE>
 __host__ __device__ constexpr int rec_consumer_warps() { return XMODE == XM_XC_SMEM ? 28 : kRecConsumerWarps; }
 // 32-row groups per chunk: a multiple of 4 (16-byte aligned chunks at any width)
@@ -767,10 +792,17 @@ __global__ void __launch_bounds__(32 * kTpgWarps, 1)
     else if constexpr (XS)
       return sx[cc];
     else if constexpr (XMODE == XM_XC_GLOBAL)
-      return xc_lookup<false>(cc, kc.xs, xrec, reinterpret_cast<const uint32_t*>(xoffs), XM, pol_x);
+      return xc_l2_fast(cc, kc.xs, xrec, reinterpret_cast<const uint32_t*>(xoffs), XM, pol_x, slow);
     else
       return ld_gather_u32(XM + cc, pol_x);
   };
+  auto exact = [&](uint32_t cc) -> uint32_t {  // the rare rows `translate` could not finish
+    if constexpr (XMODE == XM_XC_GLOBAL)
+      return xc_lookup<false>(cc, kc.xs, xrec, reinterpret_cast<const uint32_t*>(xoffs), XM, pol_x);
+    else
+      return __ldg(XM + cc);  // XC in smem: the plain X_M is whole whenever that kernel runs
+  };
+  constexpr bool XCG = XMODE == XM_XC_GLOBAL;
   const uint32_t dict_last = (uint32_t)dict_len - 1u;
   uint32_t code_max = 0;
   const uint64_t n_total = n_main + n_delta;
@@ -828,6 +860,7 @@ __global__ void __launch_bounds__(32 * kTpgWarps, 1)
     uint32_t o[NB];
 #pragma unroll
     for (int i = 0; i < NB; ++i) o[i] = 0;
+    uint32_t smask = 0;  // XC through L2: rows whose list runs past the read windows
 #pragma unroll
     for (int r = 0; r < 32; ++r) {
       const uint32_t c = tpg_code<B>(w, r);
@@ -835,6 +868,7 @@ __global__ void __launch_bounds__(32 * kTpgWarps, 1)
       const uint32_t cc = umin32(c, dict_last);
       bool su;
       const uint32_t v = translate(cc, su);
+      if (XCG) smask |= (uint32_t)su << r;
       tpg_put<NB>(o, r, (XCS && su) ? __ldg(XM + cc) : v);
     }
     if constexpr (NB % 4 == 0) {
@@ -849,6 +883,26 @@ __global__ void __launch_bounds__(32 * kTpgWarps, 1)
       uint32_t* d = reinterpret_cast<uint32_t*>(sl) + lane * NB;
 #pragma unroll
       for (int i = 0; i < NB; ++i) d[i] = o[i];
+    }
+    if (XCG && smask) {  // rare, per lane: exact values patched into the staged output words
+      uint32_t* ow = reinterpret_cast<uint32_t*>(sl) + lane * NB;
+      const uint32_t* M32 = reinterpret_cast<const uint32_t*>(M);
+      constexpr uint32_t cmask = B == 32 ? 0xffffffffu : (1u << B) - 1u;
+      constexpr uint64_t vmask = NB == 32 ? 0xffffffffull : (1ull << NB) - 1ull;
+      do {
+        const uint32_t r = __ffs(smask) - 1;
+        smask &= smask - 1;
+        const uint64_t bi = ((t * 32 + lane) * 32 + r) * (uint64_t)B;  // the row's bit offset in M
+        const uint64_t wi = bi >> 5;
+        const uint32_t hi = wi + 1 < 2 * dwords(n_main, B) ? __ldg(M32 + wi + 1) : 0u;
+        const uint32_t c = __funnelshift_r(__ldg(M32 + wi), hi, (uint32_t)(bi & 31)) & cmask;
+        const uint64_t v = exact(umin32(c, dict_last));
+        const uint32_t ob = r * NB, i = ob >> 5, sh = ob & 31;
+        uint64_t x = ow[i] | (i + 1 < (uint32_t)NB ? (uint64_t)ow[i + 1] << 32 : 0ull);
+        x = (x & ~(vmask << sh)) | (v << sh);
+        ow[i] = (uint32_t)x;
+        if (i + 1 < (uint32_t)NB) ow[i + 1] = (uint32_t)(x >> 32);
+      } while (smask);
     }
     fence_proxy_async_smem();
     __syncwarp();
@@ -888,7 +942,7 @@ __global__ void __launch_bounds__(32 * kTpgWarps, 1)
           const uint32_t cc = umin32(c, dict_last);
           bool su;
           v = translate(cc, su);
-          if (XCS && su) v = __ldg(XM + cc);
+          if (su) v = exact(cc);
         } else if (row < n_total) {
           v = __ldg(XD + (rank ? __ldg(rank + (row - n_main)) : (uint32_t)(row - n_main)));
         }
@@ -1041,13 +1095,19 @@ uint32_t tpg_budget() {
 }
 // Which (b', mode) pairs use the thread-per-group kernel: XC in shared memory
 // and the plain X_M through L2 (b, b' >= 15: |U_M| * 4 > 96 KB).  Measured and
-// not used: XC through L2 (cfg5 Step 2(b) 39.2 vs 11.9 ms: 32 dependent-load
-// chains per lane) and the plain X_M in shared memory (cfg1 0.031 vs 0.017 ms:
-// a small column is latency-bound on the per-CTA staging and the few tiles).
+// not used: XC through L2 (cfg5 Step 2(b): 39.2 vs 11.9 ms with the looping
+// lookup inside the 32-row pass; 16.6 ms with the straight-line `xc_l2_fast`
+// and the rare long lists patched afterwards -- DM_TPG_XCL2=1) and the plain
+// X_M in shared memory (cfg1 0.031 vs 0.017 ms: a small column is
+// latency-bound on the per-CTA staging and the few tiles).
 // cfg3 (plain X_M through L2): 0.298 vs 0.318 ms.
+#ifndef DM_TPG_XCL2
+#define DM_TPG_XCL2 0  // experiments: XC through L2 (cfg5 Step 2(b) 16.6 vs 11.9 ms, not used)
+#endif
 template <int NB, int XMODE>
 constexpr bool tpg_has() {
-  return NB >= kTpgMinWidth && NB <= 32 && (XMODE == XM_XC_SMEM || XMODE == XM_RAW_GLOBAL);
+  return NB >= kTpgMinWidth && NB <= 32 &&
+         (XMODE == XM_XC_SMEM || XMODE == XM_RAW_GLOBAL || (DM_TPG_XCL2 && XMODE == XM_XC_GLOBAL));
 }
 template <int B, int NB, int XMODE>
 void launch_tpg(const dm_column_in* in, const dm_column_out* out, const uint32_t* xm, const uint32_t* xd,
