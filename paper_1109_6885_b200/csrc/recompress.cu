@@ -669,6 +669,9 @@ template <int B, int NB>
 struct Tpg {
   static constexpr uint32_t slot_bytes = 128u * (B > NB ? B : NB);  // one tile in, then out (in place)
 };
+#ifndef DM_TPG_PATCH
+#define DM_TPG_PATCH 1  // XC in smem: slow rows patched after the pass (1) or a predicated X_M read per row (0)
+#endif
 #ifndef DM_TPG_NOLOOKUP
 #define DM_TPG_NOLOOKUP 0
 #endif
@@ -868,8 +871,8 @@ __global__ void __launch_bounds__(32 * kTpgWarps, 1)
       const uint32_t cc = umin32(c, dict_last);
       bool su;
       const uint32_t v = translate(cc, su);
-      if (XCG) smask |= (uint32_t)su << r;
-      tpg_put<NB>(o, r, (XCS && su) ? __ldg(XM + cc) : v);
+      if (XCG || (XCS && DM_TPG_PATCH)) smask |= (uint32_t)su << r;
+      tpg_put<NB>(o, r, (XCS && !DM_TPG_PATCH && su) ? __ldg(XM + cc) : v);
     }
     if constexpr (NB % 4 == 0) {
       uint4* d = reinterpret_cast<uint4*>(sl + lane * (NB * 4));
@@ -884,7 +887,7 @@ __global__ void __launch_bounds__(32 * kTpgWarps, 1)
 #pragma unroll
       for (int i = 0; i < NB; ++i) d[i] = o[i];
     }
-    if (XCG && smask) {  // rare, per lane: exact values patched into the staged output words
+    if ((XCG || (XCS && DM_TPG_PATCH)) && smask) {  // rare, per lane: exact values patched into the staged output
       uint32_t* ow = reinterpret_cast<uint32_t*>(sl) + lane * NB;
       const uint32_t* M32 = reinterpret_cast<const uint32_t*>(M);
       constexpr uint32_t cmask = B == 32 ? 0xffffffffu : (1u << B) - 1u;
