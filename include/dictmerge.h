@@ -425,8 +425,13 @@ dm_status dm_merge_column_host(dm_ctx* ctx, const dm_column_in* in, dm_column_ou
  *   in registers with compile-time widths; used when b' - b is 0 or 1 and the
  *   plain X_M is whole), 1 the warp-per-group kernel (a lane per row, shuffle
  *   packing) for every width pair.  Same M' either way.
- * The process starts with knobs 0..6 = $DM_XMODE / $DM_MERGE / $DM_DEDUP /
- * $DM_STEP2 / $DM_XC_SHIFT / $DM_SORT1A / $DM_TPG when set (experiments), else 0.
+ * knob 7 = grid of the sparse-delta Step 1(b) kernels (knob 1 = 3), which walk
+ *   U_M tiles t, t + grid, ... and load the next tile while working on the
+ *   current one: 0 (default) one resident wave (SMs x occupancy), 1 one CTA per
+ *   tile, 2 three CTAs (tests).  Same outputs either way.
+ * The process starts with knobs 0..7 = $DM_XMODE / $DM_MERGE / $DM_DEDUP /
+ * $DM_STEP2 / $DM_XC_SHIFT / $DM_SORT1A / $DM_TPG / $DM_SP_GRID when set
+ * (experiments), else 0.
  * Returns DM_OK, or DM_E_INVALID for an unknown knob or value.  Affects calls
  * made after it returns (a captured CUDA graph keeps the kernels it recorded). */
 int dm_set_tuning(int knob, int value);

@@ -184,7 +184,8 @@ def launch_count() -> int:
 
 
 XM_AUTO, XM_PLAIN, XM_COMPACT, XM_COMPACT_L2 = 0, 1, 2, 3
-KNOB_XMODE, KNOB_MERGE, KNOB_DEDUP, KNOB_STEP2, KNOB_XC_SHIFT, KNOB_SORT1A, KNOB_STEP2_FORM = 0, 1, 2, 3, 4, 5, 6
+KNOB_XMODE, KNOB_MERGE, KNOB_DEDUP, KNOB_STEP2, KNOB_XC_SHIFT, KNOB_SORT1A, KNOB_STEP2_FORM, KNOB_SP_GRID = \
+    0, 1, 2, 3, 4, 5, 6, 7
 
 
 def set_tuning(knob: int, value: int) -> None:
@@ -192,7 +193,8 @@ def set_tuning(knob: int, value: int) -> None:
     placement (XM_* above), 1 = Step 1(b) variant, 2 = Step 1(a) dedup front end,
     3 = Step 2 variant (1 = the paper's naive binary-search baseline), 4 = XC
     block shift, 5 = Step 1(a) sort (0 auto, 1 LSD passes, 2 bucket path), 6 =
-    Step 2(b) form with XC in shared memory (0 thread-per-group, 1 warp-per-group).  Never
+    Step 2(b) form with XC in shared memory (0 thread-per-group, 1 warp-per-group), 7 =
+    sparse Step 1(b) grid (0 one resident wave, 1 a CTA per tile, 2 three CTAs).  Never
     changes results; used by tests and experiments to select kernel variants."""
     st = _lib().dm_set_tuning(knob, value)
     if st != Status.OK:

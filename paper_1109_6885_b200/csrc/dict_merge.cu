@@ -639,7 +639,20 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge(const void* __restrict_
 // the new values -- no merge-path ranking of both sides.  A single pass with
 // decoupled look-back was slower (cfg2 0.131 vs 0.100 ms, cfg5 12.3 vs 7.6 ms):
 // the look-back serialised the concurrently resident tiles.
-constexpr uint32_t kSpTile = 2048, kSpThreads = 256, kSpItems = kSpTile / kSpThreads, kSpChunk = 512;
+#ifndef DM_SP_TILE
+#define DM_SP_TILE 2048
+#endif
+constexpr uint32_t kSpTile = DM_SP_TILE, kSpThreads = 256, kSpItems = kSpTile / kSpThreads, kSpChunk = 512;
+static_assert(kSpItems % 4 == 0, "the shift prefix reads 4 positions per 16-byte load");
+
+// Grid of the persistent sparse kernels (knob 7): 0 one resident wave (SMs x
+// occupancy), 1 one CTA per tile (non-persistent), 2 three CTAs (tests: long
+// tile walks).
+unsigned sp_grid(const void* func, size_t smem, uint64_t ntiles) {
+  const int k = tuning(7);
+  const uint64_t g = k == 1 ? ntiles : k == 2 ? 3 : (uint64_t)device_sms() * occupancy(func, kSpThreads, smem);
+  return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(g, ntiles));
+}
 
 template <class KT>
 __global__ void __launch_bounds__(256) k_sp_partition(const void* __restrict__ A, uint64_t nA,
@@ -682,33 +695,49 @@ __global__ void __launch_bounds__(kSpThreads) k_sp_count(const void* __restrict_
   extern __shared__ __align__(16) unsigned char smem_raw[];
   K* sk = reinterpret_cast<K*>(smem_raw);
   __shared__ uint32_t s_warp[NT / 32 + 1];
-  const uint64_t t = blockIdx.x;
-  const uint64_t a = t * T;
-  const uint32_t na = (uint32_t)umin64(T, nA - a);
-  const uint64_t lo = part[t], nb = part[t + 1] - lo;
   // (measured: an evict-last hint here, evict-first / streaming in the write pass,
   // made Step 1(b) slower: cfg2 0.100 -> 0.103 ms, cfg5 7.56 -> 8.81 ms)
+  // Persistent over tiles t = blockIdx.x + k * gridDim.x: the next tile's U_M
+  // values are loaded into registers while the current one is searched, so the
+  // HBM reads of the resident CTAs do not all fall in one phase.
+  K nx[IT];
+  auto fetch = [&](uint64_t tt) {
+    const uint64_t a = tt * T;
+    const uint32_t na = (uint32_t)umin64(T, nA - a);
 #pragma unroll
-  for (uint32_t r = 0; r < IT; ++r) {
-    const uint32_t i = threadIdx.x + r * NT;
-    if (i < na) sk[i] = KT::load(A, a + i);
-  }
-  __syncthreads();
-  uint32_t dups = 0;
-  for (uint64_t j = threadIdx.x; j < nb; j += NT) {
-    const K v = KT::load(B, lo + j);
-    uint32_t l = 0, h = na;  // #{tile A < v}
-    while (l < h) {
-      const uint32_t m = (l + h) >> 1;
-      if (KT::lt(sk[m], v)) l = m + 1; else h = m;
+    for (uint32_t r = 0; r < IT; ++r) {
+      const uint32_t i = threadIdx.x + r * NT;
+      if (i < na) nx[r] = KT::load(A, a + i);
     }
-    const bool found = l < na && KT::eq(sk[l], v);
-    dups += found ? 1u : 0u;
-    pf[lo + j] = l | (found ? 0x80000000u : 0u);
+  };
+  if (blockIdx.x < ntiles) fetch(blockIdx.x);
+  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const uint64_t a = t * T;
+    const uint32_t na = (uint32_t)umin64(T, nA - a);
+    const uint64_t lo = part[t], nb = part[t + 1] - lo;
+#pragma unroll
+    for (uint32_t r = 0; r < IT; ++r) {
+      const uint32_t i = threadIdx.x + r * NT;
+      if (i < na) sk[i] = nx[r];
+    }
+    __syncthreads();
+    if (t + gridDim.x < ntiles) fetch(t + gridDim.x);
+    uint32_t dups = 0;
+    for (uint64_t j = threadIdx.x; j < nb; j += NT) {
+      const K v = KT::load(B, lo + j);
+      uint32_t l = 0, h = na;  // #{tile A < v}
+      while (l < h) {
+        const uint32_t m = (l + h) >> 1;
+        if (KT::lt(sk[m], v)) l = m + 1; else h = m;
+      }
+      const bool found = l < na && KT::eq(sk[l], v);
+      dups += found ? 1u : 0u;
+      pf[lo + j] = l | (found ? 0x80000000u : 0u);
+    }
+    uint32_t tot;
+    block_exclusive_scan<NT>(dups, s_warp, tot);  // ends with a barrier: sk is free again
+    if (threadIdx.x == 0) cnt[t] = tot;
   }
-  uint32_t tot;
-  block_exclusive_scan<NT>(dups, s_warp, tot);
-  if (threadIdx.x == 0) cnt[t] = tot;
 }
 
 // Phase 3: E_t = part[t] - excl[t] new values precede the tile; copy U_M with
@@ -726,98 +755,120 @@ __global__ void __launch_bounds__(kSpThreads) k_sp_write(const void* __restrict_
   pdl_prologue();
   using K = typename KT::K;
   constexpr uint32_t T = kSpTile, NT = kSpThreads, IT = kSpItems, C = kSpChunk, JT = C / NT;
-  __shared__ uint32_t scnt[T + 1];  // cnt[p], then the inclusive shift(i)
+  __shared__ __align__(16) uint32_t scnt[T + 4];  // cnt[p], then the inclusive shift(i)
   __shared__ uint32_t s_warp[NT / 32 + 1];
   const unsigned lane = lane_id();
-  const uint64_t t = blockIdx.x;
-  const uint64_t a = t * T;
-  const uint32_t na = (uint32_t)umin64(T, nA - a);
-  const uint64_t lo = part[t], nb = part[t + 1] - lo;
-  const uint64_t E = lo - excl[t];  // new values of earlier tiles
-  const uint64_t base = a + E;
-  for (uint32_t i = threadIdx.x; i <= T; i += NT) scnt[i] = 0;
-  // the tile's U_M values (registers; the copy needs no staging)
-  K v[IT];
-#pragma unroll
-  for (uint32_t r = 0; r < IT; ++r) {
-    const uint32_t i = threadIdx.x + r * NT;
-    if (i < na) v[r] = KT::load(A, a + i);
-  }
-  __syncthreads();
-  for (uint64_t j = threadIdx.x; j < nb; j += NT) {
-    const uint32_t w = pf[lo + j];
-    if (!(w >> 31)) atomicAdd(&scnt[w], 1u);
-  }
-  __syncthreads();
-  {  // inclusive prefix over positions [0, na)
-    const uint32_t i0 = threadIdx.x * IT;
-    uint32_t c[IT], sum = 0;
+  // Persistent over tiles (as k_sp_count): the next tile's U_M values are loaded
+  // into registers while the current tile is written.
+  K nx[IT];
+  auto fetch = [&](uint64_t tt) {
+    const uint64_t a = tt * T;
+    const uint32_t na = (uint32_t)umin64(T, nA - a);
 #pragma unroll
     for (uint32_t r = 0; r < IT; ++r) {
-      c[r] = i0 + r < na ? scnt[i0 + r] : 0u;
-      sum += c[r];
+      const uint32_t i = threadIdx.x + r * NT;
+      if (i < na) nx[r] = KT::load(A, a + i);
     }
-    uint32_t tot;
-    uint32_t run = block_exclusive_scan<NT>(sum, s_warp, tot);
+  };
+  if (blockIdx.x < ntiles) fetch(blockIdx.x);
+  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const uint64_t a = t * T;
+    const uint32_t na = (uint32_t)umin64(T, nA - a);
+    const uint64_t lo = part[t], nb = part[t + 1] - lo;
+    const uint64_t E = lo - excl[t];  // new values of earlier tiles
+    const uint64_t base = a + E;
+    __syncthreads();  // the previous tile's readers of scnt are done
+    for (uint32_t i = threadIdx.x; i < T / 4 + 1; i += NT) reinterpret_cast<uint4*>(scnt)[i] = make_uint4(0, 0, 0, 0);
+    // the tile's U_M values (registers; the copy needs no staging)
+    K v[IT];
+#pragma unroll
+    for (uint32_t r = 0; r < IT; ++r) v[r] = nx[r];
+    if (t + gridDim.x < ntiles) fetch(t + gridDim.x);
+    __syncthreads();
+    for (uint64_t j = threadIdx.x; j < nb; j += NT) {
+      const uint32_t w = pf[lo + j];
+      if (!(w >> 31)) atomicAdd(&scnt[w], 1u);
+    }
+    __syncthreads();
+    {  // inclusive prefix over positions [0, na); a thread's IT positions as 16-byte
+       // loads / stores (the scalar stride-IT form was an IT-way bank conflict)
+      const uint32_t i0 = threadIdx.x * IT;
+      uint32_t c[IT], sum = 0;
+      uint4* s4 = reinterpret_cast<uint4*>(scnt + i0);
+#pragma unroll
+      for (uint32_t q = 0; q < IT / 4; ++q) {
+        const uint4 x = s4[q];
+        c[4 * q] = x.x; c[4 * q + 1] = x.y; c[4 * q + 2] = x.z; c[4 * q + 3] = x.w;
+      }
+#pragma unroll
+      for (uint32_t r = 0; r < IT; ++r) {
+        if (i0 + r >= na) c[r] = 0u;
+        sum += c[r];
+      }
+      uint32_t tot;
+      uint32_t run = block_exclusive_scan<NT>(sum, s_warp, tot);
+#pragma unroll
+      for (uint32_t r = 0; r < IT; ++r) {
+        run += c[r];
+        c[r] = run;  // positions >= na are never read as shifts
+      }
+#pragma unroll
+      for (uint32_t q = 0; q < IT / 4; ++q) s4[q] = make_uint4(c[4 * q], c[4 * q + 1], c[4 * q + 2], c[4 * q + 3]);
+    }
+    __syncthreads();
+    const uint32_t bmask = (1u << xs) - 1;
+    bool unsorted = false;
 #pragma unroll
     for (uint32_t r = 0; r < IT; ++r) {
-      run += c[r];
-      if (i0 + r < na) scnt[i0 + r] = run;
-    }
-  }
-  __syncthreads();
-  const uint32_t bmask = (1u << xs) - 1;
-  bool unsorted = false;
-#pragma unroll
-  for (uint32_t r = 0; r < IT; ++r) {
-    const uint32_t i = threadIdx.x + r * NT;
-    // predecessor for the sortedness check: the lane below, or a load at warp edges
-    // (every lane shuffles: no lane leaves the loop early)
-    const K prev_l = KT::shfl_up(v[r], 1);
-    if (i >= na) continue;
-    const uint32_t sh = scnt[i];
-    const uint64_t out = base + i + sh;
-    KT::store(U, out, v[r]);
-    if (XM) XM[a + i] = (uint32_t)out;
-    if (rblk) {  // XC block samples R(g) = X_M[2^xs g] - 2^xs g
-      if (((a + i) & bmask) == 0) rblk[(a + i) >> xs] = (uint32_t)(E + sh);
-      if (a + i == nA - 1) rblk[(nA + bmask) >> xs] = (uint32_t)(E + sh);
-    }
-    if (a + i > 0) {
-      const K prev = lane > 0 ? prev_l : KT::load(A, a + i - 1);
-      if (!KT::lt(prev, v[r])) unsorted = true;
-    }
-  }
-  if (__any_sync(FULL, unsorted) && lane == 0) atomicMin(&hdr->status, (int)DM_E_UNSORTED);
-  // the slice: new values into their slots, X_D for all (blocked chunks of C for the new-rank scan)
-  uint32_t run_new = 0;
-  for (uint64_t c0 = 0; c0 < nb; c0 += C) {
-    const uint32_t cn = (uint32_t)umin64(C, nb - c0);
-    const uint32_t j0 = threadIdx.x * JT;
-    uint32_t w[JT], cntn = 0;
-#pragma unroll
-    for (uint32_t r = 0; r < JT; ++r) {
-      w[r] = j0 + r < cn ? pf[lo + c0 + j0 + r] : 0x80000000u;
-      cntn += (w[r] >> 31) ? 0u : 1u;
-    }
-    uint32_t tot;
-    uint32_t nr = run_new + block_exclusive_scan<NT>(cntn, s_warp, tot);
-#pragma unroll
-    for (uint32_t r = 0; r < JT; ++r) {
-      const uint32_t j = j0 + r;
-      if (j >= cn) break;
-      const uint32_t p = w[r] & 0x7fffffffu;
-      if (w[r] >> 31) {  // duplicate: its U_M twin's index
-        XD[lo + c0 + j] = (uint32_t)(base + p + scnt[p]);
-      } else {
-        const uint64_t u = base + p + nr;
-        KT::store(U, u, KT::load(B, lo + c0 + j));
-        XD[lo + c0 + j] = (uint32_t)u;
-        if (offs) offs[E + nr] = (uint8_t)((a + p - 1) & bmask);
-        ++nr;
+      const uint32_t i = threadIdx.x + r * NT;
+      // predecessor for the sortedness check: the lane below, or a load at warp edges
+      // (every lane shuffles: no lane leaves the loop early)
+      const K prev_l = KT::shfl_up(v[r], 1);
+      if (i >= na) continue;
+      const uint32_t sh = scnt[i];
+      const uint64_t out = base + i + sh;
+      KT::store(U, out, v[r]);
+      if (XM) XM[a + i] = (uint32_t)out;
+      if (rblk) {  // XC block samples R(g) = X_M[2^xs g] - 2^xs g
+        if (((a + i) & bmask) == 0) rblk[(a + i) >> xs] = (uint32_t)(E + sh);
+        if (a + i == nA - 1) rblk[(nA + bmask) >> xs] = (uint32_t)(E + sh);
+      }
+      if (a + i > 0) {
+        const K prev = lane > 0 ? prev_l : KT::load(A, a + i - 1);
+        if (!KT::lt(prev, v[r])) unsorted = true;
       }
     }
-    run_new += tot;
+    if (__any_sync(FULL, unsorted) && lane == 0) atomicMin(&hdr->status, (int)DM_E_UNSORTED);
+    // the slice: new values into their slots, X_D for all (blocked chunks of C for the new-rank scan)
+    uint32_t run_new = 0;
+    for (uint64_t c0 = 0; c0 < nb; c0 += C) {
+      const uint32_t cn = (uint32_t)umin64(C, nb - c0);
+      const uint32_t j0 = threadIdx.x * JT;
+      uint32_t w[JT], cntn = 0;
+#pragma unroll
+      for (uint32_t r = 0; r < JT; ++r) {
+        w[r] = j0 + r < cn ? pf[lo + c0 + j0 + r] : 0x80000000u;
+        cntn += (w[r] >> 31) ? 0u : 1u;
+      }
+      uint32_t tot;
+      uint32_t nr = run_new + block_exclusive_scan<NT>(cntn, s_warp, tot);
+#pragma unroll
+      for (uint32_t r = 0; r < JT; ++r) {
+        const uint32_t j = j0 + r;
+        if (j >= cn) break;
+        const uint32_t p = w[r] & 0x7fffffffu;
+        if (w[r] >> 31) {  // duplicate: its U_M twin's index
+          XD[lo + c0 + j] = (uint32_t)(base + p + scnt[p]);
+        } else {
+          const uint64_t u = base + p + nr;
+          KT::store(U, u, KT::load(B, lo + c0 + j));
+          XD[lo + c0 + j] = (uint32_t)u;
+          if (offs) offs[E + nr] = (uint8_t)((a + p - 1) & bmask);
+          ++nr;
+        }
+      }
+      run_new += tot;
+    }
   }
 }
 
@@ -953,11 +1004,15 @@ cudaError_t run(const dm_column_in* in, char* ws, const WsLayout& L, const void*
     launch_k(k_sp_partition<KT>, (unsigned)((ntiles + 1 + 7) / 8), 256, 0, st, in->main_dict, in->dict_len, udict, hdr,
                                                                         ntiles, part);
     uint32_t* pf = reinterpret_cast<uint32_t*>(ws + L.vals0);  // Step 1(a) scratch, free by now (>= N_D u32)
-    launch_k(k_sp_count<KT>, (unsigned)ntiles, kSpThreads, sizeof(K) * kSpTile, st, in->main_dict, in->dict_len, udict,
+    if (sizeof(K) * kSpTile > 48 * 1024) ensure_smem((const void*)k_sp_count<KT>);
+    // persistent grids (sp_grid): every resident CTA walks tiles t, t + grid, ...
+    const unsigned g_count = sp_grid((const void*)k_sp_count<KT>, sizeof(K) * kSpTile, ntiles);
+    const unsigned g_write = sp_grid((const void*)k_sp_write<KT>, 0, ntiles);
+    launch_k(k_sp_count<KT>, g_count, kSpThreads, sizeof(K) * kSpTile, st, in->main_dict, in->dict_len, udict,
                                                               part, ntiles, pf, cnt);
     launch_k(k_scan_counts, (unsigned)((ntiles + 2047) / 2048), 256, 0, st, cnt, ntiles, excl, status, counter,
                                                                   in->dict_len, hdr);
-    launch_k(k_sp_write<KT>, (unsigned)ntiles, kSpThreads, 0, st, in->main_dict, in->dict_len, udict, part, ntiles,
+    launch_k(k_sp_write<KT>, g_write, kSpThreads, 0, st, in->main_dict, in->dict_len, udict, part, ntiles,
                                                               (const uint32_t*)pf, (const uint64_t*)excl, U, xm_w, xd,
                                                               hdr, rblk, offs, xs);
     note_launch(4);

@@ -107,10 +107,10 @@ static int env_knob(const char* name, int hi) {
   const int v = s ? std::atoi(s) : 0;
   return (v >= 0 && v <= hi) ? v : 0;
 }
-static std::atomic<int> g_tuning[7] = {env_knob("DM_XMODE", 3), env_knob("DM_MERGE", 2), env_knob("DM_DEDUP", 2),
+static std::atomic<int> g_tuning[8] = {env_knob("DM_XMODE", 3), env_knob("DM_MERGE", 2), env_knob("DM_DEDUP", 2),
                                        env_knob("DM_STEP2", 1), env_knob("DM_XC_SHIFT", 8), env_knob("DM_SORT1A", 2),
-                                       env_knob("DM_TPG", 1)};
-int tuning(int knob) { return (knob >= 0 && knob < 7) ? g_tuning[knob].load(std::memory_order_relaxed) : 0; }
+                                       env_knob("DM_TPG", 1), env_knob("DM_SP_GRID", 2)};
+int tuning(int knob) { return (knob >= 0 && knob < 8) ? g_tuning[knob].load(std::memory_order_relaxed) : 0; }
 
 static thread_local int t_xc_shift = 0;
 void set_xc_shift_override(int xs) { t_xc_shift = xs; }
@@ -429,14 +429,14 @@ struct dm_ctx {
 extern "C" {
 
 int dm_set_tuning(int knob, int value) {
-  static const int hi[7] = {3, 3, 3, 1, 8, 2, 1};
-  if (knob < 0 || knob > 6 || value < 0 || value > hi[knob]) return DM_E_INVALID;
+  static const int hi[8] = {3, 3, 3, 1, 8, 2, 1, 2};
+  if (knob < 0 || knob > 7 || value < 0 || value > hi[knob]) return DM_E_INVALID;
   if (knob == 4 && value != 0 && value != 7 && value != 8) return DM_E_INVALID;
   g_tuning[knob].store(value);
   return DM_OK;
 }
 
-int dm_get_tuning(int knob) { return (knob >= 0 && knob < 7) ? tuning(knob) : DM_E_INVALID; }
+int dm_get_tuning(int knob) { return (knob >= 0 && knob < 8) ? tuning(knob) : DM_E_INVALID; }
 
 uint32_t dm_width(uint64_t n) { return host_width(n); }
 uint64_t dm_words(uint64_t n, uint32_t bits) { return host_words(n, bits); }

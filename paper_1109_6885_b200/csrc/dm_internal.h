@@ -16,7 +16,10 @@ struct SortShape {
 constexpr SortShape kSortShapes[4] = {{512, 16, 8}, {256, 16, 8}, {256, 8, 4}, {1024, 8, 4}};
 int sort_variant();  // DM_SORT_CFG environment override (experiments), default 0
 uint64_t sort_tile_keys(int key);
-constexpr int kUniqThreads = 512;
+#ifndef DM_UNIQ_THREADS
+#define DM_UNIQ_THREADS 512
+#endif
+constexpr int kUniqThreads = DM_UNIQ_THREADS;
 constexpr int kUniqItems = 8;                            // 4096 per tile
 constexpr int kMergeThreads = 256;
 constexpr int kMergeItems = 8;                           // 2048 merged-diagonal elements per tile

@@ -93,11 +93,11 @@ def test_product_and_oracle_are_separate():
 
 
 def test_tuning_knobs_validated_on_the_host():
-    """dm_set_tuning (include/dictmerge.h): knobs 0..6 with their value ranges;
+    """dm_set_tuning (include/dictmerge.h): knobs 0..7 with their value ranges;
     anything else is DM_E_INVALID.  Pure host logic (no GPU needed)."""
     import paper_1109_6885_b200 as dm
     L = dm._lib()
-    hi = {0: 3, 1: 3, 2: 3, 3: 1, 5: 2, 6: 1}
+    hi = {0: 3, 1: 3, 2: 3, 3: 1, 5: 2, 6: 1, 7: 2}
     try:
         for k, h in hi.items():
             for v in range(h + 1):
@@ -108,10 +108,10 @@ def test_tuning_knobs_validated_on_the_host():
             assert L.dm_set_tuning(4, v) == dm.Status.OK
         for v in (1, 6, 9):
             assert L.dm_set_tuning(4, v) == dm.Status.E_INVALID
-        assert L.dm_set_tuning(7, 0) == dm.Status.E_INVALID
-        assert L.dm_get_tuning(7) == dm.Status.E_INVALID
+        assert L.dm_set_tuning(8, 0) == dm.Status.E_INVALID
+        assert L.dm_get_tuning(8) == dm.Status.E_INVALID
     finally:
-        for k in range(7):
+        for k in range(8):
             L.dm_set_tuning(k, 0)
 
 
@@ -163,4 +163,4 @@ def test_get_tuning_round_trips():
     with dm.tuning(4, 7):
         assert dm.get_tuning(4) == 7
     assert dm.get_tuning(4) == 0
-    assert dm._lib().dm_get_tuning(7) == dm.Status.E_INVALID
+    assert dm._lib().dm_get_tuning(8) == dm.Status.E_INVALID

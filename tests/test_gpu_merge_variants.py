@@ -26,6 +26,7 @@ def _reset():
     yield
     import paper_1109_6885_b200 as dm
     dm.set_tuning(1, 0)
+    dm.set_tuning(dm.KNOB_SP_GRID, 0)
 
 
 CASES = [
@@ -51,6 +52,20 @@ def test_merge_variant(variant, key, case):
     compare(col, M, r)
 
 
+@pytest.mark.parametrize("key", ["u64", "b16", "u32"])
+@pytest.mark.parametrize("case", CASES[:2] + CASES[3:])
+def test_sparse_three_ctas_walk_all_tiles(key, case):
+    """Sparse-delta Step 1(b) with knob 7 = 2: three persistent CTAs walk every
+    U_M tile (the next tile prefetched while one is written)."""
+    import paper_1109_6885_b200 as dm
+    dm.set_tuning(1, 3)
+    dm.set_tuning(dm.KNOB_SP_GRID, 2)
+    n_main, dict_len, n_delta, p_new = case
+    col = datagen.make_random_case(913 + n_delta, n_main, dict_len, n_delta, p_new, key=key)
+    M, r = run_gpu(col)
+    compare(col, M, r)
+
+
 @pytest.mark.parametrize("variant", [0, 1, 2, 3])
 def test_merge_ties_at_every_tile_boundary(variant):
     # U_D = every other U_M value plus values between: duplicates land on both
@@ -67,14 +82,17 @@ def test_merge_ties_at_every_tile_boundary(variant):
     compare(col, M, r)
 
 
+@pytest.mark.parametrize("grid", [0, 1, 2])
 @pytest.mark.parametrize("shape", ["cluster", "all_below", "all_above", "boundaries", "one_tile", "many_chunks"])
-def test_sparse_tiles_edges(shape):
+def test_sparse_tiles_edges(shape, grid):
     """Step 1(b) sparse-delta tiles (knob 1 = 3): slices larger than one 2048-value
     chunk (several passes), every new value below U_M[0] or above U_M[-1], values
     equal to tile-boundary U_M entries (U_M[2048 t]) and their neighbours, a
-    single partial tile."""
+    single partial tile.  Each under the three grids of knob 7 (one resident wave,
+    one CTA per tile, three CTAs walking ~8 tiles each)."""
     import paper_1109_6885_b200 as dm
     dm.set_tuning(1, 3)
+    dm.set_tuning(dm.KNOB_SP_GRID, grid)
     rng = np.random.default_rng(17)
     n_dict = 1500 if shape == "one_tile" else 50_000
     UM = (np.arange(n_dict, dtype=np.uint64) + np.uint64(1)) * np.uint64(1000)
