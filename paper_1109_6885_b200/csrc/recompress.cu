@@ -665,6 +665,23 @@ __global__ void __launch_bounds__(rec_threads<XMODE>(), XMODE == XM_XC_SMEM ? 1 
 // (DM_TPG_NOLOOKUP, timing only) 0.127 ms = 0.79 of the HBM copy peak: the
 // stream is no longer the limit, the ~45 instructions and ~13 shared-memory
 // wavefronts per 32 lookups are.
+#ifndef DM_TPG_DIRECT
+#define DM_TPG_DIRECT 1  // XC in smem: no tile slots -- input words straight into registers, output by 16-byte stores
+#endif
+#ifndef DM_TPG_V8
+#define DM_TPG_V8 0  // direct form: 32-byte global loads / stores when a lane's words are 32-byte aligned
+#endif
+// 256-bit global accesses (sm_100: LDG.E.ENL2.256 / STG.E.ENL2.256)
+__device__ __forceinline__ void ld_v8_na(const void* p, uint32_t* v) {
+  asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "l"(p));
+}
+__device__ __forceinline__ void st_v8_cs(void* p, const uint32_t* v) {
+  asm volatile("st.global.cs.v8.u32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(v[0]), "r"(v[1]),
+               "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
 template <int B, int NB>
 struct Tpg {
   static constexpr uint32_t slot_bytes = 128u * (B > NB ? B : NB);  // one tile in, then out (in place)
@@ -688,7 +705,8 @@ constexpr int kTpgSlots = DM_TPG_SLOTS;
 constexpr int kTpgWarps = DM_TPG_WARPS;
 constexpr int kTpgMinWarps = 4;
 constexpr int kTpgMinWidth = 15;  // XC in shared memory needs |U_M| > 24576
-constexpr int kTpgHdrBytes = 128 + 128 * 8 + 128;  // slot mbarriers, the 128-entry list-mask table, the staging mbarrier
+constexpr int kTpgBarBytes = (kTpgWarps * kTpgSlots * 8 + 127) / 128 * 128;  // slot mbarriers
+constexpr int kTpgHdrBytes = kTpgBarBytes + 128 * 8 + 128;  // slot mbarriers, the 128-entry list-mask table, the staging mbarrier
 
 template <int B>
 __device__ __forceinline__ uint32_t tpg_code(const uint32_t (&w)[B], int r) {
@@ -730,15 +748,18 @@ __global__ void __launch_bounds__(32 * kTpgWarps, 1)
   }
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  static_assert(kTpgWarps * kTpgSlots * 8 <= 128, "mbarriers fit the header");
+  // XC in shared memory: the tiles bypass shared memory (DM_TPG_DIRECT); the
+  // other modes stage them in per-warp slots filled / drained by bulk copies
+  constexpr bool DIR = DM_TPG_DIRECT && XCS;
+
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);          // kTpgWarps x kTpgSlots
-  uint2* lut = reinterpret_cast<uint2*>(smem_raw + 128);            // 128 entries
+  uint2* lut = reinterpret_cast<uint2*>(smem_raw + kTpgBarBytes);   // 128 entries
   uint32_t* sx = reinterpret_cast<uint32_t*>(smem_raw + kTpgHdrBytes);
   const uint64_t table_bytes = XCS ? xc_bytes : XS ? dict_len * 4 : 0;
   const uint32_t slot0 = (uint32_t)((kTpgHdrBytes + table_bytes + 127) & ~127ull);
-  const int W = (int)umin32(blockDim.x >> 5, (smem_bytes - slot0) / (kTpgSlots * T::slot_bytes));
+  const int W = DIR ? (int)(blockDim.x >> 5) : (int)umin32(blockDim.x >> 5, (smem_bytes - slot0) / (kTpgSlots * T::slot_bytes));
 
-  if (threadIdx.x == 0) {
+  if (!DIR && threadIdx.x == 0) {
     for (int i = 0; i < kTpgWarps * kTpgSlots; ++i) mbar_init(&bars[i], 1);
     fence_mbar_init();
   }
@@ -751,7 +772,7 @@ __global__ void __launch_bounds__(32 * kTpgWarps, 1)
     // XC staging: one bulk copy of the records and one of the lists (the global
     // arrays are padded to 16 bytes), then every 8-byte superblock record becomes
     // two 4-byte pair records in place (same size)
-    uint64_t* stage_bar = reinterpret_cast<uint64_t*>(smem_raw + 128 + 128 * 8);
+    uint64_t* stage_bar = reinterpret_cast<uint64_t*>(smem_raw + kTpgBarBytes + 128 * 8);
     if (threadIdx.x == 0) {
       mbar_init(stage_bar, 1);
       fence_mbar_init();
@@ -818,6 +839,95 @@ __global__ void __launch_bounds__(32 * kTpgWarps, 1)
   const unsigned char* Mb = reinterpret_cast<const unsigned char*>(M);
   unsigned char* Ob = reinterpret_cast<unsigned char*>(Mout);
 
+  if constexpr (DIR) {
+  // No slots: a lane's b input words come straight from global memory into
+  // registers (16-byte loads; the next tile's are in flight while this one is
+  // translated) and its b' output words leave by 16-byte streaming stores, so
+  // shared memory holds only the table and the CTA can run more warps.
+  uint32_t wn[B];
+  auto gload = [&](uint64_t t) {
+    const unsigned char* src = Mb + t * (uint64_t)(128 * B) + lane * (B * 4);
+    if constexpr (B % 8 == 0 && DM_TPG_V8) {  // 32-byte loads: every load is one whole sector
+#pragma unroll
+      for (int i = 0; i < B / 8; ++i) ld_v8_na(src + 32 * i, &wn[8 * i]);
+    } else if constexpr (B % 4 == 0) {
+#pragma unroll
+      for (int i = 0; i < B / 4; ++i) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(src) + i);
+        wn[4 * i] = v.x, wn[4 * i + 1] = v.y, wn[4 * i + 2] = v.z, wn[4 * i + 3] = v.w;
+      }
+    } else if constexpr (B % 2 == 0) {
+#pragma unroll
+      for (int i = 0; i < B / 2; ++i) {
+        const uint2 v = __ldg(reinterpret_cast<const uint2*>(src) + i);
+        wn[2 * i] = v.x, wn[2 * i + 1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < B; ++i) wn[i] = __ldg(reinterpret_cast<const uint32_t*>(src) + i);
+    }
+  };
+#ifndef DM_TPG_PREFETCH
+#define DM_TPG_PREFETCH 1  // 0: the tile's words loaded at its start (fewer registers, more warps hide the latency)
+#endif
+  if (DM_TPG_PREFETCH && gw < n_fast) gload(gw);
+  for (uint64_t t = gw; t < n_fast; t += GW) {
+    if (!DM_TPG_PREFETCH) gload(t);
+    uint32_t w[B];
+#pragma unroll
+    for (int i = 0; i < B; ++i) w[i] = wn[i];
+    if (DM_TPG_PREFETCH && t + GW < n_fast) gload(t + GW);
+    uint32_t o[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) o[i] = 0;
+    uint32_t smask = 0;
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      const uint32_t c = tpg_code<B>(w, r);
+      code_max = umax32(code_max, c);
+      const uint32_t cc = umin32(c, dict_last);
+      bool su;
+      const uint32_t v = translate(cc, su);
+      if (XCG || (XCS && DM_TPG_PATCH)) smask |= (uint32_t)su << r;
+      tpg_put<NB>(o, r, (XCS && !DM_TPG_PATCH && su) ? __ldg(XM + cc) : v);
+    }
+    unsigned char* dst = Ob + t * (uint64_t)(128 * NB) + lane * (NB * 4);
+    if constexpr (NB % 8 == 0 && DM_TPG_V8) {
+#pragma unroll
+      for (int i = 0; i < NB / 8; ++i) st_v8_cs(dst + 32 * i, &o[8 * i]);
+    } else if constexpr (NB % 4 == 0) {
+#pragma unroll
+      for (int i = 0; i < NB / 4; ++i)
+        __stcs(reinterpret_cast<uint4*>(dst) + i, make_uint4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]));
+    } else if constexpr (NB % 2 == 0) {
+#pragma unroll
+      for (int i = 0; i < NB / 2; ++i) __stcs(reinterpret_cast<uint2*>(dst) + i, make_uint2(o[2 * i], o[2 * i + 1]));
+    } else {
+#pragma unroll
+      for (int i = 0; i < NB; ++i) __stcs(reinterpret_cast<uint32_t*>(dst) + i, o[i]);
+    }
+    if ((XCG || (XCS && DM_TPG_PATCH)) && smask) {  // rare, per lane: exact values patched into the lane's own words
+      uint32_t* ow = reinterpret_cast<uint32_t*>(dst);
+      const uint32_t* M32 = reinterpret_cast<const uint32_t*>(M);
+      constexpr uint32_t cmask = B == 32 ? 0xffffffffu : (1u << B) - 1u;
+      constexpr uint64_t vmask = NB == 32 ? 0xffffffffull : (1ull << NB) - 1ull;
+      do {
+        const uint32_t r = __ffs(smask) - 1;
+        smask &= smask - 1;
+        const uint64_t bi = ((t * 32 + lane) * 32 + r) * (uint64_t)B;
+        const uint64_t wi = bi >> 5;
+        const uint32_t hi = wi + 1 < 2 * dwords(n_main, B) ? __ldg(M32 + wi + 1) : 0u;
+        const uint32_t c = __funnelshift_r(__ldg(M32 + wi), hi, (uint32_t)(bi & 31)) & cmask;
+        const uint64_t v = exact(umin32(c, dict_last));
+        const uint32_t ob = r * NB, i = ob >> 5, sh = ob & 31;
+        uint64_t x = ow[i] | (i + 1 < (uint32_t)NB ? (uint64_t)ow[i + 1] << 32 : 0ull);
+        x = (x & ~(vmask << sh)) | (v << sh);
+        ow[i] = (uint32_t)x;
+        if (i + 1 < (uint32_t)NB) ow[i + 1] = (uint32_t)(x >> 32);
+      } while (smask);
+    }
+  }
+  } else {
   auto issue = [&](uint64_t t, int k) {
     if (lane == 0) {
       mbar_arrive_expect_tx(&full[k], 128u * B);
@@ -915,6 +1025,7 @@ __global__ void __launch_bounds__(32 * kTpgWarps, 1)
     }
   }
   tma_store_wait_all<0>();
+  }
 
   // tiles holding delta rows or the ragged end: lane l still owns group l, its
   // input words read from global (bounded), every row checked at run time; the
@@ -1093,7 +1204,8 @@ static uint32_t tpg_smem() {
 // XC budget that leaves room for kTpgMinWarps warps' slots (slots: 128 b' bytes for b' - b in {0, 1})
 template <int NB>
 uint32_t tpg_budget() {
-  const int64_t b = (int64_t)tpg_smem() - kTpgHdrBytes - 128 - (int64_t)kTpgMinWarps * kTpgSlots * Tpg<NB, NB>::slot_bytes;
+  const int64_t b = (int64_t)tpg_smem() - kTpgHdrBytes - 128 -
+                    (DM_TPG_DIRECT ? 0 : (int64_t)kTpgMinWarps * kTpgSlots * Tpg<NB, NB>::slot_bytes);
   return b > 0 ? (uint32_t)(b & ~15ll) : 0u;
 }
 // Which (b', mode) pairs use the thread-per-group kernel: XC in shared memory
@@ -1117,7 +1229,7 @@ void launch_tpg(const dm_column_in* in, const dm_column_out* out, const uint32_t
                 const uint32_t* rank, dm_header* hdr, cudaStream_t st, uint32_t fixed_bits, const uint2* xrec,
                 const uint8_t* xoffs, uint32_t budget, uint32_t dens, uint32_t xs) {
   auto kern = k_recompress_tpg<B, NB, XMODE>;
-  constexpr uint32_t slots = kTpgWarps * kTpgSlots * Tpg<B, NB>::slot_bytes;
+  constexpr uint32_t slots = kTpgWarps * kTpgSlots * Tpg<B, NB>::slot_bytes;  // (unused by XC in smem, DM_TPG_DIRECT)
   const uint32_t smem = XMODE == XM_XC_SMEM ? tpg_smem()
                         : XMODE == XM_RAW_SMEM
                             ? (uint32_t)((kTpgHdrBytes + in->dict_len * 4 + 127) & ~127ull) + slots
