@@ -669,7 +669,7 @@ __global__ void __launch_bounds__(rec_threads<XMODE>(), XMODE == XM_XC_SMEM ? 1 
 #define DM_TPG_DIRECT 1  // XC in smem: no tile slots -- input words straight into registers, output by 16-byte stores
 #endif
 #ifndef DM_TPG_V8
-#define DM_TPG_V8 0  // direct form: 32-byte global loads / stores when a lane's words are 32-byte aligned
+#define DM_TPG_V8 1  // direct form: 32-byte global loads / stores when b, b' are multiples of 8 and M, M' are 32-byte aligned (checked at run time: the ABI asks for 16)
 #endif
 // 256-bit global accesses (sm_100: LDG.E.ENL2.256 / STG.E.ENL2.256)
 __device__ __forceinline__ void ld_v8_na(const void* p, uint32_t* v) {
@@ -845,12 +845,19 @@ __global__ void __launch_bounds__(32 * kTpgWarps, 1)
   // translated) and its b' output words leave by 16-byte streaming stores, so
   // shared memory holds only the table and the CTA can run more warps.
   uint32_t wn[B];
+  // 32-byte accesses (every one a whole sector; cfg2 Step 2(b) 0.278 -> 0.275 ms) need M and M'
+  // 32-byte aligned: a tile starts at a multiple of 128 b bytes and a lane's words at 4 b l
+  const bool al32 = ((reinterpret_cast<uintptr_t>(M) | reinterpret_cast<uintptr_t>(Mout)) & 31u) == 0;
   auto gload = [&](uint64_t t) {
     const unsigned char* src = Mb + t * (uint64_t)(128 * B) + lane * (B * 4);
-    if constexpr (B % 8 == 0 && DM_TPG_V8) {  // 32-byte loads: every load is one whole sector
+    if constexpr (B % 8 == 0 && DM_TPG_V8) {
+      if (al32) {
 #pragma unroll
-      for (int i = 0; i < B / 8; ++i) ld_v8_na(src + 32 * i, &wn[8 * i]);
-    } else if constexpr (B % 4 == 0) {
+        for (int i = 0; i < B / 8; ++i) ld_v8_na(src + 32 * i, &wn[8 * i]);
+        return;
+      }
+    }
+    if constexpr (B % 4 == 0) {
 #pragma unroll
       for (int i = 0; i < B / 4; ++i) {
         const uint4 v = __ldg(reinterpret_cast<const uint4*>(src) + i);
@@ -892,9 +899,15 @@ __global__ void __launch_bounds__(32 * kTpgWarps, 1)
       tpg_put<NB>(o, r, (XCS && !DM_TPG_PATCH && su) ? __ldg(XM + cc) : v);
     }
     unsigned char* dst = Ob + t * (uint64_t)(128 * NB) + lane * (NB * 4);
+    bool stored = false;
     if constexpr (NB % 8 == 0 && DM_TPG_V8) {
+      if (al32) {
 #pragma unroll
-      for (int i = 0; i < NB / 8; ++i) st_v8_cs(dst + 32 * i, &o[8 * i]);
+        for (int i = 0; i < NB / 8; ++i) st_v8_cs(dst + 32 * i, &o[8 * i]);
+        stored = true;
+      }
+    }
+    if (stored) {
     } else if constexpr (NB % 4 == 0) {
 #pragma unroll
       for (int i = 0; i < NB / 4; ++i)

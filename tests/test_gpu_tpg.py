@@ -83,3 +83,25 @@ def test_tpg_tiles_and_tails(n_main):
 
 def test_tpg_cfg2_scaled():
     _both_forms(datagen.make_config(2, scale=0.05))
+
+
+@pytest.mark.parametrize("n_dict,n_main", [(60_001, 200_000), (8_500_000, 3_000_007)])
+@pytest.mark.parametrize("offset_words", [0, 2])
+def test_tpg_wide_accesses_and_16_byte_aligned_codes(n_dict, n_main, offset_words):
+    """b = b' = 16 / 24 (multiples of 8): the slot-free kernel moves a lane's words by
+    32-byte accesses when M and M' are 32-byte aligned and by 16-byte ones otherwise
+    (the ABI promises 16: include/dictmerge.h).  M at a 16-byte offset takes the second path;
+    both must give the oracle's M' (Eq 11)."""
+    import paper_1109_6885_b200 as dm
+    from tests.parity import to_device
+    col = _column(n_dict, n_main, _spread(n_dict, max(n_dict // 100, 64), 25), 4000, seed=25)
+    assert col.main_bits in (16, 24)
+    UM, M, D = to_device(col)
+    buf = torch.empty(M.numel() + 4, dtype=M.dtype, device=M.device)
+    Mo = buf[offset_words:offset_words + M.numel()]
+    Mo.copy_(M)
+    assert Mo.data_ptr() % 32 == (16 if offset_words else 0)
+    r = dm.merge_column(UM, Mo, col.n_main, col.main_bits, D, x_tables=True, delta_dict=True)
+    torch.cuda.synchronize()
+    ref = compare(col, M, r)
+    assert ref.merged_bits == col.main_bits
